@@ -1,0 +1,143 @@
+/*
+ * rmat_b200.h -- C ABI of the B200 R-MAT fragment-sampling library
+ * (librmat_b200.so, built from paper_1905_03525_b200/csrc/).
+ *
+ * The boundary replaces the reference's private kernel interface
+ *   _compile(table) -> _Compiled          pkg/src/rmatgen/generator.py:114-130
+ *   _emit(comp, k, count, gen) -> edges,nf pkg/src/rmatgen/generator.py:293-298
+ * and the per-block / per-tile drivers that call it
+ *   generate_result                       generator.py:435-469 (blocks)
+ *   _tile_result / generate_part          partition.py:140-163, 198-222 (tiles)
+ * Plain pointers and sizes only; all device buffers are allocated by the
+ * caller except the table, which the library owns behind an opaque handle.
+ * Every entry point returns an rmat_status (0 = OK) and never throws.
+ * Calls are re-entrant; the library keeps no global mutable state.
+ */
+#ifndef RMAT_B200_H_
+#define RMAT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RMAT_ABI_VERSION 1
+
+typedef enum {
+  RMAT_OK = 0,
+  RMAT_ERR_INVALID = 1,     /* bad argument (null pointer, size, k range ...) */
+  RMAT_ERR_TABLE = 2,       /* table arrays inconsistent (alias out of range, depth 0 ...) */
+  RMAT_ERR_CUDA = 3,        /* a CUDA runtime call failed */
+  RMAT_ERR_UNSUPPORTED = 4, /* combination not supported by any kernel */
+  RMAT_ERR_DEVICE = 5       /* table used on a device other than its own */
+} rmat_status;
+
+typedef struct rmat_table rmat_table; /* opaque; device-resident fragment table */
+
+/* Table description: exactly the reference's `_Compiled` arrays
+ * (generator.py:114-130), host pointers, n entries each. */
+typedef struct {
+  uint64_t n;             /* entries (>= 1) */
+  const uint64_t* thr32;  /* ceil(threshold * 2^32), each in [0, 2^32] */
+  const int64_t* alias;   /* alias index, each in [0, n) */
+  const uint64_t* row;    /* row bits of the fragment, MSB = first level */
+  const uint64_t* col;    /* column bits */
+  const uint64_t* depth;  /* fragment length in levels, each in [1, 62] */
+} rmat_table_desc;
+
+typedef struct {
+  uint64_t n;
+  uint32_t min_depth, max_depth;
+  uint32_t scheme;        /* 1 = P (power-of-two n, one 32-bit word/sample), 0 = G */
+  uint32_t lg;            /* log2(n) when scheme P */
+  uint32_t packed_width;  /* fragment field width of the packed layout: 16, 32, 0 = none */
+  uint32_t packed_smem;   /* 1 if the packed layout fits shared memory */
+  uint64_t packed_bytes;  /* bytes of the packed bucket arrays (what smem must hold) */
+  uint64_t device_bytes;  /* total device bytes owned by the handle */
+  int device;
+} rmat_table_info;
+
+/* Replaces `_compile` (generator.py:114): validates and uploads the table to
+ * `device` (synchronously), building every device layout it is eligible for. */
+rmat_status rmat_table_create(int device, const rmat_table_desc* desc, rmat_table** out);
+rmat_status rmat_table_destroy(rmat_table* table);
+rmat_status rmat_table_get_info(const rmat_table* table, rmat_table_info* info);
+
+/* One segment = a run of streams that share prefixes: a slice of generate()'s
+ * block streams, or one tile of the partitioned mode.  Local stream j of the
+ * segment uses stream id sid_base + j and writes rows
+ * [out_row + j*E, out_row + j*E + min(E, edge_count - j*E)). */
+typedef struct {
+  uint64_t sid_base;
+  uint64_t edge_count;
+  uint64_t out_row;
+  uint64_t row_prefix;  /* OR'd into every row endpoint (tile prefix, else 0) */
+  uint64_t col_prefix;
+} rmat_segment;
+
+typedef enum {
+  RMAT_KERNEL_AUTO = 0,
+  RMAT_KERNEL_PACKED_SMEM = 1,   /* packed buckets staged in shared memory */
+  RMAT_KERNEL_PACKED_GLOBAL = 2, /* packed buckets read through L1/L2 */
+  RMAT_KERNEL_GENERIC = 3        /* any table, k <= 62, 128-bit accumulators */
+} rmat_kernel;
+
+typedef struct {
+  const rmat_table* table;
+  uint32_t k;                 /* bits per endpoint produced by the stream (k - t for tiles) */
+  uint32_t out_width;         /* bytes per endpoint in `out`: 4 or 8 */
+  uint64_t seed;
+  uint64_t domain;            /* key = seed ^ domain */
+  uint64_t edges_per_stream;  /* E >= 1 */
+  const rmat_segment* segments; /* host array */
+  uint32_t n_segments;
+  void* out;                  /* device, rows x 2 endpoints of out_width bytes */
+  uint64_t out_rows;          /* capacity of `out` in rows (bounds check) */
+  uint64_t* samples_total;    /* device, optional: += samples consumed (atomic) */
+  uint64_t* samples_per_stream; /* device, optional: nf of every stream, global stream order */
+  int kernel;                 /* rmat_kernel; AUTO picks the fastest eligible */
+  int* kernel_used;           /* host, optional: receives the variant launched */
+} rmat_gen_args;
+
+/* Replaces the `_emit` loop over blocks / tiles (generator.py:447-456,
+ * partition.py:211-219).  Asynchronous on `cuda_stream` (a cudaStream_t). */
+rmat_status rmat_generate(const rmat_gen_args* args, void* cuda_stream);
+
+/* Oracle-mode support (K1-dump): the 64-bit replay words that stream `sid`
+ * feeds the reference's `_select` (generator.py:133-142) for samples
+ * [start, start+count), written to device memory `out`. */
+rmat_status rmat_replay_words(const rmat_table* table, uint64_t seed, uint64_t domain,
+                              uint64_t sid, uint64_t start, uint64_t count, uint64_t* out,
+                              void* cuda_stream);
+
+/* Reference-stream mode: bit-identical to rmatgen.generate (numpy Philox4x64-10
+ * block streams keyed [seed ^ domain, first_block + b], generator.py:435-456).
+ * Blocks b in [0, n_blocks), block b writes rows [b*B, b*B + count_b),
+ * count_b = min(B, edge_count - (first_block+b)*B) relative to the whole run. */
+typedef struct {
+  const rmat_table* table;
+  uint32_t k;
+  uint32_t out_width;         /* 4 or 8 */
+  uint64_t seed;
+  uint64_t domain;
+  uint64_t block_size;        /* B */
+  uint64_t edge_count;        /* m of the whole run */
+  uint64_t first_block;
+  uint64_t n_blocks;
+  void* out;                  /* device; row 0 = first row of first_block */
+  uint64_t* samples_per_block; /* device, optional */
+  uint64_t* samples_total;    /* device, optional */
+} rmat_refstream_args;
+
+rmat_status rmat_generate_refstream(const rmat_refstream_args* args, void* cuda_stream);
+
+const char* rmat_strerror(rmat_status status);
+int rmat_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RMAT_B200_H_ */

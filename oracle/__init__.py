@@ -1,0 +1,201 @@
+"""CPU ORACLE for the R-MAT sampling path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs import this package, and only as the checker.
+The product (paper_1905_03525_b200/) never imports it; its CUDA path fails
+loudly instead of falling back here.
+
+Contents
+  * ctypes bindings to rmat_oracle.c, a plain-C restatement of the
+    reference's emission loop (reference pkg/src/rmatgen/generator.py:324-356)
+    and alias select (generator.py:133-142), plus the two counter RNGs:
+    the fast path's Philox4x32-10 stream spec and numpy's Philox4x64-10
+    (reference _rng.py:25-38);
+  * `refport` -- a numpy restatement of the reference's vectorised CPU
+    generator (generator.py:114-298, 435-469) used as the CPU baseline.
+
+Pinning: tests/test_oracle.py checks this oracle against fixtures produced by
+running the reference itself (tests/golden/make_golden.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from functools import lru_cache
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "_build", "liboracle.so")
+
+DOMAIN_BLOCK = 0x9E3779B97F4A7C15  # reference _rng.py:18
+DOMAIN_NODE = 0xBF58476D1CE4E5B9
+DOMAIN_TILE = 0x94D049BB133111EB
+M64 = (1 << 64) - 1
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+
+
+def build(force: bool = False) -> str:
+    """Compile rmat_oracle.c into oracle/_build/liboracle.so (gcc)."""
+    src = os.path.join(_HERE, "rmat_oracle.c")
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB
+
+
+@lru_cache(maxsize=1)
+def lib() -> ctypes.CDLL:
+    build()
+    L = ctypes.CDLL(_LIB)
+    T = [ctypes.c_uint64, _u64p, _i64p, _u64p, _u64p, _u64p]
+    L.oracle_philox4x32_10.argtypes = [_u32p, _u32p, _u32p]
+    L.oracle_philox4x64_10.argtypes = [_u64p, _u64p, _u64p]
+    L.oracle_fast_word.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64,
+                                   ctypes.c_uint64, ctypes.c_uint64]
+    L.oracle_fast_word.restype = ctypes.c_uint64
+    L.oracle_fast_words.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64,
+                                    ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p]
+    L.oracle_ref_words.argtypes = [ctypes.c_uint64] * 4 + [_u64p]
+    L.oracle_emit.argtypes = T + [ctypes.c_uint32, ctypes.c_uint64, _u64p, ctypes.c_uint64, _u64p]
+    L.oracle_emit.restype = ctypes.c_int64
+    L.oracle_fast_stream.argtypes = T + [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int,
+                                         ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                         ctypes.c_uint64, ctypes.c_uint64, _u64p]
+    L.oracle_fast_stream.restype = ctypes.c_int64
+    L.oracle_ref_stream.argtypes = T + [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                        ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p]
+    L.oracle_ref_stream.restype = ctypes.c_int64
+    return L
+
+
+def _p(a: np.ndarray, ptype):
+    assert a.flags.c_contiguous
+    return a.ctypes.data_as(ptype)
+
+
+class OracleTable:
+    """The compiled arrays the reference's kernels read (generator.py:114-130)."""
+
+    def __init__(self, thr32, alias, row, col, depth):
+        self.thr32 = np.ascontiguousarray(thr32, dtype=np.uint64)
+        self.alias = np.ascontiguousarray(alias, dtype=np.int64)
+        self.row = np.ascontiguousarray(row, dtype=np.uint64)
+        self.col = np.ascontiguousarray(col, dtype=np.uint64)
+        self.depth = np.ascontiguousarray(depth, dtype=np.uint64)
+        self.n = int(self.thr32.shape[0])
+
+    @classmethod
+    def from_fragment_table(cls, table) -> "OracleTable":
+        """From any object with .sampler.threshold/.alias and .row_bits/.col_bits/.depths."""
+        thr32 = np.ceil(np.asarray(table.sampler.threshold) * 2.0**32).astype(np.uint64)
+        return cls(thr32, table.sampler.alias, table.row_bits, table.col_bits, table.depths)
+
+    def args(self):
+        return (self.n, _p(self.thr32, _u64p), _p(self.alias, _i64p), _p(self.row, _u64p),
+                _p(self.col, _u64p), _p(self.depth, _u64p))
+
+    @property
+    def scheme_p(self) -> bool:
+        n = self.n
+        return n & (n - 1) == 0 and 2 <= n.bit_length() - 1 <= 24
+
+    @property
+    def lg(self) -> int:
+        return self.n.bit_length() - 1
+
+
+def philox4x32(ctr, key) -> np.ndarray:
+    c = np.asarray(ctr, dtype=np.uint32)
+    k = np.asarray(key, dtype=np.uint32)
+    o = np.zeros(4, dtype=np.uint32)
+    lib().oracle_philox4x32_10(_p(c, _u32p), _p(k, _u32p), _p(o, _u32p))
+    return o
+
+
+def philox4x64(ctr, key) -> np.ndarray:
+    c = np.asarray(ctr, dtype=np.uint64)
+    k = np.asarray(key, dtype=np.uint64)
+    o = np.zeros(4, dtype=np.uint64)
+    lib().oracle_philox4x64_10(_p(c, _u64p), _p(k, _u64p), _p(o, _u64p))
+    return o
+
+
+def fast_words(table: OracleTable, seed: int, domain: int, sid: int, count: int,
+               start: int = 0) -> np.ndarray:
+    out = np.empty(count, dtype=np.uint64)
+    lib().oracle_fast_words(int(table.scheme_p), table.lg, (seed ^ domain) & M64, sid & M64,
+                            start, count, _p(out, _u64p))
+    return out
+
+
+def ref_words(key0: int, key1: int, count: int, start: int = 0) -> np.ndarray:
+    out = np.empty(count, dtype=np.uint64)
+    lib().oracle_ref_words(key0 & M64, key1 & M64, start, count, _p(out, _u64p))
+    return out
+
+
+def emit(table: OracleTable, k: int, count: int, words: np.ndarray) -> tuple[np.ndarray, int]:
+    """Replay `words` through the normative emission loop -> ((count,2) uint64, nf)."""
+    words = np.ascontiguousarray(words, dtype=np.uint64)
+    out = np.zeros((count, 2), dtype=np.uint64)
+    nf = lib().oracle_emit(*table.args(), k, count, _p(words, _u64p), words.shape[0],
+                           _p(out, _u64p))
+    if nf < 0:
+        raise ValueError("replay words ran out before count edges were emitted")
+    return out, int(nf)
+
+
+def fast_stream(table: OracleTable, k: int, count: int, seed: int, sid: int,
+                domain: int = DOMAIN_BLOCK, row_prefix: int = 0, col_prefix: int = 0):
+    """Edges of one fast-path stream (the GPU kernel's exact semantics) -> (edges, nf)."""
+    out = np.zeros((count, 2), dtype=np.uint64)
+    nf = lib().oracle_fast_stream(*table.args(), k, count, int(table.scheme_p), table.lg,
+                                  (seed ^ domain) & M64, sid & M64, row_prefix, col_prefix,
+                                  _p(out, _u64p))
+    return out, int(nf)
+
+
+def ref_stream(table: OracleTable, k: int, count: int, key0: int, key1: int,
+               row_prefix: int = 0, col_prefix: int = 0):
+    """Edges of one reference (numpy Philox) stream -> (edges, nf)."""
+    out = np.zeros((count, 2), dtype=np.uint64)
+    nf = lib().oracle_ref_stream(*table.args(), k, count, key0 & M64, key1 & M64, row_prefix,
+                                 col_prefix, _p(out, _u64p))
+    return out, int(nf)
+
+
+def ref_block(table: OracleTable, k: int, count: int, seed: int, block: int):
+    """Reference emit_block(table, k, count, (seed, block)) (generator.py:306-321)."""
+    return ref_stream(table, k, count, (seed ^ DOMAIN_BLOCK) & M64, block)
+
+
+def fast_generate(table: OracleTable, k: int, m: int, seed: int, edges_per_stream: int,
+                  first_stream: int = 0):
+    """Fast-path generate(): stream s owns rows [s*E, s*E+count_s) -> (edges, samples)."""
+    out = np.empty((m, 2), dtype=np.uint64)
+    E = edges_per_stream
+    total = 0
+    for s in range((m + E - 1) // E):
+        cnt = min(E, m - s * E)
+        e, nf = fast_stream(table, k, cnt, seed, first_stream + s)
+        out[s * E: s * E + cnt] = e
+        total += nf
+    return out, total
+
+
+def ref_generate(table: OracleTable, k: int, m: int, seed: int, block_size: int = 1 << 16):
+    """Reference generate_result() semantics (generator.py:435-456) -> (edges, samples)."""
+    out = np.empty((m, 2), dtype=np.uint64)
+    B = block_size
+    total = 0
+    for b in range((m + B - 1) // B):
+        cnt = min(B, m - b * B)
+        e, nf = ref_block(table, k, cnt, seed, b)
+        out[b * B: b * B + cnt] = e
+        total += nf
+    return out, total

@@ -1,0 +1,141 @@
+"""ctypes binding of librmat_b200.so (include/rmat_b200.h).
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, every generating call raises NativeUnavailable.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from functools import lru_cache
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "_build", "librmat_b200.so")
+_SOURCES = [os.path.join(_PKG, "csrc", f) for f in
+            ("rmat_capi.cu", "rmat_kernels.cuh", "rmat_refstream.cuh", "rmat_device.cuh",
+             "philox.cuh")] + [os.path.join(_ROOT, "include", "rmat_b200.h")]
+
+NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
+              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library or a CUDA device is not available."""
+
+
+class NativeError(RuntimeError):
+    """A C-ABI call returned a non-zero rmat_status."""
+
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {strerror(status)} (status {status})")
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/ into _build/librmat_b200.so for sm_100a with nvcc."""
+    newest = max(os.path.getmtime(p) for p in _SOURCES)
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
+        return LIB_PATH
+    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
+    tmp = LIB_PATH + ".tmp"
+    cmd = ["nvcc", *NVCC_FLAGS, os.path.join(_PKG, "csrc", "rmat_capi.cu"), "-o", tmp]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed:\n{res.stderr}")
+    if verbose:
+        print(res.stderr)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+# ---- ABI structs (must match include/rmat_b200.h) ----
+class TableDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("thr32", ctypes.c_void_p), ("alias", ctypes.c_void_p),
+                ("row", ctypes.c_void_p), ("col", ctypes.c_void_p), ("depth", ctypes.c_void_p)]
+
+
+class TableInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("min_depth", ctypes.c_uint32),
+                ("max_depth", ctypes.c_uint32), ("scheme", ctypes.c_uint32),
+                ("lg", ctypes.c_uint32), ("packed_width", ctypes.c_uint32),
+                ("packed_smem", ctypes.c_uint32), ("packed_bytes", ctypes.c_uint64),
+                ("device_bytes", ctypes.c_uint64), ("device", ctypes.c_int)]
+
+
+class Segment(ctypes.Structure):
+    _fields_ = [("sid_base", ctypes.c_uint64), ("edge_count", ctypes.c_uint64),
+                ("out_row", ctypes.c_uint64), ("row_prefix", ctypes.c_uint64),
+                ("col_prefix", ctypes.c_uint64)]
+
+
+class GenArgs(ctypes.Structure):
+    _fields_ = [("table", ctypes.c_void_p), ("k", ctypes.c_uint32),
+                ("out_width", ctypes.c_uint32), ("seed", ctypes.c_uint64),
+                ("domain", ctypes.c_uint64), ("edges_per_stream", ctypes.c_uint64),
+                ("segments", ctypes.POINTER(Segment)), ("n_segments", ctypes.c_uint32),
+                ("out", ctypes.c_void_p), ("out_rows", ctypes.c_uint64),
+                ("samples_total", ctypes.c_void_p), ("samples_per_stream", ctypes.c_void_p),
+                ("kernel", ctypes.c_int), ("kernel_used", ctypes.POINTER(ctypes.c_int))]
+
+
+class RefArgs(ctypes.Structure):
+    _fields_ = [("table", ctypes.c_void_p), ("k", ctypes.c_uint32),
+                ("out_width", ctypes.c_uint32), ("seed", ctypes.c_uint64),
+                ("domain", ctypes.c_uint64), ("block_size", ctypes.c_uint64),
+                ("edge_count", ctypes.c_uint64), ("first_block", ctypes.c_uint64),
+                ("n_blocks", ctypes.c_uint64), ("out", ctypes.c_void_p),
+                ("samples_per_block", ctypes.c_void_p), ("samples_total", ctypes.c_void_p)]
+
+
+KERNEL_AUTO, KERNEL_PACKED_SMEM, KERNEL_PACKED_GLOBAL, KERNEL_GENERIC = 0, 1, 2, 3
+KERNEL_NAMES = {1: "packed_smem", 2: "packed_global", 3: "generic"}
+
+#: symbols include/rmat_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
+           "rmat_replay_words", "rmat_generate_refstream", "rmat_strerror", "rmat_abi_version")
+
+
+@lru_cache(maxsize=1)
+def lib() -> ctypes.CDLL:
+    """Load (building first if stale) the library; raise NativeUnavailable on failure."""
+    try:
+        path = build()
+    except (OSError, RuntimeError) as exc:
+        if not os.path.exists(LIB_PATH):
+            raise NativeUnavailable(f"cannot build {LIB_PATH}: {exc}") from exc
+        path = LIB_PATH
+    try:
+        L = ctypes.CDLL(path)
+    except OSError as exc:
+        raise NativeUnavailable(f"cannot load {path}: {exc}") from exc
+    vp = ctypes.c_void_p
+    L.rmat_table_create.argtypes = [ctypes.c_int, ctypes.POINTER(TableDesc),
+                                    ctypes.POINTER(ctypes.c_void_p)]
+    L.rmat_table_destroy.argtypes = [vp]
+    L.rmat_table_get_info.argtypes = [vp, ctypes.POINTER(TableInfo)]
+    L.rmat_generate.argtypes = [ctypes.POINTER(GenArgs), vp]
+    L.rmat_replay_words.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                    ctypes.c_uint64, ctypes.c_uint64, vp, vp]
+    L.rmat_generate_refstream.argtypes = [ctypes.POINTER(RefArgs), vp]
+    L.rmat_strerror.argtypes = [ctypes.c_int]
+    L.rmat_strerror.restype = ctypes.c_char_p
+    L.rmat_abi_version.restype = ctypes.c_int
+    for f in ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
+              "rmat_replay_words", "rmat_generate_refstream"):
+        getattr(L, f).restype = ctypes.c_int
+    return L
+
+
+def strerror(status: int) -> str:
+    try:
+        return lib().rmat_strerror(status).decode()
+    except NativeUnavailable:
+        return "unknown"
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        raise NativeError(status, what)

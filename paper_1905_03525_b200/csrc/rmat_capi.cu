@@ -1,0 +1,431 @@
+// extern "C" boundary of librmat_b200.so (see include/rmat_b200.h).
+//
+// Host-side native code: table validation + device packing (the device half
+// of the reference's `_compile`, generator.py:114-130) and kernel dispatch
+// (the block / tile loops of generator.py:447-456 and partition.py:211-219).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/rmat_b200.h"
+#include "philox.cuh"
+#include "rmat_device.cuh"
+#include "rmat_kernels.cuh"
+#include "rmat_refstream.cuh"
+
+struct rmat_table {
+  int device;
+  uint64_t n;
+  uint32_t dmin, dmax;
+  uint32_t scheme_p, lg;
+  // generic layout
+  uint32_t* T;
+  uint32_t* alias;
+  uint64_t* row;
+  uint64_t* col;
+  uint8_t* depth;
+  // packed layout (optional)
+  uint32_t fb;  // 0 = absent
+  uint32_t* pB;
+  void* pA;
+  uint32_t* ptlo;
+  uint64_t packed_bytes;
+  uint32_t packed_smem;
+  uint64_t device_bytes;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) return;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+rmat_status upload(const std::vector<T>& h, T** d, uint64_t* bytes) {
+  size_t nb = h.size() * sizeof(T);
+  if (cudaMalloc(reinterpret_cast<void**>(d), std::max<size_t>(nb, 16)) != cudaSuccess)
+    return RMAT_ERR_CUDA;
+  if (cudaMemcpy(*d, h.data(), nb, cudaMemcpyHostToDevice) != cudaSuccess) return RMAT_ERR_CUDA;
+  *bytes += nb;
+  return RMAT_OK;
+}
+
+void free_table(rmat_table* t) {
+  if (!t) return;
+  cudaFree(t->T);
+  cudaFree(t->alias);
+  cudaFree(t->row);
+  cudaFree(t->col);
+  cudaFree(t->depth);
+  cudaFree(t->pB);
+  cudaFree(t->pA);
+  cudaFree(t->ptlo);
+  delete t;
+}
+
+int max_smem_optin(int dev) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v;
+}
+
+int num_sms(int dev) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
+
+rmat::PackedTab packed_view(const rmat_table* t) {
+  rmat::PackedTab p;
+  p.B = t->pB;
+  p.A = t->pA;
+  p.tlo = t->ptlo;
+  p.idxmask4 = (uint32_t)((t->n - 1) << 2);
+  p.fm = (1u << rmat::scheme_p_fbits(t->lg)) - 1u;
+  p.n = (uint32_t)t->n;
+  p.fb = t->fb;
+  return p;
+}
+
+rmat::GenericTab generic_view(const rmat_table* t) {
+  rmat::GenericTab g;
+  g.T = t->T;
+  g.alias = t->alias;
+  g.row = t->row;
+  g.col = t->col;
+  g.depth = t->depth;
+  g.n = (uint32_t)t->n;
+  g.scheme_p = t->scheme_p;
+  g.lg = t->lg;
+  return g;
+}
+
+template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT>
+rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT>;
+  const int sms = num_sms(t->device);
+  int threads, blocks;
+  size_t smem = 0;
+  if (SMEM) {
+    smem = t->packed_bytes;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return RMAT_ERR_CUDA;
+    threads = 1024;
+    blocks = sms;
+  } else {
+    threads = 256;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess)
+      return RMAT_ERR_CUDA;
+    blocks = sms * std::max(per_sm, 1);
+  }
+  uint64_t need = (g.total_streams + threads - 1) / threads;
+  blocks = (int)std::min<uint64_t>((uint64_t)blocks, std::max<uint64_t>(need, 1));
+  kern<<<blocks, threads, smem, st>>>(packed_view(t), g);
+  return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+}
+
+template <int FB, bool SMEM>
+rmat_status launch_packed_fb(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
+                             bool count, cudaStream_t st) {
+  if (out64) {
+    if (prefix)
+      return count ? launch_packed_t<FB, SMEM, true, true, true>(t, g, st)
+                   : launch_packed_t<FB, SMEM, true, true, false>(t, g, st);
+    return count ? launch_packed_t<FB, SMEM, true, false, true>(t, g, st)
+                 : launch_packed_t<FB, SMEM, true, false, false>(t, g, st);
+  }
+  if (prefix)
+    return count ? launch_packed_t<FB, SMEM, false, true, true>(t, g, st)
+                 : launch_packed_t<FB, SMEM, false, true, false>(t, g, st);
+  return count ? launch_packed_t<FB, SMEM, false, false, true>(t, g, st)
+               : launch_packed_t<FB, SMEM, false, false, false>(t, g, st);
+}
+
+rmat_status launch_generic(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
+                           cudaStream_t st) {
+  const int threads = 256;
+  const int sms = num_sms(t->device);
+  uint64_t need = (g.total_streams + threads - 1) / threads;
+  int blocks = (int)std::min<uint64_t>((uint64_t)sms * 8, std::max<uint64_t>(need, 1));
+  if (out64)
+    rmat::k_generic<true><<<blocks, threads, 0, st>>>(generic_view(t), g);
+  else
+    rmat::k_generic<false><<<blocks, threads, 0, st>>>(generic_view(t), g);
+  return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rmat_abi_version(void) { return RMAT_ABI_VERSION; }
+
+const char* rmat_strerror(rmat_status s) {
+  switch (s) {
+    case RMAT_OK: return "ok";
+    case RMAT_ERR_INVALID: return "invalid argument";
+    case RMAT_ERR_TABLE: return "inconsistent fragment table";
+    case RMAT_ERR_CUDA: return "CUDA runtime error";
+    case RMAT_ERR_UNSUPPORTED: return "unsupported configuration";
+    case RMAT_ERR_DEVICE: return "table belongs to another device";
+  }
+  return "unknown status";
+}
+
+rmat_status rmat_table_create(int device, const rmat_table_desc* d, rmat_table** out) {
+  if (!d || !out || d->n == 0 || d->n > (1ull << 31) || !d->thr32 || !d->alias || !d->row ||
+      !d->col || !d->depth)
+    return RMAT_ERR_INVALID;
+  *out = nullptr;
+  const uint64_t n = d->n;
+  uint32_t dmin = 63, dmax = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t dep = d->depth[i];
+    if (dep < 1 || dep > 62) return RMAT_ERR_TABLE;
+    if (d->alias[i] < 0 || (uint64_t)d->alias[i] >= n) return RMAT_ERR_TABLE;
+    if (d->thr32[i] > (1ull << 32)) return RMAT_ERR_TABLE;
+    if ((d->row[i] >> dep) != 0 || (d->col[i] >> dep) != 0) return RMAT_ERR_TABLE;
+    dmin = std::min<uint32_t>(dmin, (uint32_t)dep);
+    dmax = std::max<uint32_t>(dmax, (uint32_t)dep);
+  }
+  rmat_table* t = new (std::nothrow) rmat_table();
+  if (!t) return RMAT_ERR_CUDA;
+  t->device = device;
+  t->n = n;
+  t->dmin = dmin;
+  t->dmax = dmax;
+  const bool pow2 = (n & (n - 1)) == 0;
+  uint32_t lg = 0;
+  while ((1ull << lg) < n) ++lg;
+  t->scheme_p = (pow2 && lg >= 2 && lg <= 24) ? 1u : 0u;
+  t->lg = lg;
+
+  DeviceGuard guard(device);
+  if (!guard.ok) { delete t; return RMAT_ERR_DEVICE; }
+
+  // Exact 32-bit form of the acceptance test: thr32 == 2^32 always accepts,
+  // which equals "threshold 0xFFFFFFFF, alias = self" for every fraction.
+  std::vector<uint32_t> T(n), al(n);
+  std::vector<uint64_t> row(d->row, d->row + n), col(d->col, d->col + n);
+  std::vector<uint8_t> dep(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    const bool full = d->thr32[i] == (1ull << 32);
+    T[i] = full ? 0xFFFFFFFFu : (uint32_t)d->thr32[i];
+    al[i] = full ? (uint32_t)i : (uint32_t)d->alias[i];
+    dep[i] = (uint8_t)d->depth[i];
+  }
+  rmat_status st = RMAT_OK;
+  uint64_t bytes = 0;
+  if ((st = upload(T, &t->T, &bytes)) || (st = upload(al, &t->alias, &bytes)) ||
+      (st = upload(row, &t->row, &bytes)) || (st = upload(col, &t->col, &bytes)) ||
+      (st = upload(dep, &t->depth, &bytes))) {
+    free_table(t);
+    return st;
+  }
+
+  // Packed bucket layout (scheme P; see rmat_device.cuh).
+  uint32_t fb = 0;
+  if (t->scheme_p && lg >= 2 && dmax <= 16) fb = 16;
+  else if (t->scheme_p && dmax <= 31) fb = 32;
+  if (fb) {
+    const uint32_t fm = (1u << rmat::scheme_p_fbits(lg)) - 1u;
+    std::vector<uint32_t> B(n), tlo(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint32_t a = al[i];
+      B[i] = (T[i] & ~fm) | (uint32_t)dep[i] | ((uint32_t)dep[a] << 8);
+      tlo[i] = T[i] & fm;
+    }
+    if ((st = upload(B, &t->pB, &bytes)) || (st = upload(tlo, &t->ptlo, &bytes))) {
+      free_table(t);
+      return st;
+    }
+    if (fb == 16) {
+      std::vector<uint2> A(n);
+      for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t a = al[i];
+        A[i].x = (uint32_t)row[i] | ((uint32_t)row[a] << 16);
+        A[i].y = (uint32_t)col[i] | ((uint32_t)col[a] << 16);
+      }
+      uint2* dA = nullptr;
+      st = upload(A, &dA, &bytes);
+      t->pA = dA;
+    } else {
+      std::vector<uint4> A(n);
+      for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t a = al[i];
+        A[i] = make_uint4((uint32_t)row[i], (uint32_t)row[a], (uint32_t)col[i], (uint32_t)col[a]);
+      }
+      uint4* dA = nullptr;
+      st = upload(A, &dA, &bytes);
+      t->pA = dA;
+    }
+    if (st) { free_table(t); return st; }
+    t->fb = fb;
+    t->packed_bytes = n * (fb == 16 ? 12ull : 20ull);
+    t->packed_smem = t->packed_bytes <= (uint64_t)max_smem_optin(device) ? 1u : 0u;
+  }
+  t->device_bytes = bytes;
+  *out = t;
+  return RMAT_OK;
+}
+
+rmat_status rmat_table_destroy(rmat_table* t) {
+  if (!t) return RMAT_ERR_INVALID;
+  DeviceGuard guard(t->device);
+  free_table(t);
+  return RMAT_OK;
+}
+
+rmat_status rmat_table_get_info(const rmat_table* t, rmat_table_info* info) {
+  if (!t || !info) return RMAT_ERR_INVALID;
+  info->n = t->n;
+  info->min_depth = t->dmin;
+  info->max_depth = t->dmax;
+  info->scheme = t->scheme_p;
+  info->lg = t->lg;
+  info->packed_width = t->fb;
+  info->packed_smem = t->packed_smem;
+  info->packed_bytes = t->packed_bytes;
+  info->device_bytes = t->device_bytes;
+  info->device = t->device;
+  return RMAT_OK;
+}
+
+rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
+  if (!a || !a->table || a->k < 1 || a->k > 62 || (a->out_width != 4 && a->out_width != 8) ||
+      a->edges_per_stream < 1 || (a->n_segments && !a->segments))
+    return RMAT_ERR_INVALID;
+  const rmat_table* t = a->table;
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) return RMAT_ERR_CUDA;
+  DeviceGuard guard(t->device);
+  if (!guard.ok) return RMAT_ERR_DEVICE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+
+  // Validate segments: rows in bounds, values representable in out_width.
+  const uint64_t E = a->edges_per_stream;
+  const uint64_t kmask = (a->k >= 64) ? ~0ull : ((1ull << a->k) - 1);
+  bool prefix = false;
+  uint64_t streams_total = 0;
+  for (uint32_t i = 0; i < a->n_segments; ++i) {
+    const rmat_segment& s = a->segments[i];
+    if (s.edge_count > a->out_rows || s.out_row > a->out_rows - s.edge_count)
+      return RMAT_ERR_INVALID;
+    if ((s.row_prefix & kmask) || (s.col_prefix & kmask)) return RMAT_ERR_INVALID;
+    const uint64_t top = s.row_prefix | s.col_prefix | kmask;
+    if (a->out_width == 4 && (top >> 32)) return RMAT_ERR_INVALID;
+    prefix = prefix || s.row_prefix || s.col_prefix;
+    streams_total += (s.edge_count + E - 1) / E;
+  }
+  if (streams_total == 0) return RMAT_OK;
+  if (!a->out) return RMAT_ERR_INVALID;
+
+  const bool out64 = a->out_width == 8;
+  const bool count = a->samples_total || a->samples_per_stream;
+  int kernel = a->kernel;
+  const bool packed_ok = t->fb != 0 && t->dmax <= a->k && a->k <= 33;
+  if (kernel == RMAT_KERNEL_AUTO)
+    kernel = packed_ok ? (t->packed_smem ? RMAT_KERNEL_PACKED_SMEM : RMAT_KERNEL_PACKED_GLOBAL)
+                       : RMAT_KERNEL_GENERIC;
+  if ((kernel == RMAT_KERNEL_PACKED_SMEM && !(packed_ok && t->packed_smem)) ||
+      (kernel == RMAT_KERNEL_PACKED_GLOBAL && !packed_ok) || kernel < 0 || kernel > 3)
+    return RMAT_ERR_UNSUPPORTED;
+  if (a->kernel_used) *a->kernel_used = kernel;
+
+  const uint64_t key = a->seed ^ a->domain;
+  uint64_t stream_begin = 0;
+  for (uint32_t s0 = 0; s0 < a->n_segments; s0 += rmat::kMaxSegsPerLaunch) {
+    rmat::GenLaunch g;
+    std::memset(&g, 0, sizeof g);
+    g.k = a->k;
+    g.k0 = (uint32_t)key;
+    g.k1 = (uint32_t)(key >> 32);
+    g.E = E;
+    g.out = a->out;
+    g.samples_total = a->samples_total;
+    g.samples_per_stream = a->samples_per_stream;
+    uint32_t nseg = 0;
+    const uint64_t launch_begin = stream_begin;
+    for (uint32_t i = s0; i < a->n_segments && nseg < (uint32_t)rmat::kMaxSegsPerLaunch; ++i) {
+      const rmat_segment& s = a->segments[i];
+      rmat::SegDev& dv = g.segs[nseg++];
+      dv.sid_base = s.sid_base;
+      dv.edge_count = s.edge_count;
+      dv.out_row = s.out_row;
+      dv.row_prefix = s.row_prefix;
+      dv.col_prefix = s.col_prefix;
+      dv.stream_begin = stream_begin;
+      stream_begin += (s.edge_count + E - 1) / E;
+    }
+    g.nseg = nseg;
+    // Streams of this launch are [launch_begin, stream_begin); the kernels index
+    // streams globally so samples_per_stream stays in global order.
+    if (stream_begin == launch_begin) continue;
+    // Kernels start at stream index gt (< total); offset by launch_begin via segs.
+    for (uint32_t i = 0; i < nseg; ++i) g.segs[i].stream_begin -= launch_begin;
+    g.total_streams = stream_begin - launch_begin;
+    if (a->samples_per_stream) g.samples_per_stream = a->samples_per_stream + launch_begin;
+    rmat_status rs;
+    switch (kernel) {
+      case RMAT_KERNEL_PACKED_SMEM:
+        rs = t->fb == 16 ? launch_packed_fb<16, true>(t, g, out64, prefix, count, st)
+                         : launch_packed_fb<32, true>(t, g, out64, prefix, count, st);
+        break;
+      case RMAT_KERNEL_PACKED_GLOBAL:
+        rs = t->fb == 16 ? launch_packed_fb<16, false>(t, g, out64, prefix, count, st)
+                         : launch_packed_fb<32, false>(t, g, out64, prefix, count, st);
+        break;
+      default:
+        rs = launch_generic(t, g, out64, st);
+    }
+    if (rs != RMAT_OK) return rs;
+  }
+  return RMAT_OK;
+}
+
+rmat_status rmat_replay_words(const rmat_table* t, uint64_t seed, uint64_t domain, uint64_t sid,
+                              uint64_t start, uint64_t count, uint64_t* out, void* cuda_stream) {
+  if (!t || (count && !out)) return RMAT_ERR_INVALID;
+  if (count == 0) return RMAT_OK;
+  DeviceGuard guard(t->device);
+  if (!guard.ok) return RMAT_ERR_DEVICE;
+  const uint64_t key = seed ^ domain;
+  const int threads = 256;
+  const int blocks = (int)std::min<uint64_t>(1024, (count + threads - 1) / threads);
+  rmat::k_replay_words<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      (int)t->scheme_p, t->lg, sid, (uint32_t)key, (uint32_t)(key >> 32), start, count, out);
+  return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+}
+
+rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_stream) {
+  if (!a || !a->table || a->k < 1 || a->k > 62 || (a->out_width != 4 && a->out_width != 8) ||
+      a->block_size < 1)
+    return RMAT_ERR_INVALID;
+  if (a->out_width == 4 && a->k > 32) return RMAT_ERR_INVALID;
+  if (a->n_blocks == 0) return RMAT_OK;
+  if (!a->out) return RMAT_ERR_INVALID;
+  const uint64_t nblocks_all = (a->edge_count + a->block_size - 1) / a->block_size;
+  if (a->first_block > nblocks_all || a->n_blocks > nblocks_all - a->first_block)
+    return RMAT_ERR_INVALID;
+  const rmat_table* t = a->table;
+  DeviceGuard guard(t->device);
+  if (!guard.ok) return RMAT_ERR_DEVICE;
+  return rmat::launch_refstream(generic_view(t), t->dmax, *a,
+                                reinterpret_cast<cudaStream_t>(cuda_stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// Device-side table layouts and launch parameter blocks shared by the
+// sampling kernels (rmat_kernels.cu) and the host dispatcher (rmat_capi.cu).
+#pragma once
+#include <stdint.h>
+
+namespace rmat {
+
+constexpr int kMaxSegsPerLaunch = 64;
+
+// Segment as the kernels see it: rmat_segment plus the global index of its
+// first stream (prefix sum over ceil(edge_count / E)).
+struct SegDev {
+  uint64_t sid_base;
+  uint64_t edge_count;
+  uint64_t out_row;
+  uint64_t row_prefix;
+  uint64_t col_prefix;
+  uint64_t stream_begin;
+};
+
+// ---------------------------------------------------------------------------
+// Packed bucket layout (scheme P tables only).  Bucket i is the alias bucket
+// hit by a sample whose word carries i in bits [2, 2+lg):
+//   B[i] = T_hi | (d_self - 1) | (d_alias - 1) << DB
+//          T = thr32 clamped to 32 bits (alias forced to self when thr32 == 2^32),
+//          T_hi = T & ~(4n-1), DB = 4 (16-bit fields) or 5 (32-bit fields)
+//   A[i] = both candidate fragments, so one pair of independent loads resolves
+//          the sample without a dependent second lookup:
+//          FB=16: uint2 {row_self | row_alias << 16, col_self | col_alias << 16}
+//          FB=32: uint4 {row_self, row_alias, col_self, col_alias}
+//   TLO[i] = T & (4n-1): only read when the fraction's top bits tie T_hi.
+// ---------------------------------------------------------------------------
+struct PackedTab {
+  const uint32_t* B;
+  const void* A;
+  const uint32_t* tlo;
+  uint32_t idxmask4;  // (n-1) << 2
+  uint32_t fm;        // 4n - 1
+  uint32_t n;
+  uint32_t fb;        // 16 or 32
+};
+
+// Generic layout: one record per fragment, any n / depth <= 62.
+struct GenericTab {
+  const uint32_t* T;      // clamped thr32 (see above)
+  const uint32_t* alias;  // alias index (self where thr32 == 2^32)
+  const uint64_t* row;
+  const uint64_t* col;
+  const uint8_t* depth;
+  uint32_t n;
+  uint32_t scheme_p;
+  uint32_t lg;
+};
+
+struct GenLaunch {
+  uint32_t k;           // bits per endpoint emitted by the stream
+  uint32_t k0, k1;      // Philox key = seed ^ domain
+  uint32_t nseg;
+  uint64_t E;           // edges per stream
+  uint64_t total_streams;
+  void* out;
+  uint64_t* samples_total;
+  uint64_t* samples_per_stream;
+  SegDev segs[kMaxSegsPerLaunch];
+};
+
+}  // namespace rmat

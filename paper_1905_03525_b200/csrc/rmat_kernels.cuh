@@ -1,0 +1,295 @@
+// R-MAT fragment-sampling kernels for sm_100a (B200).
+//
+// One thread = one counter-based Philox4x32-10 stream (north_star (3)).  Per
+// sample: one Philox word -> alias bucket + fraction -> fragment (row bits,
+// col bits, depth) -> appended to 32-bit register bit buffers; whenever k
+// bits have accumulated an edge is cut and stored, leftover bits carry on.
+// Semantics per stream are exactly the reference's scalar loop
+// (pkg/src/rmatgen/generator.py:324-356) fed with the stream's replay words
+// (csrc/philox.cuh replay_word), which tests/ check bit-for-bit.
+//
+// Kernels
+//   k_packed<FB, SMEM, OUT64, PREFIX, COUNT>   fast path (scheme P tables,
+//       one edge per sample at most: max depth <= k <= 33, depth <= 31)
+//   k_generic<OUT64>                           everything else (any table,
+//       k <= 62, 128-bit accumulators, reference generator.py:46-59 bound)
+//   k_replay_words                             oracle-mode word dump
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "philox.cuh"
+#include "rmat_device.cuh"
+
+namespace rmat {
+
+__device__ __forceinline__ uint32_t bmsk32(uint32_t width) {
+  uint32_t m;
+  asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(m) : "r"(width));
+  return m;
+}
+
+// Global stream index -> (segment, local stream).  Rare (once per stream).
+__device__ __forceinline__ int find_segment(const GenLaunch& g, uint64_t s) {
+  int lo = 0, hi = (int)g.nseg - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (g.segs[mid].stream_begin <= s) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+struct StreamPos {
+  uint64_t sid;
+  uint64_t left;      // edges still to emit
+  uint64_t row;       // first output row
+  uint64_t rpre, cpre;
+  bool valid;
+};
+
+__device__ __forceinline__ StreamPos open_stream(const GenLaunch& g, uint64_t s) {
+  StreamPos p;
+  p.valid = s < g.total_streams;
+  if (!p.valid) return p;
+  const SegDev& sg = g.segs[find_segment(g, s)];
+  uint64_t j = s - sg.stream_begin;
+  uint64_t first = j * g.E;
+  p.sid = sg.sid_base + j;
+  p.left = min(g.E, sg.edge_count - first);
+  p.row = sg.out_row + first;
+  p.rpre = sg.row_prefix;
+  p.cpre = sg.col_prefix;
+  return p;
+}
+
+template <bool OUT64>
+__device__ __forceinline__ void store_edge(void* out, uint64_t row, uint64_t u, uint64_t v) {
+  if (OUT64) {
+    ulonglong2 e = make_ulonglong2(u, v);
+    reinterpret_cast<ulonglong2*>(out)[row] = e;
+  } else {
+    uint2 e = make_uint2((uint32_t)u, (uint32_t)v);
+    reinterpret_cast<uint2*>(out)[row] = e;
+  }
+}
+
+template <int FB> struct AEntry;
+template <> struct AEntry<16> { using T = uint2; };
+template <> struct AEntry<32> { using T = uint4; };
+
+// ---------------------------------------------------------------------------
+// Fast path.
+//
+// Per 4 samples (one Philox call): 4 bucket loads (independent of the bit
+// accumulator chain, issued first), one rare-path branch for fraction ties,
+// then 4 accumulator steps.  The accumulator keeps stale bits above its f
+// valid bits; they never reach an edge because edges are masked to k bits.
+// ---------------------------------------------------------------------------
+template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT>
+__global__ void __launch_bounds__(SMEM ? 1024 : 256, 1)
+k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
+  using AE = typename AEntry<FB>::T;
+  extern __shared__ __align__(16) uint8_t smem[];
+
+  const uint8_t* baseA;
+  const uint8_t* baseB;
+  if (SMEM) {
+    // Stage the bucket arrays: A first (16B aligned), then B.
+    const uint32_t n = tab.n;
+    const size_t abytes = (size_t)n * sizeof(AE);
+    const size_t bbytes = (size_t)n * 4;
+    const uint4* srcA = reinterpret_cast<const uint4*>(tab.A);
+    uint4* dstA = reinterpret_cast<uint4*>(smem);
+    for (size_t i = threadIdx.x; i < abytes / 16; i += blockDim.x) dstA[i] = __ldg(srcA + i);
+    const uint4* srcB = reinterpret_cast<const uint4*>(tab.B);
+    uint4* dstB = reinterpret_cast<uint4*>(smem + abytes);
+    for (size_t i = threadIdx.x; i < bbytes / 16; i += blockDim.x) dstB[i] = __ldg(srcB + i);
+    __syncthreads();
+    baseA = smem;
+    baseB = smem + abytes;
+  } else {
+    baseA = reinterpret_cast<const uint8_t*>(tab.A);
+    baseB = reinterpret_cast<const uint8_t*>(tab.B);
+  }
+
+  const uint32_t k = g.k;
+  const uint32_t kmask = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
+  const uint32_t k0 = g.k0, k1 = g.k1;
+  const uint32_t idxmask4 = tab.idxmask4, fm = tab.fm;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+
+  StreamPos p = open_stream(g, s);
+  if (!p.valid) return;
+  uint64_t j = 0;                    // Philox call index within the stream
+  uint32_t cur_r = 0, cur_c = 0, f = 0;
+  uint64_t total_nf = 0;
+  uint32_t ebits = 0;                // COUNT: samples of the current call that stored an edge
+  char* optr = reinterpret_cast<char*>(g.out) + p.row * (OUT64 ? 16 : 8);
+  int left = (int)p.left;
+
+  for (;;) {
+    if (left <= 0) {
+      if (COUNT) {
+        // nf (generator.py:255-257) = index of the sample that produced the
+        // stream's last edge + 1: the highest sample of call j-1 that stored.
+        const uint64_t nf = 4 * (j - 1) + (32 - __clz(ebits));
+        total_nf += nf;
+        if (g.samples_per_stream) g.samples_per_stream[s] = nf;
+      }
+      s += T;
+      p = open_stream(g, s);
+      if (!p.valid) break;
+      j = 0; cur_r = cur_c = f = 0;
+      optr = reinterpret_cast<char*>(g.out) + p.row * (OUT64 ? 16 : 8);
+      left = (int)p.left;
+    }
+    const u32x4 w4 = stream_call(j, 0, p.sid, k0, k1);
+    const uint32_t wq[4] = {w4.x, w4.y, w4.z, w4.w};
+    uint32_t bq[4];
+    AE aq[4];
+    bool ltq[4];
+    bool tie = false;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t a4 = wq[t] & idxmask4;
+      bq[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
+      aq[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
+      // B = T_hi | d_alias << 8 | d_self; the fields sit below T_hi, so these
+      // compare the fraction's top bits H against T_hi only.
+      ltq[t] = (wq[t] | fm) < bq[t];                 // H <  T_hi
+      tie |= !ltq[t] && (wq[t] & ~fm) <= bq[t];      // H == T_hi
+    }
+    if (tie) {
+      // Rare (p ~ 2^-(32-F) per sample): decide ties with the lazy word.
+      const u32x4 z4 = stream_call(j, 1, p.sid, k0, k1);
+      const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (!ltq[t] && (wq[t] & ~fm) <= bq[t])
+          ltq[t] = (zq[t] & fm) < __ldg(tab.tlo + ((wq[t] & idxmask4) >> 2));
+    }
+    if (COUNT) ebits = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const bool lt = ltq[t];
+      uint32_t r, c;
+      if constexpr (FB == 16) {
+        const uint32_t sel = lt ? 0x4410u : 0x4432u;
+        r = __byte_perm(aq[t].x, 0, sel);
+        c = __byte_perm(aq[t].y, 0, sel);
+      } else {
+        r = lt ? aq[t].x : aq[t].y;
+        c = lt ? aq[t].z : aq[t].w;
+      }
+      const uint32_t d = __byte_perm(bq[t], 0, lt ? 0x4440u : 0x4441u);
+      // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
+      const uint32_t pw = 1u << d;
+      const uint32_t tt = f + d;
+      const uint32_t vr = cur_r * pw + r, vrh = __umulhi(cur_r, pw);
+      const uint32_t vc = cur_c * pw + c, vch = __umulhi(cur_c, pw);
+      const bool emit = tt >= k;
+      const uint32_t over = emit ? tt - k : tt;
+      cur_r = vr;
+      cur_c = vc;
+      f = over;
+      const bool st = emit && left > 0;
+      if (st) {
+        uint64_t u = __funnelshift_r(vr, vrh, over) & kmask;
+        uint64_t v = __funnelshift_r(vc, vch, over) & kmask;
+        if constexpr (OUT64) {
+          u |= (uint64_t)((vrh >> over) & (k > 32 ? 1u : 0u)) << 32;  // k <= 33
+          v |= (uint64_t)((vch >> over) & (k > 32 ? 1u : 0u)) << 32;
+        }
+        if (PREFIX) { u |= p.rpre; v |= p.cpre; }
+        if constexpr (OUT64) {
+          *reinterpret_cast<ulonglong2*>(optr) = make_ulonglong2(u, v);
+        } else {
+          *reinterpret_cast<uint2*>(optr) = make_uint2((uint32_t)u, (uint32_t)v);
+        }
+      }
+      if (COUNT) ebits |= (uint32_t)st << t;
+      optr += emit ? (OUT64 ? 16 : 8) : 0;
+      left -= emit;
+    }
+    ++j;
+  }
+  if (COUNT && g.samples_total && total_nf)
+    atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)total_nf);
+}
+
+// ---------------------------------------------------------------------------
+// Generic path: any table (scheme P or G), any k <= 62, depth <= 62.
+// ---------------------------------------------------------------------------
+template <bool OUT64>
+__global__ void __launch_bounds__(256)
+k_generic(const GenericTab tab, const __grid_constant__ GenLaunch g) {
+  typedef unsigned __int128 u128;
+  const uint32_t k = g.k;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t n = tab.n;
+  const uint32_t fm = tab.scheme_p ? ((1u << scheme_p_fbits(tab.lg)) - 1u) : 0u;
+  const u128 kmask = (((u128)1) << k) - 1;
+  uint64_t total_nf = 0;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < g.total_streams; s += T) {
+    StreamPos p = open_stream(g, s);
+    u128 racc = 0, cacc = 0;
+    uint32_t len = 0;
+    uint64_t left = p.left, i = 0, outrow = p.row;
+    u32x4 cache = {0, 0, 0, 0};
+    while (left > 0) {
+      uint32_t idx, lt;
+      if (tab.scheme_p) {
+        if ((i & 3) == 0) cache = stream_call(i >> 2, 0, p.sid, g.k0, g.k1);
+        const uint32_t w = pick4(cache, (uint32_t)(i & 3));
+        idx = (w >> 2) & (n - 1);
+        const uint32_t Tv = tab.T[idx];
+        const uint32_t hi = w & ~fm, thi = Tv & ~fm;
+        if (hi != thi) {
+          lt = hi < thi;
+        } else {
+          const uint32_t z = pick4(stream_call(i >> 2, 1, p.sid, g.k0, g.k1), (uint32_t)(i & 3));
+          lt = (z & fm) < (Tv & fm);
+        }
+      } else {
+        if ((i & 1) == 0) cache = stream_call(i >> 1, 0, p.sid, g.k0, g.k1);
+        const uint32_t w1 = (i & 1) ? cache.z : cache.x;
+        const uint32_t w2 = (i & 1) ? cache.w : cache.y;
+        idx = ((n & (n - 1)) == 0) ? (w1 & (n - 1)) : (w1 % n);
+        lt = w2 < tab.T[idx];
+      }
+      ++i;
+      const uint32_t e = lt ? idx : tab.alias[idx];
+      const uint32_t d = tab.depth[e];
+      racc = (racc << d) | tab.row[e];
+      cacc = (cacc << d) | tab.col[e];
+      len += d;
+      while (len >= k && left > 0) {
+        const uint32_t over = len - k;
+        const uint64_t u = (uint64_t)((racc >> over) & kmask) | p.rpre;
+        const uint64_t v = (uint64_t)((cacc >> over) & kmask) | p.cpre;
+        store_edge<OUT64>(g.out, outrow++, u, v);
+        const u128 keep = (((u128)1) << over) - 1;
+        racc &= keep;
+        cacc &= keep;
+        len = over;
+        --left;
+      }
+    }
+    total_nf += i;
+    if (g.samples_per_stream) g.samples_per_stream[s] = i;
+  }
+  if (g.samples_total && total_nf) atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)total_nf);
+}
+
+// ---------------------------------------------------------------------------
+// Oracle mode: replay words of one stream.
+// ---------------------------------------------------------------------------
+__global__ void k_replay_words(int scheme_p, uint32_t lg, uint64_t sid, uint32_t k0, uint32_t k1,
+                               uint64_t start, uint64_t count, uint64_t* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = replay_word(scheme_p, lg, start + i, sid, k0, k1);
+}
+
+}  // namespace rmat

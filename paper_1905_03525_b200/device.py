@@ -1,0 +1,161 @@
+"""Device-resident fragment tables and raw launches through the C ABI.
+
+`DeviceTable` is the device half of the reference's `_compile`
+(reference generator.py:114-130): the host hands the compiled arrays
+(thr32, alias, row, col, depth) to `rmat_table_create`, which validates
+them and builds the packed bucket layouts the kernels read.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .alias import threshold_to_u32
+from .table import FragmentTable
+
+__all__ = ["DeviceTable", "device_table", "launch_generate", "launch_refstream",
+           "replay_words", "require_cuda", "Segment"]
+
+Segment = N.Segment
+
+
+def require_cuda(device=None):
+    """Return a torch.device on CUDA or raise NativeUnavailable (no CPU fallback)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise N.NativeUnavailable("no CUDA device: the R-MAT sampling path runs only on the GPU")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.type != "cuda":
+        raise N.NativeUnavailable(f"device {dev} is not a CUDA device")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+@dataclass(frozen=True)
+class TableInfo:
+    n: int
+    min_depth: int
+    max_depth: int
+    scheme_p: bool
+    lg: int
+    packed_width: int
+    packed_smem: bool
+    packed_bytes: int
+    device_bytes: int
+    device: int
+
+
+class DeviceTable:
+    """A FragmentTable uploaded to one GPU (owns an rmat_table handle)."""
+
+    def __init__(self, table: FragmentTable, device=None):
+        dev = require_cuda(device)
+        self.device = dev
+        self.table = table
+        self.thr32 = threshold_to_u32(table.sampler.threshold)
+        self.alias = np.ascontiguousarray(table.sampler.alias, dtype=np.int64)
+        self.row = np.ascontiguousarray(table.row_bits, dtype=np.uint64)
+        self.col = np.ascontiguousarray(table.col_bits, dtype=np.uint64)
+        self.depth = np.ascontiguousarray(table.depths, dtype=np.uint64)
+        desc = N.TableDesc(len(table), self.thr32.ctypes.data, self.alias.ctypes.data,
+                           self.row.ctypes.data, self.col.ctypes.data, self.depth.ctypes.data)
+        handle = ctypes.c_void_p()
+        L = N.lib()
+        N.check(L.rmat_table_create(dev.index, ctypes.byref(desc), ctypes.byref(handle)),
+                "rmat_table_create")
+        self.handle = handle.value
+        self._finalizer = weakref.finalize(self, L.rmat_table_destroy, handle.value)
+        inf = N.TableInfo()
+        N.check(L.rmat_table_get_info(self.handle, ctypes.byref(inf)), "rmat_table_get_info")
+        self.info = TableInfo(inf.n, inf.min_depth, inf.max_depth, bool(inf.scheme), inf.lg,
+                              inf.packed_width, bool(inf.packed_smem), inf.packed_bytes,
+                              inf.device_bytes, inf.device)
+
+    def close(self) -> None:
+        self._finalizer()
+
+
+_cache: dict[tuple[int, int], tuple[weakref.ref, DeviceTable]] = {}
+_cache_lock = threading.Lock()
+
+
+def device_table(table: FragmentTable, device=None) -> DeviceTable:
+    """Upload `table` to `device` once; later calls reuse the handle."""
+    dev = require_cuda(device)
+    key = (id(table), dev.index)
+    with _cache_lock:
+        hit = _cache.get(key)
+        if hit is not None and hit[0]() is table:
+            return hit[1]
+        dt = DeviceTable(table, dev)
+        _cache[key] = (weakref.ref(table), dt)
+        return dt
+
+
+def _stream_ptr(dev) -> int:
+    import torch
+
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def launch_generate(dt: DeviceTable, k: int, seed: int, domain: int, edges_per_stream: int,
+                    segments: list[tuple[int, int, int, int, int]], out, *,
+                    samples_total=None, samples_per_stream=None,
+                    kernel: int = N.KERNEL_AUTO) -> int:
+    """rmat_generate on dt's device and torch's current stream; returns the kernel used."""
+    import torch
+
+    assert out.device == dt.device and out.is_contiguous() and out.dim() == 2 and out.shape[1] == 2
+    width = out.element_size()
+    segs = (N.Segment * max(len(segments), 1))(*[N.Segment(*map(int, s)) for s in segments])
+    used = ctypes.c_int(0)
+    args = N.GenArgs(
+        table=dt.handle, k=k, out_width=width, seed=seed & (2**64 - 1), domain=domain,
+        edges_per_stream=edges_per_stream, segments=segs, n_segments=len(segments),
+        out=out.data_ptr() if out.numel() else None, out_rows=out.shape[0],
+        samples_total=samples_total.data_ptr() if samples_total is not None else None,
+        samples_per_stream=(samples_per_stream.data_ptr()
+                            if samples_per_stream is not None else None),
+        kernel=kernel, kernel_used=ctypes.pointer(used))
+    with torch.cuda.device(dt.device):
+        N.check(N.lib().rmat_generate(ctypes.byref(args), _stream_ptr(dt.device)),
+                "rmat_generate")
+    return used.value
+
+
+def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size: int,
+                     edge_count: int, first_block: int, n_blocks: int, out, *,
+                     samples_per_block=None, samples_total=None) -> None:
+    import torch
+
+    assert out.device == dt.device and out.is_contiguous()
+    args = N.RefArgs(
+        table=dt.handle, k=k, out_width=out.element_size(), seed=seed & (2**64 - 1),
+        domain=domain, block_size=block_size, edge_count=edge_count, first_block=first_block,
+        n_blocks=n_blocks, out=out.data_ptr() if out.numel() else None,
+        samples_per_block=(samples_per_block.data_ptr()
+                           if samples_per_block is not None else None),
+        samples_total=samples_total.data_ptr() if samples_total is not None else None)
+    with torch.cuda.device(dt.device):
+        N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), _stream_ptr(dt.device)),
+                "rmat_generate_refstream")
+
+
+def replay_words(dt: DeviceTable, seed: int, domain: int, sid: int, count: int, start: int = 0):
+    """K1-dump: the replay words stream `sid` feeds `_select` -> device uint64 tensor."""
+    import torch
+
+    out = torch.empty(count, dtype=torch.uint64, device=dt.device)
+    with torch.cuda.device(dt.device):
+        N.check(N.lib().rmat_replay_words(dt.handle, seed & (2**64 - 1), domain, sid, start,
+                                          count, out.data_ptr() if count else None,
+                                          _stream_ptr(dt.device)), "rmat_replay_words")
+    return out

@@ -1,0 +1,250 @@
+"""Edge generation: the drop-in for the reference's sampling path.
+
+Mirrors reference pkg/src/rmatgen/generator.py -- `GenConfig`, `GenResult`,
+`generate`, `generate_result`, `emit_block`, `DEFAULT_BLOCK_SIZE` -- with the
+same argument meaning and errors, but every edge is produced on the GPU by
+the sm_100a kernels behind the C ABI (include/rmat_b200.h).  There is no CPU
+fallback: without CUDA these functions raise `NativeUnavailable`.
+
+Two random-stream modes:
+
+* ``rng="philox4x32"`` (default; north_star's fast path): stream b is a
+  Philox4x32-10 stream keyed (seed ^ DOMAIN_BLOCK, b), one thread each.
+  Per stream the edges equal the reference's `_emit` replayed on that
+  stream's words (`replay_words`), bit for bit.
+* ``rng="reference"``: block b draws numpy's Philox4x64-10 stream keyed
+  [seed ^ DOMAIN_BLOCK, b] exactly like the reference, so `generate()`
+  returns the same bytes as `rmatgen.generate()`.
+
+Layout is the reference's: block (stream) b owns output rows
+[b*B, b*B + count_b) (generator.py:451-455), so the output is a pure
+function of (table, k, m, seed, block_size, rng) and never of the GPU count.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import NamedTuple
+
+import numpy as np
+
+from . import _native as N
+from .device import device_table, launch_generate, launch_refstream, replay_words, require_cuda
+from .params import MAX_K, BadExponent, RmatParams, check_k
+from .table import FragmentTable
+
+__all__ = [
+    "DEFAULT_BLOCK_SIZE", "FAST_STREAM_EDGES", "DOMAIN_BLOCK", "DOMAIN_TILE", "RNG_MODES",
+    "Edge", "GenConfig", "GenResult", "generate", "generate_result", "generate_device",
+    "generate_shard", "emit_block", "shard_rows", "stream_replay_words", "edge_dtype",
+]
+
+#: Reference block size (reference generator.py:31) -- the default in "reference" mode.
+DEFAULT_BLOCK_SIZE = 1 << 16
+#: Default edges per Philox4x32 stream in fast mode (one stream per GPU thread).
+FAST_STREAM_EDGES = 1 << 10
+
+# Stream-family constants, as in reference _rng.py:18-22.
+DOMAIN_BLOCK = 0x9E3779B97F4A7C15
+DOMAIN_NODE = 0xBF58476D1CE4E5B9
+DOMAIN_TILE = 0x94D049BB133111EB
+
+RNG_MODES = ("philox4x32", "reference")
+_M64 = (1 << 64) - 1
+
+
+class Edge(NamedTuple):
+    u: int
+    v: int
+
+
+@dataclass(frozen=True)
+class GenConfig:
+    """Everything `generate` needs (reference generator.py:62-79).
+
+    block_size: edges per random stream; None = the mode's default
+    (2^16 for "reference", 2^10 for "philox4x32").  threads: accepted for
+    API compatibility; like the reference, it never changes the output.
+    devices: CUDA device indices to spread the streams over (None = current).
+    """
+
+    params: RmatParams
+    table: FragmentTable
+    edge_count: int
+    seed: int
+    block_size: int | None = None
+    threads: int = 1
+    rng: str = "philox4x32"
+    devices: tuple[int, ...] | None = field(default=None)
+
+    def __post_init__(self) -> None:
+        if not 0 <= self.edge_count < 1 << 63:
+            raise ValueError(f"edge_count must be in [0, 2**63), got {self.edge_count}")
+        if self.block_size is not None and self.block_size < 1:
+            raise ValueError(f"block_size must be >= 1, got {self.block_size}")
+        if self.threads < 1:
+            raise ValueError(f"threads must be >= 1, got {self.threads}")
+        if self.rng not in RNG_MODES:
+            raise ValueError(f"rng must be one of {RNG_MODES}, got {self.rng!r}")
+        if self.rng == "philox4x32" and self.stream_edges >= 1 << 31:
+            raise ValueError("fast-mode block_size (edges per stream) must be < 2**31")
+
+    @property
+    def stream_edges(self) -> int:
+        if self.block_size is not None:
+            return self.block_size
+        return DEFAULT_BLOCK_SIZE if self.rng == "reference" else FAST_STREAM_EDGES
+
+
+@dataclass(frozen=True)
+class GenResult:
+    """Edges plus the alias-sample count (reference generator.py:82-87)."""
+
+    edges: np.ndarray  # (m, 2) uint64
+    samples_consumed: int
+
+
+def edge_dtype(k: int):
+    """Device edge dtype: uint32 endpoints when k <= 32, else uint64."""
+    import torch
+
+    return torch.uint32 if k <= 32 else torch.uint64
+
+
+def shard_rows(m: int, block: int, rank: int, world: int) -> tuple[int, int, int, int]:
+    """Streams [s_lo, s_hi) and rows [r_lo, r_hi) owned by `rank` of `world`.
+
+    Whole streams are dealt in near-equal contiguous runs, so shards
+    concatenated in rank order are exactly the single-GPU output.
+    """
+    nstreams = (m + block - 1) // block
+    base, extra = divmod(nstreams, world)
+    s_lo = rank * base + min(rank, extra)
+    s_hi = s_lo + base + (1 if rank < extra else 0)
+    return s_lo, s_hi, min(s_lo * block, m), min(s_hi * block, m)
+
+
+def generate_shard(config: GenConfig, rank: int = 0, world: int = 1, device=None, out=None,
+                   count_samples: bool = False, kernel: int = N.KERNEL_AUTO):
+    """Rows [r_lo, r_hi) of generate(config) on one GPU -> (tensor, r_lo, samples|None).
+
+    The device-resident building block of every generate variant and of the
+    multi-GPU bench (one rank per GPU, no collective on the data path).
+    """
+    import torch
+
+    k = config.params.k
+    check_k(k)
+    dev = require_cuda(device)
+    B = config.stream_edges
+    s_lo, s_hi, r_lo, r_hi = shard_rows(config.edge_count, B, rank, world)
+    rows = r_hi - r_lo
+    if out is None:
+        out = torch.empty((rows, 2), dtype=edge_dtype(k), device=dev)
+    elif out.shape != (rows, 2) or out.dtype != edge_dtype(k) or out.device != dev:
+        raise ValueError(f"out must be ({rows}, 2) {edge_dtype(k)} on {dev}")
+    samples = torch.zeros(1, dtype=torch.int64, device=dev) if count_samples else None
+    if rows:
+        dt = device_table(config.table, dev)
+        if config.rng == "reference":
+            launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, config.edge_count, s_lo,
+                             s_hi - s_lo, out, samples_total=samples)
+        else:
+            launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B,
+                            [(s_lo, rows, 0, 0, 0)], out, samples_total=samples, kernel=kernel)
+    return out, r_lo, samples
+
+
+def generate_device(config: GenConfig, count_samples: bool = False):
+    """All edges in HBM: a list of (device tensor, first row) shards, one per device.
+
+    With one device the list has one (m, 2) tensor; shards concatenated in
+    order equal the single-device output (GPU-count invariance).
+    """
+    devices = config.devices or (None,)
+    shards = []
+    counters = []
+    for r, d in enumerate(devices):
+        out, r_lo, s = generate_shard(config, r, len(devices), device=d,
+                                      count_samples=count_samples)
+        shards.append((out, r_lo))
+        counters.append(s)
+    if count_samples:
+        return shards, sum(int(s.item()) for s in counters)
+    return shards
+
+
+def _to_host_u64(t) -> np.ndarray:
+    import torch
+
+    host = t.to("cpu")
+    if host.dtype == torch.uint32:
+        return host.numpy().astype(np.uint64)
+    return host.numpy()
+
+
+def generate_result(config: GenConfig) -> GenResult:
+    """Generate `edge_count` edges; host (m, 2) uint64 plus samples consumed.
+
+    Reference generator.py:435-469.  Edges are produced in HBM and copied
+    back once (the reference's return type is a host numpy array).
+    """
+    check_k(config.params.k)
+    m = config.edge_count
+    if m == 0:
+        return GenResult(np.empty((0, 2), dtype=np.uint64), 0)
+    shards, samples = generate_device(config, count_samples=True)
+    edges = np.empty((m, 2), dtype=np.uint64)
+    for t, r_lo in shards:
+        edges[r_lo:r_lo + t.shape[0]] = _to_host_u64(t)
+    return GenResult(edges, samples)
+
+
+def generate(config: GenConfig) -> np.ndarray:
+    """Generate `edge_count` edges as a (m, 2) uint64 host array (reference generator.py:472)."""
+    check_k(config.params.k)
+    m = config.edge_count
+    if m == 0:
+        return np.empty((0, 2), dtype=np.uint64)
+    edges = np.empty((m, 2), dtype=np.uint64)
+    for t, r_lo in generate_device(config):
+        edges[r_lo:r_lo + t.shape[0]] = _to_host_u64(t)
+    return edges
+
+
+def emit_block(table: FragmentTable, k: int, count: int, stream_key: tuple[int, int],
+               rng: str = "philox4x32", device=None) -> np.ndarray:
+    """One stream of `count` edges keyed (seed, block_index) (reference generator.py:306-321)."""
+    check_k(k)
+    if count < 0:
+        raise ValueError(f"count must be >= 0, got {count}")
+    if rng not in RNG_MODES:
+        raise ValueError(f"rng must be one of {RNG_MODES}, got {rng!r}")
+    seed, block = int(stream_key[0]), int(stream_key[1])
+    if count == 0:
+        return np.empty((0, 2), dtype=np.uint64)
+    import torch
+
+    dev = require_cuda(device)
+    dt = device_table(table, dev)
+    out = torch.empty((count, 2), dtype=edge_dtype(int(k)), device=dev)
+    if rng == "reference":
+        # one reference block whose index is `block`: run a 1-block launch
+        launch_refstream(dt, int(k), seed, DOMAIN_BLOCK, count, (block + 1) * count, block, 1,
+                         out)
+    else:
+        if count >= 1 << 31:
+            raise ValueError("fast-mode stream length must be < 2**31")
+        launch_generate(dt, int(k), seed, DOMAIN_BLOCK, count, [(block, count, 0, 0, 0)], out)
+    return _to_host_u64(out)
+
+
+def stream_replay_words(table: FragmentTable, seed: int, stream: int, count: int,
+                        domain: int = DOMAIN_BLOCK, device=None) -> np.ndarray:
+    """Oracle mode: the 64-bit words fast-mode stream `stream` feeds `_select`.
+
+    Feeding them to the reference's `_emit(_compile(table), k, count, gen)`
+    reproduces that stream's edges bit for bit (north_star "oracle mode").
+    """
+    dev = require_cuda(device)
+    return replay_words(device_table(table, dev), seed, domain, stream, count).cpu().numpy()

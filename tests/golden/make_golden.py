@@ -1,0 +1,188 @@
+"""Generate the golden fixtures by running the REFERENCE package itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports rmatgen from /root/reference/pkg/src and records, for the hot
+path, outputs the oracle and the GPU path are later checked against:
+
+* compiled table arrays (the reference `_compile`, generator.py:114-130) for
+  every BASELINE config table and the reference tests' tables -- as SHA-256
+  digests plus summary numbers;
+* replay emissions: the reference `_emit` fed fixed word sequences through a
+  replay bit generator (generator.py:293-298), for many (table, k, count);
+* reference-stream blocks: `emit_block` / `generate_result` outputs;
+* numpy Philox words for a few keys (the reference RNG convention);
+* partition plans (`plan_tiles`, partition.py:112-137) for C4.
+
+Nothing here is imported at test time; the fixtures are plain JSON.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import zlib
+import json
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+G500 = (0.57, 0.19, 0.19, 0.05)
+LESS = (0.45, 0.22, 0.22, 0.11)
+SKEW = (0.9, 0.025, 0.025, 0.05)
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+class Replay:
+    """Bit generator stand-in serving fixed words (zero beyond the end)."""
+
+    class _BG:
+        def __init__(self, words):
+            self.words = np.asarray(words, dtype=np.uint64)
+            self.pos = 0
+
+        def random_raw(self, n):
+            out = np.zeros(n, dtype=np.uint64)
+            take = self.words[self.pos:self.pos + n]
+            out[:len(take)] = take
+            self.pos += n
+            return out
+
+    def __init__(self, words):
+        self.bit_generator = self._BG(words)
+
+
+def replay_words(seed: int, n: int) -> np.ndarray:
+    """The fixed word sequence used by replay fixtures (numpy PCG64, seeded)."""
+    return np.random.default_rng(seed).integers(0, 2**63, size=n, dtype=np.uint64) * np.uint64(2) \
+        + np.random.default_rng(seed + 1).integers(0, 2, size=n, dtype=np.uint64)
+
+
+def main() -> None:
+    sys.path.insert(0, REF)
+    import rmatgen
+    from rmatgen.generator import _compile, _emit
+    from rmatgen.partition import default_plan, plan_tiles
+
+    out: dict = {"generator": "tests/golden/make_golden.py", "numpy": np.__version__}
+
+    # ---- tables
+    tables = {}
+    specs = []
+    for name, quads in (("g500", G500), ("less", LESS), ("skew", SKEW)):
+        for size in (253, 256, 1021, 1024, 4096, 8191, 16384, 65536):
+            specs.append((f"{name}:v{size}", quads, "v", size))
+        for depth in (1, 2, 4, 5, 6, 8):
+            specs.append((f"{name}:f{depth}", quads, "f", depth))
+    built = {}
+    for tag, quads, kind, arg in specs:
+        p = rmatgen.validate(*quads, 20)
+        t = rmatgen.build_variable_table(p, arg) if kind == "v" else rmatgen.build_fixed_table(p, arg)
+        built[tag] = t
+        c = _compile(t)
+        tables[tag] = {
+            "n": len(t), "max_depth": int(t.max_depth), "min_depth": int(t.depths.min()),
+            "mean_depth": repr(float(t.mean_depth)),
+            "thr32": sha(c.thr32.astype(np.uint64)), "alias": sha(c.alias.astype(np.int64)),
+            "row": sha(t.row_bits), "col": sha(t.col_bits), "depth": sha(t.depths),
+            "probs": sha(t.probs),
+        }
+    out["tables"] = tables
+
+    # ---- replay emissions through the reference's own _emit
+    emits = []
+    for tag in ("g500:f1", "g500:f5", "g500:v253", "g500:v1024", "g500:v4096", "g500:v16384",
+                "less:v16384", "g500:f8", "g500:v65536"):
+        comp = _compile(built[tag])
+        for k in (1, 3, 13, 16, 24, 26, 28, 31, 32, 33, 36, 62):
+            for count in (1, 17, 1000):
+                wseed = zlib.crc32(f"{tag}/{k}/{count}".encode()) & 0xFFFF
+                nwords = count * (k // int(built[tag].depths.min()) + 2) + 64
+                words = replay_words(wseed, nwords)
+                edges, nf = _emit(comp, k, count, Replay(words))
+                emits.append({"table": tag, "k": k, "count": count, "word_seed": wseed,
+                              "nwords": nwords, "nf": int(nf), "edges": sha(edges.astype(np.uint64)),
+                              "first": edges[0].tolist(), "last": edges[-1].tolist()})
+    out["replay_emits"] = emits
+
+    # ---- reference-stream blocks (emit_block / generate_result)
+    blocks = []
+    for tag in ("g500:f1", "g500:f5", "g500:v253", "g500:v1024", "g500:v16384", "less:v16384"):
+        for k in (1, 3, 13, 16, 28, 32, 33, 62):
+            for count in (1, 17, 1000):
+                e = rmatgen.emit_block(built[tag], k, count, (9, 3))
+                blocks.append({"table": tag, "k": k, "count": count, "seed": 9, "block": 3,
+                               "edges": sha(e), "first": e[0].tolist(), "last": e[-1].tolist()})
+    out["ref_blocks"] = blocks
+
+    p16 = rmatgen.validate(*G500, 16)
+    t1024 = built["g500:v1024"]
+    r1 = rmatgen.generate_result(rmatgen.GenConfig(params=p16, table=t1024, edge_count=1 << 20,
+                                                    seed=1, block_size=1 << 20))
+    r2 = rmatgen.generate_result(rmatgen.GenConfig(params=p16, table=t1024, edge_count=1 << 20,
+                                                    seed=1))
+    out["known_answers"] = {
+        "c1_single_stream": {"samples": r1.samples_consumed, "first4": r1.edges[:4].tolist(),
+                             "last": r1.edges[-1].tolist(), "edges": sha(r1.edges)},
+        "c1_default_blocks": {"samples": r2.samples_consumed, "edges": sha(r2.edges),
+                              "first4": r2.edges[:4].tolist(), "last": r2.edges[-1].tolist()},
+    }
+    gens = []
+    for tag, quads, k, m, B, seed in (("g500:v4096", G500, 24, 200_000, 65536, 2),
+                                      ("less:v16384", LESS, 36, 150_000, 65536, 4),
+                                      ("g500:f4", G500, 26, 100_000, 1000, 5),
+                                      ("g500:v253", G500, 6, 2500, 512, 77)):
+        pp = rmatgen.validate(*quads, k)
+        r = rmatgen.generate_result(rmatgen.GenConfig(params=pp, table=built[tag], edge_count=m,
+                                                       seed=seed, block_size=B))
+        gens.append({"table": tag, "k": k, "m": m, "block_size": B, "seed": seed,
+                     "samples": r.samples_consumed, "edges": sha(r.edges)})
+    out["ref_generate"] = gens
+
+    # ---- numpy Philox convention
+    from rmatgen._rng import keyed_stream, raw_words
+    out["philox_words"] = [
+        {"seed": s, "domain": d, "payload": pl,
+         "words": [int(x) for x in raw_words(keyed_stream(s, d, pl), 9)]}
+        for s, d, pl in ((1, 0x9E3779B97F4A7C15, 0), (9, 0x9E3779B97F4A7C15, 3),
+                         (2**64 - 1, 0, 2**64 - 1), (5, 0x94D049BB133111EB, 11))]
+
+    # ---- partition plans (C4: less-skewed, k=36, m=2^33, t=3, 8 parts)
+    pl = rmatgen.validate(*LESS, 36)
+    plans = []
+    for k, t, m, seed, parts in ((36, 3, 1 << 33, 1, 8), (12, 2, 10**6, 7, 4), (20, 4, 123457, 3, 3)):
+        plan = default_plan(k, t, m, seed, parts)
+        pp = pl if k == 36 else rmatgen.validate(*G500, k)
+        quads = "less" if k == 36 else "g500"
+        for part in range(parts):
+            tiles = plan_tiles(plan, pp, part)
+            plans.append({"quads": quads, "k": k, "t": t, "m": m, "seed": seed, "parts": parts,
+                          "part": part,
+                          "tiles": [[tc.tile_row, tc.tile_col, tc.count] for tc in tiles]})
+    out["plans"] = plans
+    tiles = []
+    for (r, c, cnt, k, t, seed) in ((0, 0, 5000, 12, 2, 7), (3, 1, 777, 12, 2, 7),
+                                    (2, 5, 1000, 36, 3, 1)):
+        quads = LESS if k == 36 else G500
+        pp = rmatgen.validate(*quads, k)
+        tab = built["less:v16384" if k == 36 else "g500:v1024"]
+        e = rmatgen.generate_tile((r, c), cnt, pp, tab, k, t, seed)
+        tiles.append({"tile": [r, c], "count": cnt, "k": k, "t": t, "seed": seed,
+                      "table": "less:v16384" if k == 36 else "g500:v1024", "edges": sha(e)})
+    out["ref_tiles"] = tiles
+
+    with open(os.path.join(HERE, "golden.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote", os.path.join(HERE, "golden.json"))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA path against the CPU oracle, bit for bit.
+
+Mirrors the reference's bit-identity tests (pkg/tests/test_generator.py:32-60,
+156-176): every stream's edges must equal the normative emission loop
+(reference generator.py:324-356, restated in oracle/rmat_oracle.c) fed with
+that stream's words, for every kernel variant, k and table shape.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import G500, LESS_SKEWED, oracle_table, params_for, table_for
+from paper_1905_03525_b200 import (
+    DOMAIN_BLOCK,
+    GenConfig,
+    emit_block,
+    generate,
+    generate_result,
+    generate_shard,
+    stream_replay_words,
+)
+from paper_1905_03525_b200 import _native as N
+from paper_1905_03525_b200.device import device_table, launch_generate
+
+pytestmark = pytest.mark.gpu
+
+TAGS = ["f1", "f4", "f5", "v253", "v1024", "v4096", "v16384", "v8191"]
+KS = [1, 3, 13, 16, 24, 28, 31, 32, 33, 36, 62]
+
+
+def host(t):
+    t = t.cpu()
+    return t.numpy().astype(np.uint64) if t.dtype == torch.uint32 else t.numpy()
+
+
+@pytest.mark.parametrize("tag", TAGS + ["v65536"])
+@pytest.mark.parametrize("sid", [0, 7, (1 << 32) + 5])
+def test_replay_words_match_oracle(cuda, tag, sid):
+    table = table_for(tag)
+    got = stream_replay_words(table, 12345, sid, 1500)
+    want = oracle.fast_words(oracle_table(tag), 12345, DOMAIN_BLOCK, sid, 1500)
+    assert got.dtype == np.uint64
+    assert (got == want).all()
+
+
+@pytest.mark.parametrize("tag", TAGS)
+@pytest.mark.parametrize("k", KS)
+@pytest.mark.parametrize("count", [1, 17, 1000])
+def test_fast_stream_matches_oracle(cuda, tag, k, count):
+    table = table_for(tag)
+    got = emit_block(table, k, count, (9, 3))
+    want, _ = oracle.fast_stream(oracle_table(tag), k, count, 9, 3)
+    assert got.dtype == np.uint64 and got.shape == (count, 2)
+    assert (got == want).all()
+    assert int(got.max()) >> k == 0
+
+
+@pytest.mark.parametrize("tag,k", [("v1024", 16), ("v4096", 24), ("v16384", 28),
+                                   ("f4", 26), ("f6", 26), ("f8", 26), ("v65536", 26),
+                                   ("v256", 26), ("v253", 20), ("f5", 3)])
+def test_multi_stream_generate_matches_oracle(cuda, tag, k):
+    table = table_for(tag)
+    m, E, seed = 20_000, 777, 31
+    cfg = GenConfig(params=params_for(G500, k), table=table, edge_count=m, seed=seed,
+                    block_size=E)
+    res = generate_result(cfg)
+    want, samples = oracle.fast_generate(oracle_table(tag), k, m, seed, E)
+    assert (res.edges == want).all()
+    assert res.samples_consumed == samples
+
+
+def _variants(table, k):
+    dt = device_table(table, torch.device("cuda", 0))
+    out = [N.KERNEL_GENERIC]
+    if dt.info.packed_width and dt.info.max_depth <= k <= 33:
+        out.append(N.KERNEL_PACKED_GLOBAL)
+        if dt.info.packed_smem:
+            out.append(N.KERNEL_PACKED_SMEM)
+    return dt, out
+
+
+@pytest.mark.parametrize("tag,k", [("v16384", 28), ("v4096", 24), ("v1024", 16), ("f8", 26),
+                                   ("v16384", 33), ("f4", 4), ("f1", 5), ("v65536", 30)])
+def test_kernel_variants_identical(cuda, tag, k):
+    table = table_for(tag)
+    dt, variants = _variants(table, k)
+    assert len(variants) >= 2 or tag == "v65536"
+    m, E = 50_000, 333
+    ref = None
+    nstreams = (m + E - 1) // E
+    for kern in variants:
+        out = torch.empty((m, 2), dtype=torch.uint32 if k <= 32 else torch.uint64, device=cuda)
+        tot = torch.zeros(1, dtype=torch.int64, device=cuda)
+        per = torch.zeros(nstreams, dtype=torch.int64, device=cuda)
+        used = launch_generate(dt, k, 5, DOMAIN_BLOCK, E, [(0, m, 0, 0, 0)], out,
+                               samples_total=tot, samples_per_stream=per, kernel=kern)
+        assert used == kern
+        got = (host(out), int(tot.item()), per.cpu().numpy())
+        if ref is None:
+            ref = got
+            # oracle: per-stream nf
+            ot = oracle_table(tag)
+            for s in (0, 1, nstreams // 2, nstreams - 1):
+                cnt = min(E, m - s * E)
+                e, nf = oracle.fast_stream(ot, k, cnt, 5, s)
+                assert (got[0][s * E: s * E + cnt] == e).all()
+                assert got[2][s] == nf
+            assert got[1] == int(got[2].sum())
+        else:
+            assert (got[0] == ref[0]).all(), N.KERNEL_NAMES[kern]
+            assert got[1] == ref[1] and (got[2] == ref[2]).all()
+
+
+def test_oracle_mode_replay_of_dumped_words(cuda):
+    """north_star oracle mode: the kernel's own per-stream words, replayed through
+    the normative loop, give the kernel's edges."""
+    tag, k, E = "v4096", 24, 5000
+    table = table_for(tag)
+    ot = oracle_table(tag)
+    cfg = GenConfig(params=params_for(G500, k), table=table, edge_count=4 * E, seed=1,
+                    block_size=E)
+    edges = generate(cfg)
+    for s in range(4):
+        words = stream_replay_words(table, 1, s, 4 * E)  # ample: <= k/dmin + slack per edge
+        replay, nf = oracle.emit(ot, k, E, words)
+        assert nf <= len(words)
+        assert (replay == edges[s * E:(s + 1) * E]).all()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shards_concatenate_to_single_gpu_output(cuda, world):
+    cfg = GenConfig(params=params_for(G500, 20), table=table_for("v4096"), edge_count=123_457,
+                    seed=77, block_size=1000)
+    whole, r0, _ = generate_shard(cfg, 0, 1)
+    parts = []
+    for r in range(world):
+        t, r_lo, _ = generate_shard(cfg, r, world)
+        assert r_lo == sum(p.shape[0] for p in parts)
+        parts.append(t)
+    assert torch.equal(torch.cat([p.view(torch.int32) for p in parts]), whole.view(torch.int32))
+
+
+# ---------------------------------------------------------------- reference mode
+@pytest.mark.parametrize("tag", ["f1", "f5", "v253", "v1024", "v16384"])
+@pytest.mark.parametrize("k", [1, 3, 13, 16, 28, 32, 33, 62])
+@pytest.mark.parametrize("count", [1, 17, 1000, 5000])
+def test_reference_mode_emit_block(cuda, tag, k, count):
+    table = table_for(tag)
+    got = emit_block(table, k, count, (9, 3), rng="reference")
+    want, _ = oracle.ref_block(oracle_table(tag), k, count, 9, 3)
+    assert (got == want).all()
+
+
+def test_reference_mode_c1_known_answers(cuda):
+    """C1 (k=16, S=2^10, m=2^20, seed 1): known answers from the reference run
+    (tests/golden/known_answers.json)."""
+    p = params_for(G500, 16)
+    table = table_for("v1024")
+    single = generate_result(GenConfig(params=p, table=table, edge_count=1 << 20, seed=1,
+                                       block_size=1 << 20, rng="reference"))
+    assert single.samples_consumed == 2_761_463
+    assert single.edges[:4].tolist() == [[37953, 37477], [5376, 20556], [49676, 18928],
+                                         [185, 25096]]
+    assert single.edges[-1].tolist() == [28706, 17522]
+    blocks = generate_result(GenConfig(params=p, table=table, edge_count=1 << 20, seed=1,
+                                       rng="reference"))
+    assert blocks.samples_consumed == 2_760_933
+    want, samples = oracle.ref_generate(oracle_table("v1024"), 16, 1 << 20, 1)
+    assert samples == 2_760_933
+    assert (blocks.edges == want).all()
+
+
+def test_reference_mode_generate_less_skewed_k36(cuda):
+    quads = LESS_SKEWED
+    p = params_for(quads, 36)
+    table = table_for("v16384", quads)
+    m = 300_000
+    got = generate_result(GenConfig(params=p, table=table, edge_count=m, seed=4,
+                                    block_size=65536, rng="reference"))
+    want, samples = oracle.ref_generate(oracle_table("v16384", quads), 36, m, 4, 65536)
+    assert (got.edges == want).all()
+    assert got.samples_consumed == samples

@@ -1,0 +1,159 @@
+"""Pin the CPU oracle (and the host table builders) to the reference's own outputs.
+
+tests/golden/golden.json was produced by running the reference package
+(tests/golden/make_golden.py).  Before the oracle may judge the GPU path it
+must reproduce every one of those fixtures.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import G500, LESS_SKEWED, SKEWED
+from paper_1905_03525_b200 import build_fixed_table, build_variable_table, validate
+from paper_1905_03525_b200.alias import threshold_to_u32
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+QUADS = {"g500": G500, "less": LESS_SKEWED, "skew": SKEWED}
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def build(tag: str):
+    name, spec = tag.split(":")
+    p = validate(*QUADS[name], 20)
+    if spec[0] == "v":
+        return build_variable_table(p, int(spec[1:]))
+    return build_fixed_table(p, int(spec[1:]))
+
+
+_tables: dict = {}
+
+
+def table(tag):
+    if tag not in _tables:
+        _tables[tag] = build(tag)
+    return _tables[tag]
+
+
+def otable(tag):
+    return oracle.OracleTable.from_fragment_table(table(tag))
+
+
+def replay_words(seed: int, n: int) -> np.ndarray:
+    # identical to make_golden.replay_words
+    return np.random.default_rng(seed).integers(0, 2**63, size=n, dtype=np.uint64) * np.uint64(2) \
+        + np.random.default_rng(seed + 1).integers(0, 2, size=n, dtype=np.uint64)
+
+
+@pytest.mark.parametrize("tag", sorted(GOLD["tables"]))
+def test_host_table_matches_reference(tag):
+    """Host builders (table.py, alias.py) == reference _compile arrays, bit for bit."""
+    g = GOLD["tables"][tag]
+    t = table(tag)
+    assert len(t) == g["n"] and t.max_depth == g["max_depth"]
+    assert int(t.depths.min()) == g["min_depth"]
+    assert repr(float(t.mean_depth)) == g["mean_depth"]
+    assert sha(threshold_to_u32(t.sampler.threshold)) == g["thr32"]
+    assert sha(t.sampler.alias.astype(np.int64)) == g["alias"]
+    assert sha(t.row_bits) == g["row"] and sha(t.col_bits) == g["col"]
+    assert sha(t.depths) == g["depth"] and sha(t.probs) == g["probs"]
+
+
+@pytest.mark.parametrize("case", GOLD["replay_emits"],
+                         ids=lambda c: f"{c['table']}-k{c['k']}-n{c['count']}")
+def test_oracle_emit_matches_reference_emit(case):
+    """oracle.emit (normative scalar loop in C) == reference _emit on the same words."""
+    words = replay_words(case["word_seed"], case["nwords"])
+    edges, nf = oracle.emit(otable(case["table"]), case["k"], case["count"], words)
+    assert nf == case["nf"]
+    assert sha(edges) == case["edges"]
+    assert edges[0].tolist() == case["first"] and edges[-1].tolist() == case["last"]
+
+
+@pytest.mark.parametrize("case", GOLD["ref_blocks"],
+                         ids=lambda c: f"{c['table']}-k{c['k']}-n{c['count']}")
+def test_oracle_ref_block_matches_reference_emit_block(case):
+    edges, _ = oracle.ref_block(otable(case["table"]), case["k"], case["count"], case["seed"],
+                                case["block"])
+    assert sha(edges) == case["edges"]
+
+
+def test_oracle_known_answers_c1():
+    ka = GOLD["known_answers"]
+    t = otable("g500:v1024")
+    e, nf = oracle.ref_generate(t, 16, 1 << 20, 1, 1 << 20)
+    assert nf == ka["c1_single_stream"]["samples"] == 2_761_463
+    assert e[:4].tolist() == ka["c1_single_stream"]["first4"]
+    assert sha(e) == ka["c1_single_stream"]["edges"]
+    e, nf = oracle.ref_generate(t, 16, 1 << 20, 1)
+    assert nf == ka["c1_default_blocks"]["samples"] == 2_760_933
+    assert sha(e) == ka["c1_default_blocks"]["edges"]
+
+
+@pytest.mark.parametrize("case", GOLD["ref_generate"], ids=lambda c: c["table"])
+def test_oracle_ref_generate_matches_reference(case):
+    e, nf = oracle.ref_generate(otable(case["table"]), case["k"], case["m"], case["seed"],
+                                case["block_size"])
+    assert nf == case["samples"]
+    assert sha(e) == case["edges"]
+
+
+@pytest.mark.parametrize("case", GOLD["philox_words"], ids=lambda c: str(c["payload"]))
+def test_oracle_philox4x64_is_numpys_stream(case):
+    """Pins the reference RNG convention: numpy Philox word i = philox(ctr=i/4+1)[i%4]."""
+    M = 2**64 - 1
+    got = oracle.ref_words((case["seed"] ^ case["domain"]) & M, case["payload"] & M, 9)
+    assert [int(x) for x in got] == case["words"]
+    # and numpy itself agrees on this box
+    import numpy.random as npr
+    g = npr.Philox(key=np.array([(case["seed"] ^ case["domain"]) & M, case["payload"] & M],
+                                dtype=np.uint64))
+    assert [int(x) for x in g.random_raw(9)] == case["words"]
+
+
+def test_philox4x32_known_answers():
+    """Random123 known-answer vectors for Philox4x32-10 (the fast path's generator)."""
+    assert [hex(x) for x in oracle.philox4x32([0, 0, 0, 0], [0, 0])] == \
+        ["0x6627e8d5", "0xe169c58d", "0xbc57ac4c", "0x9b00dbd8"]
+    assert [hex(x) for x in oracle.philox4x32([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2)] == \
+        ["0x408f276d", "0x41c83b0e", "0xa20bc7c6", "0x6d5451fd"]
+    assert [hex(x) for x in oracle.philox4x32([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344],
+                                              [0xA4093822, 0x299F31D0])] == \
+        ["0xd16cfe09", "0x94fdcceb", "0x5001e420", "0x24126ea1"]
+
+
+def test_philox4x64_known_answers():
+    assert [hex(x) for x in oracle.philox4x64([0, 0, 0, 0], [0, 0])] == \
+        ["0x16554d9eca36314c", "0xdb20fe9d672d0fdc", "0xd7e772cee186176b", "0x7e68b68aec7ba23b"]
+    assert [hex(x) for x in oracle.philox4x64([2**64 - 1] * 4, [2**64 - 1] * 2)] == \
+        ["0x87b092c3013fe90b", "0x438c3c67be8d0224", "0x9cc7d7c69cd777b6", "0xa09caebf594f0ba0"]
+
+
+@pytest.mark.parametrize("tag", ["g500:v1024", "g500:v16384", "g500:v253", "g500:f1"])
+def test_fast_words_feed_the_normative_loop(tag):
+    """Fast-path streams are (words, normative loop): oracle.fast_stream == emit(fast_words)."""
+    ot = otable(tag)
+    for k in (3, 16, 28, 33):
+        e1, nf1 = oracle.fast_stream(ot, k, 500, 11, 7)
+        words = oracle.fast_words(ot, 11, oracle.DOMAIN_BLOCK, 7, nf1 + 10)
+        e2, nf2 = oracle.emit(ot, k, 500, words)
+        assert nf1 == nf2 and (e1 == e2).all()
+
+
+def test_fast_words_scheme_p_fraction_layout():
+    """Scheme P: bucket = w bits [2,2+lg); fraction = top 32-F bits of w + low F of the lazy word."""
+    ot = otable("g500:v16384")  # lg 14 -> F 16
+    words = oracle.fast_words(ot, 3, oracle.DOMAIN_BLOCK, 5, 64)
+    key = (3 ^ oracle.DOMAIN_BLOCK) & (2**64 - 1)
+    for i in (0, 1, 2, 3, 17, 63):
+        w = oracle.philox4x32([i >> 2, 0, 5, 0], [key & 0xFFFFFFFF, key >> 32])[i & 3]
+        z = oracle.philox4x32([i >> 2, 1, 5, 0], [key & 0xFFFFFFFF, key >> 32])[i & 3]
+        want = (((int(w) >> 2) & 0x3FFF) << 32) | (int(w) & 0xFFFF0000) | (int(z) & 0xFFFF)
+        assert int(words[i]) == want
