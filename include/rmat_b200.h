@@ -75,6 +75,7 @@ typedef struct {
   uint64_t out_row;
   uint64_t row_prefix;  /* OR'd into every row endpoint (tile prefix, else 0) */
   uint64_t col_prefix;
+  uint64_t key_tweak;   /* XORed into seed ^ domain for this segment's Philox key (tiles) */
 } rmat_segment;
 
 typedef enum {
@@ -129,6 +130,8 @@ typedef struct {
   void* out;                  /* device; row 0 = first row of first_block */
   uint64_t* samples_per_block; /* device, optional */
   uint64_t* samples_total;    /* device, optional */
+  uint64_t row_prefix;        /* OR'd into every endpoint (partition tiles), else 0 */
+  uint64_t col_prefix;
 } rmat_refstream_args;
 
 rmat_status rmat_generate_refstream(const rmat_refstream_args* args, void* cuda_stream);

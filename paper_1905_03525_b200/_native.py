@@ -68,7 +68,7 @@ class TableInfo(ctypes.Structure):
 class Segment(ctypes.Structure):
     _fields_ = [("sid_base", ctypes.c_uint64), ("edge_count", ctypes.c_uint64),
                 ("out_row", ctypes.c_uint64), ("row_prefix", ctypes.c_uint64),
-                ("col_prefix", ctypes.c_uint64)]
+                ("col_prefix", ctypes.c_uint64), ("key_tweak", ctypes.c_uint64)]
 
 
 class GenArgs(ctypes.Structure):
@@ -87,7 +87,8 @@ class RefArgs(ctypes.Structure):
                 ("domain", ctypes.c_uint64), ("block_size", ctypes.c_uint64),
                 ("edge_count", ctypes.c_uint64), ("first_block", ctypes.c_uint64),
                 ("n_blocks", ctypes.c_uint64), ("out", ctypes.c_void_p),
-                ("samples_per_block", ctypes.c_void_p), ("samples_total", ctypes.c_void_p)]
+                ("samples_per_block", ctypes.c_void_p), ("samples_total", ctypes.c_void_p),
+                ("row_prefix", ctypes.c_uint64), ("col_prefix", ctypes.c_uint64)]
 
 
 KERNEL_AUTO, KERNEL_PACKED_SMEM, KERNEL_PACKED_GLOBAL, KERNEL_GENERIC = 0, 1, 2, 3

@@ -77,6 +77,32 @@ RMAT_HD u64x4 philox4x64_10(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
   return u64x4{c0, c1, c2, c3};
 }
 
+// Philox4x32-10 with a precomputed key schedule rk[2r], rk[2r+1] = round-r key
+// (the fast kernel reads it from the constant bank: no key adds in the loop).
+RMAT_HD u32x4 philox4x32_10_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                               const uint32_t* rk) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0, lo0, hi1, lo1;
+    mul_wide32(M0, c0, hi0, lo0);
+    mul_wide32(M1, c2, hi1, lo1);
+    uint32_t n0 = hi1 ^ c1 ^ rk[2 * r];
+    uint32_t n2 = hi0 ^ c3 ^ rk[2 * r + 1];
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  return u32x4{c0, c1, c2, c3};
+}
+
+RMAT_HD void philox4x32_key_schedule(uint32_t k0, uint32_t k1, uint32_t* rk) {
+  for (int r = 0; r < 10; ++r) {
+    rk[2 * r] = k0;
+    rk[2 * r + 1] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Fast-path stream spec.  key = seed ^ domain,
 // stream id sid occupies counter words 2..3, the per-stream call index j

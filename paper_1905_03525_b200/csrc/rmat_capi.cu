@@ -119,16 +119,19 @@ rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaS
   int threads, blocks;
   size_t smem = 0;
   if (SMEM) {
-    smem = t->packed_bytes;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return RMAT_ERR_CUDA;
     threads = 1024;
+    smem = t->packed_bytes + (size_t)threads * rmat::kStageBytes;
     blocks = sms;
   } else {
     threads = 256;
+    smem = (size_t)threads * rmat::kStageBytes;
+  }
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return RMAT_ERR_CUDA;
+  if (!SMEM) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess)
       return RMAT_ERR_CUDA;
     blocks = sms * std::max(per_sm, 1);
   }
@@ -276,7 +279,8 @@ rmat_status rmat_table_create(int device, const rmat_table_desc* d, rmat_table**
     if (st) { free_table(t); return st; }
     t->fb = fb;
     t->packed_bytes = n * (fb == 16 ? 12ull : 20ull);
-    t->packed_smem = t->packed_bytes <= (uint64_t)max_smem_optin(device) ? 1u : 0u;
+    t->packed_smem =
+        t->packed_bytes + 1024ull * rmat::kStageBytes <= (uint64_t)max_smem_optin(device) ? 1u : 0u;
   }
   t->device_bytes = bytes;
   *out = t;
@@ -328,7 +332,7 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
     if ((s.row_prefix & kmask) || (s.col_prefix & kmask)) return RMAT_ERR_INVALID;
     const uint64_t top = s.row_prefix | s.col_prefix | kmask;
     if (a->out_width == 4 && (top >> 32)) return RMAT_ERR_INVALID;
-    prefix = prefix || s.row_prefix || s.col_prefix;
+    prefix = prefix || s.row_prefix || s.col_prefix || s.key_tweak;
     streams_total += (s.edge_count + E - 1) / E;
   }
   if (streams_total == 0) return RMAT_OK;
@@ -337,7 +341,10 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
   const bool out64 = a->out_width == 8;
   const bool count = a->samples_total || a->samples_per_stream;
   int kernel = a->kernel;
-  const bool packed_ok = t->fb != 0 && t->dmax <= a->k && a->k <= 33;
+  // one edge per sample at most (dmax <= k), 33-bit accumulators, and a
+  // 32-bit Philox call index: E * k / dmin samples < 2^34.
+  const bool packed_ok = t->fb != 0 && t->dmax <= a->k && a->k <= 33 &&
+                         (double)E * a->k / t->dmin < 17179869184.0;
   if (kernel == RMAT_KERNEL_AUTO)
     kernel = packed_ok ? (t->packed_smem ? RMAT_KERNEL_PACKED_SMEM : RMAT_KERNEL_PACKED_GLOBAL)
                        : RMAT_KERNEL_GENERIC;
@@ -354,6 +361,7 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
     g.k = a->k;
     g.k0 = (uint32_t)key;
     g.k1 = (uint32_t)(key >> 32);
+    rmat::philox4x32_key_schedule(g.k0, g.k1, g.rk);
     g.E = E;
     g.out = a->out;
     g.samples_total = a->samples_total;
@@ -369,6 +377,7 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
       dv.row_prefix = s.row_prefix;
       dv.col_prefix = s.col_prefix;
       dv.stream_begin = stream_begin;
+      dv.key = key ^ s.key_tweak;
       stream_begin += (s.edge_count + E - 1) / E;
     }
     g.nseg = nseg;

@@ -16,6 +16,7 @@ struct SegDev {
   uint64_t row_prefix;
   uint64_t col_prefix;
   uint64_t stream_begin;
+  uint64_t key;  // Philox key of the segment's streams: seed ^ domain ^ key_tweak
 };
 
 // ---------------------------------------------------------------------------
@@ -55,6 +56,7 @@ struct GenericTab {
 struct GenLaunch {
   uint32_t k;           // bits per endpoint emitted by the stream
   uint32_t k0, k1;      // Philox key = seed ^ domain
+  uint32_t rk[20];      // its round keys (philox4x32_key_schedule)
   uint32_t nseg;
   uint64_t E;           // edges per stream
   uint64_t total_streams;

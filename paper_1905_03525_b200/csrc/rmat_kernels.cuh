@@ -44,6 +44,7 @@ struct StreamPos {
   uint64_t left;      // edges still to emit
   uint64_t row;       // first output row
   uint64_t rpre, cpre;
+  uint32_t k0, k1;    // segment key
   bool valid;
 };
 
@@ -59,6 +60,8 @@ __device__ __forceinline__ StreamPos open_stream(const GenLaunch& g, uint64_t s)
   p.row = sg.out_row + first;
   p.rpre = sg.row_prefix;
   p.cpre = sg.col_prefix;
+  p.k0 = (uint32_t)sg.key;
+  p.k1 = (uint32_t)(sg.key >> 32);
   return p;
 }
 
@@ -84,15 +87,58 @@ template <> struct AEntry<32> { using T = uint4; };
 // accumulator chain, issued first), one rare-path branch for fraction ties,
 // then 4 accumulator steps.  The accumulator keeps stale bits above its f
 // valid bits; they never reach an edge because edges are masked to k bits.
+//
+// Edges are staged per thread in shared memory (4 slots of 8 B, slot-major)
+// and leave as one 32-byte store per full sector, so DRAM only ever sees
+// whole sectors (8-byte scattered stores made L2 read-modify-write them).
 // ---------------------------------------------------------------------------
+constexpr uint32_t kStageBytes = 32;  // per thread: one DRAM sector
+
+template <bool OUT64>
+__device__ __forceinline__ void store_sector(char* gptr, const uint8_t* st, uint32_t stride) {
+  // slots 0..3 (u32 pairs) or 0..1 (u64 pairs) -> one 256-bit store
+  uint32_t v[8];
+  if (OUT64) {
+    const uint4 e0 = *reinterpret_cast<const uint4*>(st);
+    const uint4 e1 = *reinterpret_cast<const uint4*>(st + stride);
+    v[0] = e0.x; v[1] = e0.y; v[2] = e0.z; v[3] = e0.w;
+    v[4] = e1.x; v[5] = e1.y; v[6] = e1.z; v[7] = e1.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint2 e = *reinterpret_cast<const uint2*>(st + q * stride);
+      v[2 * q] = e.x; v[2 * q + 1] = e.y;
+    }
+  }
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(gptr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
+template <bool OUT64>
+__device__ __forceinline__ void store_slots(char* gptr, const uint8_t* st, uint32_t stride,
+                                            uint32_t lo, uint32_t hi) {
+  // partial sector (stream head / tail): slot by slot
+  constexpr uint32_t EB = OUT64 ? 16 : 8;
+  for (uint32_t q = lo; q < hi; ++q) {
+    if (OUT64)
+      *reinterpret_cast<uint4*>(gptr + q * EB) = *reinterpret_cast<const uint4*>(st + q * stride);
+    else
+      *reinterpret_cast<uint2*>(gptr + q * EB) = *reinterpret_cast<const uint2*>(st + q * stride);
+  }
+}
+
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT>
 __global__ void __launch_bounds__(SMEM ? 1024 : 256, 1)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
+  constexpr uint32_t EB = OUT64 ? 16 : 8;       // bytes per edge
+  constexpr uint32_t G = kStageBytes / EB;      // edges per sector
   extern __shared__ __align__(16) uint8_t smem[];
 
   const uint8_t* baseA;
   const uint8_t* baseB;
+  uint8_t* stage;
   if (SMEM) {
     // Stage the bucket arrays: A first (16B aligned), then B.
     const uint32_t n = tab.n;
@@ -107,33 +153,41 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     __syncthreads();
     baseA = smem;
     baseB = smem + abytes;
+    stage = smem + abytes + bbytes;
   } else {
     baseA = reinterpret_cast<const uint8_t*>(tab.A);
     baseB = reinterpret_cast<const uint8_t*>(tab.B);
+    stage = smem;
   }
+  // slot q of this thread lives at stage + q * sstride + threadIdx.x * EB
+  const uint32_t sstride = blockDim.x * EB;
+  uint8_t* const mystage = stage + threadIdx.x * EB;
 
   const uint32_t k = g.k;
   const uint32_t kmask = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
-  const uint32_t k0 = g.k0, k1 = g.k1;
   const uint32_t idxmask4 = tab.idxmask4, fm = tab.fm;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
 
   StreamPos p = open_stream(g, s);
   if (!p.valid) return;
-  uint64_t j = 0;                    // Philox call index within the stream
+  uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
   uint32_t cur_r = 0, cur_c = 0, f = 0;
   uint64_t total_nf = 0;
-  uint32_t ebits = 0;                // COUNT: samples of the current call that stored an edge
-  char* optr = reinterpret_cast<char*>(g.out) + p.row * (OUT64 ? 16 : 8);
-  int left = (int)p.left;
+  uint32_t ebits = 0;                // COUNT: samples of the current call that produced an edge
+  uint32_t left = (uint32_t)p.left;  // edges still to produce
+  char* gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+  uint32_t slot = (uint32_t)(p.row & (G - 1));  // next staging slot = position in the sector
+  uint32_t head = slot;                         // first valid slot of the current sector
 
   for (;;) {
-    if (left <= 0) {
+    if (left == 0) {
+      // Stream done: write the partial last sector, account nf, open the next.
+      if (slot > head) store_slots<OUT64>(gptr, mystage, sstride, head, slot);
       if (COUNT) {
-        // nf (generator.py:255-257) = index of the sample that produced the
-        // stream's last edge + 1: the highest sample of call j-1 that stored.
-        const uint64_t nf = 4 * (j - 1) + (32 - __clz(ebits));
+        // nf (generator.py:255-257): the highest sample of call j-1 that
+        // produced an edge this stream needed.
+        const uint64_t nf = 4ull * (j - 1) + (32 - __clz(ebits));
         total_nf += nf;
         if (g.samples_per_stream) g.samples_per_stream[s] = nf;
       }
@@ -141,10 +195,16 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       p = open_stream(g, s);
       if (!p.valid) break;
       j = 0; cur_r = cur_c = f = 0;
-      optr = reinterpret_cast<char*>(g.out) + p.row * (OUT64 ? 16 : 8);
-      left = (int)p.left;
+      left = (uint32_t)p.left;
+      gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+      slot = head = (uint32_t)(p.row & (G - 1));
     }
-    const u32x4 w4 = stream_call(j, 0, p.sid, k0, k1);
+    u32x4 w4;
+    if (PREFIX) {
+      w4 = stream_call(j, 0, p.sid, p.k0, p.k1);  // tile segments: per-stream key
+    } else {
+      w4 = philox4x32_10_rk(j, 0, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), g.rk);
+    }
     const uint32_t wq[4] = {w4.x, w4.y, w4.z, w4.w};
     uint32_t bq[4];
     AE aq[4];
@@ -155,18 +215,22 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       const uint32_t a4 = wq[t] & idxmask4;
       bq[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
       aq[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
-      // B = T_hi | d_alias << 8 | d_self; the fields sit below T_hi, so these
-      // compare the fraction's top bits H against T_hi only.
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      // B = T_hi | d_alias << 8 | d_self with the fields below T_hi (F >= 16
+      // bits): compare the fraction's top bits H = w & ~fm with T_hi.
       ltq[t] = (wq[t] | fm) < bq[t];                 // H <  T_hi
-      tie |= !ltq[t] && (wq[t] & ~fm) <= bq[t];      // H == T_hi
+      tie |= ((wq[t] ^ bq[t]) & ~fm) == 0;           // H == T_hi
     }
     if (tie) {
-      // Rare (p ~ 2^-(32-F) per sample): decide ties with the lazy word.
-      const u32x4 z4 = stream_call(j, 1, p.sid, k0, k1);
+      // Rare (2^-(32-F) per sample): decide ties with the lazy word's low bits.
+      const u32x4 z4 = PREFIX ? stream_call(j, 1, p.sid, p.k0, p.k1)
+                              : philox4x32_10_rk(j, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), g.rk);
       const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (!ltq[t] && (wq[t] & ~fm) <= bq[t])
+        if (((wq[t] ^ bq[t]) & ~fm) == 0)
           ltq[t] = (zq[t] & fm) < __ldg(tab.tlo + ((wq[t] & idxmask4) >> 2));
     }
     if (COUNT) ebits = 0;
@@ -193,7 +257,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       cur_r = vr;
       cur_c = vc;
       f = over;
-      const bool st = emit && left > 0;
+      const bool st = emit && left != 0;
       if (st) {
         uint64_t u = __funnelshift_r(vr, vrh, over) & kmask;
         uint64_t v = __funnelshift_r(vc, vch, over) & kmask;
@@ -202,15 +266,21 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           v |= (uint64_t)((vch >> over) & (k > 32 ? 1u : 0u)) << 32;
         }
         if (PREFIX) { u |= p.rpre; v |= p.cpre; }
+        uint8_t* sp = mystage + slot * sstride;
         if constexpr (OUT64) {
-          *reinterpret_cast<ulonglong2*>(optr) = make_ulonglong2(u, v);
+          *reinterpret_cast<ulonglong2*>(sp) = make_ulonglong2(u, v);
         } else {
-          *reinterpret_cast<uint2*>(optr) = make_uint2((uint32_t)u, (uint32_t)v);
+          *reinterpret_cast<uint2*>(sp) = make_uint2((uint32_t)u, (uint32_t)v);
+        }
+        --left;
+        if (++slot == G) {
+          if (head == 0) store_sector<OUT64>(gptr, mystage, sstride);
+          else store_slots<OUT64>(gptr, mystage, sstride, head, G);  // unaligned stream head
+          gptr += kStageBytes;
+          slot = head = 0;
         }
       }
       if (COUNT) ebits |= (uint32_t)st << t;
-      optr += emit ? (OUT64 ? 16 : 8) : 0;
-      left -= emit;
     }
     ++j;
   }
@@ -240,7 +310,7 @@ k_generic(const GenericTab tab, const __grid_constant__ GenLaunch g) {
     while (left > 0) {
       uint32_t idx, lt;
       if (tab.scheme_p) {
-        if ((i & 3) == 0) cache = stream_call(i >> 2, 0, p.sid, g.k0, g.k1);
+        if ((i & 3) == 0) cache = stream_call(i >> 2, 0, p.sid, p.k0, p.k1);
         const uint32_t w = pick4(cache, (uint32_t)(i & 3));
         idx = (w >> 2) & (n - 1);
         const uint32_t Tv = tab.T[idx];
@@ -248,11 +318,11 @@ k_generic(const GenericTab tab, const __grid_constant__ GenLaunch g) {
         if (hi != thi) {
           lt = hi < thi;
         } else {
-          const uint32_t z = pick4(stream_call(i >> 2, 1, p.sid, g.k0, g.k1), (uint32_t)(i & 3));
+          const uint32_t z = pick4(stream_call(i >> 2, 1, p.sid, p.k0, p.k1), (uint32_t)(i & 3));
           lt = (z & fm) < (Tv & fm);
         }
       } else {
-        if ((i & 1) == 0) cache = stream_call(i >> 1, 0, p.sid, g.k0, g.k1);
+        if ((i & 1) == 0) cache = stream_call(i >> 1, 0, p.sid, p.k0, p.k1);
         const uint32_t w1 = (i & 1) ? cache.z : cache.x;
         const uint32_t w2 = (i & 1) ? cache.w : cache.y;
         idx = ((n & (n - 1)) == 0) ? (w1 & (n - 1)) : (w1 % n);

@@ -37,6 +37,7 @@ struct RefLaunch {
   void* out;
   uint64_t* samples_per_block;
   uint64_t* samples_total;
+  uint64_t rpre, cpre;
 };
 
 __device__ __forceinline__ uint64_t lowmask64(uint32_t w) {
@@ -146,9 +147,11 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
       }
       const uint64_t row = b * g.B + emitted + e - g.first_block * g.B;
       if (OUT64) {
-        reinterpret_cast<ulonglong2*>(g.out)[row] = make_ulonglong2(ur & kmask, uc & kmask);
+        reinterpret_cast<ulonglong2*>(g.out)[row] =
+            make_ulonglong2((ur & kmask) | g.rpre, (uc & kmask) | g.cpre);
       } else {
-        reinterpret_cast<uint2*>(g.out)[row] = make_uint2((uint32_t)ur, (uint32_t)uc);
+        reinterpret_cast<uint2*>(g.out)[row] =
+            make_uint2((uint32_t)(ur | g.rpre), (uint32_t)(uc | g.cpre));
       }
     }
     // 4. carry / nf (one thread), then advance
@@ -220,6 +223,8 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
   g.out = a.out;
   g.samples_per_block = a.samples_per_block;
   g.samples_total = a.samples_total;
+  g.rpre = a.row_prefix;
+  g.cpre = a.col_prefix;
   const uint64_t nb = a.n_blocks;
   for (uint64_t done = 0; done < nb;) {
     const uint64_t cnt = std::min<uint64_t>(nb - done, 1u << 30);

@@ -133,7 +133,8 @@ def launch_generate(dt: DeviceTable, k: int, seed: int, domain: int, edges_per_s
 
 def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size: int,
                      edge_count: int, first_block: int, n_blocks: int, out, *,
-                     samples_per_block=None, samples_total=None) -> None:
+                     samples_per_block=None, samples_total=None, row_prefix: int = 0,
+                     col_prefix: int = 0) -> None:
     import torch
 
     assert out.device == dt.device and out.is_contiguous()
@@ -143,7 +144,8 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
         n_blocks=n_blocks, out=out.data_ptr() if out.numel() else None,
         samples_per_block=(samples_per_block.data_ptr()
                            if samples_per_block is not None else None),
-        samples_total=samples_total.data_ptr() if samples_total is not None else None)
+        samples_total=samples_total.data_ptr() if samples_total is not None else None,
+        row_prefix=row_prefix, col_prefix=col_prefix)
     with torch.cuda.device(dt.device):
         N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), _stream_ptr(dt.device)),
                 "rmat_generate_refstream")

@@ -1,0 +1,99 @@
+"""Streaming generation into host memory (the end-to-end public path).
+
+`generate_to_host` produces rows [r_lo, r_hi) of `generate(config)` into a
+pinned host buffer with device generation and device->host copies
+overlapped: chunk i is generated on the compute stream while chunk i-1 is
+copied on a copy stream, double-buffered in HBM.  This is the call a user
+makes when the edges are wanted on the host (the reference's return type),
+and what bench.py's `e2e` leg times.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .device import DeviceTable, device_table, launch_generate, launch_refstream, require_cuda
+from .generator import DOMAIN_BLOCK, GenConfig, edge_dtype, shard_rows
+from .params import check_k
+
+__all__ = ["generate_to_host", "DEFAULT_CHUNK_EDGES"]
+
+DEFAULT_CHUNK_EDGES = 1 << 28
+
+
+def generate_to_host(config: GenConfig, out=None, *, rank: int = 0, world: int = 1, device=None,
+                     chunk_edges: int = DEFAULT_CHUNK_EDGES, fresh_table: bool = False) -> dict:
+    """Rows of shard `rank`/`world` into host memory; returns {'out', 'r_lo', 'h2d_bytes'}.
+
+    out: None (a pinned torch tensor is allocated) or a (rows, 2) CPU tensor /
+    numpy array of the device edge width (4-byte for k <= 32, else 8-byte).
+    fresh_table: upload the table again (counted in h2d_bytes) instead of
+    reusing the cached device copy.
+    """
+    import torch
+
+    k = config.params.k
+    check_k(k)
+    dev = require_cuda(device)
+    B = config.stream_edges
+    s_lo, s_hi, r_lo, r_hi = shard_rows(config.edge_count, B, rank, world)
+    rows = r_hi - r_lo
+    dt_edge = edge_dtype(k)
+    width = 4 if k <= 32 else 8
+    if out is None:
+        out = torch.empty((rows, 2), dtype=torch.int32 if width == 4 else torch.int64,
+                          pin_memory=True)
+    if isinstance(out, np.ndarray):
+        out = torch.from_numpy(out)
+    if tuple(out.shape) != (rows, 2) or out.element_size() != width or out.device.type != "cpu":
+        raise ValueError(f"out must be a ({rows}, 2) host buffer of {width}-byte endpoints")
+    out_dev_view = out.view(torch.int32 if width == 4 else torch.int64)
+
+    if fresh_table:
+        dt = DeviceTable(config.table, dev)
+        h2d = sum(a.nbytes for a in (dt.thr32, dt.alias, dt.row, dt.col, dt.depth))
+    else:
+        dt = device_table(config.table, dev)
+        h2d = 0
+    if rows == 0:
+        return {"out": out, "r_lo": r_lo, "h2d_bytes": h2d}
+
+    # chunk = whole streams
+    streams_per_chunk = max(1, chunk_edges // B)
+    chunk_rows = streams_per_chunk * B
+    nbuf = 2 if rows > chunk_rows else 1
+    bufs = [torch.empty((min(chunk_rows, rows), 2), dtype=dt_edge, device=dev) for _ in range(nbuf)]
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    done_gen = [torch.cuda.Event() for _ in range(nbuf)]
+    done_copy = [None] * nbuf
+    s = s_lo
+    i = 0
+    while s < s_hi:
+        ns = min(streams_per_chunk, s_hi - s)
+        c_lo = s * B
+        c_hi = min((s + ns) * B, config.edge_count)
+        n = c_hi - c_lo
+        b = i % nbuf
+        buf = bufs[b][:n]
+        if done_copy[b] is not None:
+            compute.wait_event(done_copy[b])
+        if config.rng == "reference":
+            launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, config.edge_count, s, ns, buf)
+        else:
+            launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B, [(s, n, 0, 0, 0)], buf)
+        done_gen[b].record(compute)
+        with torch.cuda.stream(copy):
+            copy.wait_event(done_gen[b])
+            dst = out_dev_view[c_lo - r_lo:c_hi - r_lo]
+            dst.copy_(buf.view(dst.dtype), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            done_copy[b] = ev
+        s += ns
+        i += 1
+    copy.synchronize()
+    compute.synchronize()
+    if fresh_table:
+        dt.close()
+    return {"out": out, "r_lo": r_lo, "h2d_bytes": h2d}
