@@ -119,12 +119,12 @@ rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaS
   int threads, blocks;
   size_t smem = 0;
   if (SMEM) {
-    threads = 1024;
-    smem = t->packed_bytes + (size_t)threads * rmat::kStageBytes;
+    threads = rmat::kSmemThreads;
+    smem = t->packed_bytes + (size_t)threads * rmat::kRingBytes;
     blocks = sms;
   } else {
-    threads = 256;
-    smem = (size_t)threads * rmat::kStageBytes;
+    threads = rmat::kGlobalThreads;
+    smem = (size_t)threads * rmat::kRingBytes;
   }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
@@ -280,7 +280,8 @@ rmat_status rmat_table_create(int device, const rmat_table_desc* d, rmat_table**
     t->fb = fb;
     t->packed_bytes = n * (fb == 16 ? 12ull : 20ull);
     t->packed_smem =
-        t->packed_bytes + 1024ull * rmat::kStageBytes <= (uint64_t)max_smem_optin(device) ? 1u : 0u;
+        t->packed_bytes + (uint64_t)rmat::kSmemThreads * rmat::kRingBytes <=
+            (uint64_t)max_smem_optin(device) ? 1u : 0u;
   }
   t->device_bytes = bytes;
   *out = t;

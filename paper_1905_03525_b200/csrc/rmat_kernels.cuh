@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "philox.cuh"
 #include "rmat_device.cuh"
 
@@ -76,6 +78,13 @@ __device__ __forceinline__ void store_edge(void* out, uint64_t row, uint64_t u, 
   }
 }
 
+// PRMT with selectors whose nibbles are already < 8 (no & 0x7777 needed).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(a), "r"(sel));
+  return r;
+}
+
 template <int FB> struct AEntry;
 template <> struct AEntry<16> { using T = uint2; };
 template <> struct AEntry<32> { using T = uint4; };
@@ -88,52 +97,74 @@ template <> struct AEntry<32> { using T = uint4; };
 // then 4 accumulator steps.  The accumulator keeps stale bits above its f
 // valid bits; they never reach an edge because edges are masked to k bits.
 //
-// Edges are staged per thread in shared memory (4 slots of 8 B, slot-major)
-// and leave as one 32-byte store per full sector, so DRAM only ever sees
-// whole sectors (8-byte scattered stores made L2 read-modify-write them).
+// Output: every edge is staged in a per-thread shared-memory ring of 2G slots
+// (G = edges per 32-byte DRAM sector; slot-major so a warp's staging stores
+// hit distinct banks), indexed by output row mod 2G.  After every G samples
+// at most one sector can have completed; it leaves as a single 32-byte
+// store, so DRAM sees whole sectors and the per-sample path has no branch.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kStageBytes = 32;  // per thread: one DRAM sector
+constexpr uint32_t kSectorBytes = 32;
+constexpr uint32_t kRingBytes = 2 * kSectorBytes;  // staging bytes per thread
+constexpr int kSmemThreads = 512;                   // packed_smem CTA size
+constexpr int kGlobalThreads = 256;                 // packed_global CTA size
 
-template <bool OUT64>
-__device__ __forceinline__ void store_sector(char* gptr, const uint8_t* st, uint32_t stride) {
-  // slots 0..3 (u32 pairs) or 0..1 (u64 pairs) -> one 256-bit store
-  uint32_t v[8];
-  if (OUT64) {
-    const uint4 e0 = *reinterpret_cast<const uint4*>(st);
-    const uint4 e1 = *reinterpret_cast<const uint4*>(st + stride);
-    v[0] = e0.x; v[1] = e0.y; v[2] = e0.z; v[3] = e0.w;
-    v[4] = e1.x; v[5] = e1.y; v[6] = e1.z; v[7] = e1.w;
-  } else {
+template <bool OUT64, int THREADS>
+__device__ __forceinline__ void flush_sector(char* gptr, const uint8_t* ring, uint32_t half,
+                                             uint32_t lo) {
+  constexpr uint32_t EB = OUT64 ? 16 : 8;
+  constexpr uint32_t G = kSectorBytes / EB;
+  constexpr uint32_t STRIDE = THREADS * EB;
+  const uint8_t* st = ring + half * G * STRIDE;
+  if (lo == 0) {
+    uint32_t v[8];
+    if (OUT64) {
+      const uint4 e0 = *reinterpret_cast<const uint4*>(st);
+      const uint4 e1 = *reinterpret_cast<const uint4*>(st + STRIDE);
+      v[0] = e0.x; v[1] = e0.y; v[2] = e0.z; v[3] = e0.w;
+      v[4] = e1.x; v[5] = e1.y; v[6] = e1.z; v[7] = e1.w;
+    } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint2 e = *reinterpret_cast<const uint2*>(st + q * stride);
-      v[2 * q] = e.x; v[2 * q + 1] = e.y;
+      for (int q = 0; q < 4; ++q) {
+        const uint2 e = *reinterpret_cast<const uint2*>(st + q * STRIDE);
+        v[2 * q] = e.x; v[2 * q + 1] = e.y;
+      }
+    }
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(gptr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+  } else {
+    for (uint32_t q = lo; q < G; ++q) {  // a stream's unaligned first sector
+      if (OUT64)
+        *reinterpret_cast<uint4*>(gptr + q * EB) = *reinterpret_cast<const uint4*>(st + q * STRIDE);
+      else
+        *reinterpret_cast<uint2*>(gptr + q * EB) = *reinterpret_cast<const uint2*>(st + q * STRIDE);
     }
   }
-  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(gptr), "r"(v[0]),
-               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-               : "memory");
 }
 
-template <bool OUT64>
-__device__ __forceinline__ void store_slots(char* gptr, const uint8_t* st, uint32_t stride,
-                                            uint32_t lo, uint32_t hi) {
-  // partial sector (stream head / tail): slot by slot
+template <bool OUT64, int THREADS>
+__device__ __forceinline__ void flush_tail(char* gptr, const uint8_t* ring, uint32_t half,
+                                           uint32_t lo, uint32_t hi) {
   constexpr uint32_t EB = OUT64 ? 16 : 8;
-  for (uint32_t q = lo; q < hi; ++q) {
+  constexpr uint32_t G = kSectorBytes / EB;
+  constexpr uint32_t STRIDE = THREADS * EB;
+  const uint8_t* st = ring + half * G * STRIDE;
+  for (uint32_t q = lo; q < hi; ++q) {  // a stream's partial last sector
     if (OUT64)
-      *reinterpret_cast<uint4*>(gptr + q * EB) = *reinterpret_cast<const uint4*>(st + q * stride);
+      *reinterpret_cast<uint4*>(gptr + q * EB) = *reinterpret_cast<const uint4*>(st + q * STRIDE);
     else
-      *reinterpret_cast<uint2*>(gptr + q * EB) = *reinterpret_cast<const uint2*>(st + q * stride);
+      *reinterpret_cast<uint2*>(gptr + q * EB) = *reinterpret_cast<const uint2*>(st + q * STRIDE);
   }
 }
 
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT>
-__global__ void __launch_bounds__(SMEM ? 1024 : 256, 1)
+__global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, 1)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
+  constexpr int THREADS = SMEM ? kSmemThreads : kGlobalThreads;
   constexpr uint32_t EB = OUT64 ? 16 : 8;       // bytes per edge
-  constexpr uint32_t G = kStageBytes / EB;      // edges per sector
+  constexpr uint32_t G = kSectorBytes / EB;     // edges per sector (4 or 2)
+  constexpr uint32_t R = 2 * G;                 // ring slots
+  constexpr uint32_t STRIDE = THREADS * EB;     // slot-major ring
   extern __shared__ __align__(16) uint8_t smem[];
 
   const uint8_t* baseA;
@@ -146,10 +177,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     const size_t bbytes = (size_t)n * 4;
     const uint4* srcA = reinterpret_cast<const uint4*>(tab.A);
     uint4* dstA = reinterpret_cast<uint4*>(smem);
-    for (size_t i = threadIdx.x; i < abytes / 16; i += blockDim.x) dstA[i] = __ldg(srcA + i);
+    for (size_t i = threadIdx.x; i < abytes / 16; i += THREADS) dstA[i] = __ldg(srcA + i);
     const uint4* srcB = reinterpret_cast<const uint4*>(tab.B);
     uint4* dstB = reinterpret_cast<uint4*>(smem + abytes);
-    for (size_t i = threadIdx.x; i < bbytes / 16; i += blockDim.x) dstB[i] = __ldg(srcB + i);
+    for (size_t i = threadIdx.x; i < bbytes / 16; i += THREADS) dstB[i] = __ldg(srcB + i);
     __syncthreads();
     baseA = smem;
     baseB = smem + abytes;
@@ -159,15 +190,13 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     baseB = reinterpret_cast<const uint8_t*>(tab.B);
     stage = smem;
   }
-  // slot q of this thread lives at stage + q * sstride + threadIdx.x * EB
-  const uint32_t sstride = blockDim.x * EB;
-  uint8_t* const mystage = stage + threadIdx.x * EB;
+  uint8_t* const ring = stage + threadIdx.x * EB;  // slot q at ring + q * STRIDE
 
   const uint32_t k = g.k;
   const uint32_t kmask = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
   const uint32_t idxmask4 = tab.idxmask4, fm = tab.fm;
-  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t T = (uint64_t)gridDim.x * THREADS;
+  uint64_t s = (uint64_t)blockIdx.x * THREADS + threadIdx.x;
 
   StreamPos p = open_stream(g, s);
   if (!p.valid) return;
@@ -176,14 +205,20 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   uint64_t total_nf = 0;
   uint32_t ebits = 0;                // COUNT: samples of the current call that produced an edge
   uint32_t left = (uint32_t)p.left;  // edges still to produce
+  // roff = ring slot of the next output row (row mod R) times STRIDE.  The
+  // first unflushed sector starts at gptr, occupies ring half `half`, and is
+  // valid from slot lo.
+  // stage + roff = ring slot of the next edge; roff = slot * STRIDE + tid * EB
+  uint32_t roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
+  uint32_t half = roff / (G * STRIDE);
+  uint32_t lo = roff / STRIDE & (G - 1);
   char* gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
-  uint32_t slot = (uint32_t)(p.row & (G - 1));  // next staging slot = position in the sector
-  uint32_t head = slot;                         // first valid slot of the current sector
 
   for (;;) {
     if (left == 0) {
-      // Stream done: write the partial last sector, account nf, open the next.
-      if (slot > head) store_slots<OUT64>(gptr, mystage, sstride, head, slot);
+      // Stream done: write its partial last sector, account nf, open the next.
+      if ((roff / STRIDE & (G - 1)) > lo)
+        flush_tail<OUT64, THREADS>(gptr, ring, half, lo, roff / STRIDE & (G - 1));
       if (COUNT) {
         // nf (generator.py:255-257): the highest sample of call j-1 that
         // produced an edge this stream needed.
@@ -196,8 +231,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       if (!p.valid) break;
       j = 0; cur_r = cur_c = f = 0;
       left = (uint32_t)p.left;
+      roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
+      half = roff / (G * STRIDE);
+      lo = roff / STRIDE & (G - 1);
       gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
-      slot = head = (uint32_t)(p.row & (G - 1));
     }
     u32x4 w4;
     if (PREFIX) {
@@ -208,7 +245,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     const uint32_t wq[4] = {w4.x, w4.y, w4.z, w4.w};
     uint32_t bq[4];
     AE aq[4];
-    bool ltq[4];
+    // Fragment / depth byte selectors per sample (self: bytes 0-1 of A's
+    // halves and byte 0 of B; alias: bytes 2-3 and byte 1).  Kept as
+    // registers so no predicate has to survive the tie branch.
+    uint32_t selq[4], seldq[4];
     bool tie = false;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -220,8 +260,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     for (int t = 0; t < 4; ++t) {
       // B = T_hi | d_alias << 8 | d_self with the fields below T_hi (F >= 16
       // bits): compare the fraction's top bits H = w & ~fm with T_hi.
-      ltq[t] = (wq[t] | fm) < bq[t];                 // H <  T_hi
+      const bool lt = (wq[t] | fm) < bq[t];           // H <  T_hi
       tie |= ((wq[t] ^ bq[t]) & ~fm) == 0;           // H == T_hi
+      selq[t] = lt ? 0x4410u : 0x4432u;
+      seldq[t] = lt ? 0x4440u : 0x4441u;
     }
     if (tie) {
       // Rare (2^-(32-F) per sample): decide ties with the lazy word's low bits.
@@ -230,35 +272,40 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (((wq[t] ^ bq[t]) & ~fm) == 0)
-          ltq[t] = (zq[t] & fm) < __ldg(tab.tlo + ((wq[t] & idxmask4) >> 2));
+        if (((wq[t] ^ bq[t]) & ~fm) == 0) {
+          const bool lt = (zq[t] & fm) < __ldg(tab.tlo + ((wq[t] & idxmask4) >> 2));
+          selq[t] = lt ? 0x4410u : 0x4432u;
+          seldq[t] = lt ? 0x4440u : 0x4441u;
+        }
     }
-    if (COUNT) ebits = 0;
+    // Edges needed by this stream cap what the 4 samples may store; in the
+    // common case (>= 4 left in every lane) the per-sample check disappears.
+    auto step = [&](auto careful_tag) {
+      constexpr bool CAREFUL = decltype(careful_tag)::value;
+      if (COUNT) ebits = 0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const bool lt = ltq[t];
-      uint32_t r, c;
-      if constexpr (FB == 16) {
-        const uint32_t sel = lt ? 0x4410u : 0x4432u;
-        r = __byte_perm(aq[t].x, 0, sel);
-        c = __byte_perm(aq[t].y, 0, sel);
-      } else {
-        r = lt ? aq[t].x : aq[t].y;
-        c = lt ? aq[t].z : aq[t].w;
-      }
-      const uint32_t d = __byte_perm(bq[t], 0, lt ? 0x4440u : 0x4441u);
-      // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
-      const uint32_t pw = 1u << d;
-      const uint32_t tt = f + d;
-      const uint32_t vr = cur_r * pw + r, vrh = __umulhi(cur_r, pw);
-      const uint32_t vc = cur_c * pw + c, vch = __umulhi(cur_c, pw);
-      const bool emit = tt >= k;
-      const uint32_t over = emit ? tt - k : tt;
-      cur_r = vr;
-      cur_c = vc;
-      f = over;
-      const bool st = emit && left != 0;
-      if (st) {
+      for (int t = 0; t < 4; ++t) {
+        uint32_t r, c;
+        if constexpr (FB == 16) {
+          r = prmt(aq[t].x, selq[t]);
+          c = prmt(aq[t].y, selq[t]);
+        } else {
+          const bool lt = selq[t] == 0x4410u;
+          r = lt ? aq[t].x : aq[t].y;
+          c = lt ? aq[t].z : aq[t].w;
+        }
+        const uint32_t d = prmt(bq[t], seldq[t]);
+        // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
+        const uint32_t pw = 1u << d;
+        const uint32_t tt = f + d;
+        const uint32_t vr = cur_r * pw + r, vrh = __umulhi(cur_r, pw);
+        const uint32_t vc = cur_c * pw + c, vch = __umulhi(cur_c, pw);
+        const bool emit = tt >= k;
+        const uint32_t over = emit ? tt - k : tt;
+        cur_r = vr;
+        cur_c = vc;
+        f = over;
+        const bool st = CAREFUL ? (emit && left != 0) : emit;
         uint64_t u = __funnelshift_r(vr, vrh, over) & kmask;
         uint64_t v = __funnelshift_r(vc, vch, over) & kmask;
         if constexpr (OUT64) {
@@ -266,22 +313,31 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           v |= (uint64_t)((vch >> over) & (k > 32 ? 1u : 0u)) << 32;
         }
         if (PREFIX) { u |= p.rpre; v |= p.cpre; }
-        uint8_t* sp = mystage + slot * sstride;
-        if constexpr (OUT64) {
-          *reinterpret_cast<ulonglong2*>(sp) = make_ulonglong2(u, v);
-        } else {
-          *reinterpret_cast<uint2*>(sp) = make_uint2((uint32_t)u, (uint32_t)v);
+        if (st) {
+          uint8_t* sp = stage + roff;
+          if constexpr (OUT64) {
+            *reinterpret_cast<ulonglong2*>(sp) = make_ulonglong2(u, v);
+          } else {
+            *reinterpret_cast<uint2*>(sp) = make_uint2((uint32_t)u, (uint32_t)v);
+          }
+          // next slot; the mask keeps this thread's column bits (tid * EB < STRIDE)
+          roff = (roff + STRIDE) & (R * STRIDE - 1);
+          --left;
         }
-        --left;
-        if (++slot == G) {
-          if (head == 0) store_sector<OUT64>(gptr, mystage, sstride);
-          else store_slots<OUT64>(gptr, mystage, sstride, head, G);  // unaligned stream head
-          gptr += kStageBytes;
-          slot = head = 0;
+        if (COUNT) ebits |= (uint32_t)st << t;
+        if ((uint32_t)t % G == G - 1 && (roff / (G * STRIDE)) != half) {
+          // At most G edges since the last check: the sector at gptr is complete.
+          flush_sector<OUT64, THREADS>(gptr, ring, half, lo);
+          gptr += kSectorBytes;
+          half ^= 1;
+          lo = 0;
         }
       }
-      if (COUNT) ebits |= (uint32_t)st << t;
-    }
+    };
+    if (__all_sync(0xFFFFFFFFu, left >= 4))
+      step(std::false_type{});
+    else
+      step(std::true_type{});
     ++j;
   }
   if (COUNT && g.samples_total && total_nf)

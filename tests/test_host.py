@@ -1,0 +1,216 @@
+"""Host-side logic on CPU: parameter validation, tables, alias, config errors,
+shard arithmetic, partition plans -- mirroring the reference's unit tests
+(pkg/tests/test_params.py, test_table.py, test_alias.py, test_partition.py)."""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import G500, LESS_SKEWED, SKEWED, UNIFORM, params_for, variable_table
+from paper_1905_03525_b200 import (
+    BadExponent,
+    DepthOutOfRange,
+    GenConfig,
+    NegativeOrZeroWeight,
+    SizeLimitTooSmall,
+    SumOutOfTolerance,
+    build_alias,
+    build_fixed_table,
+    build_variable_table,
+    entropy,
+    shard_rows,
+    speedup_bound,
+    table_stats,
+    validate,
+)
+from paper_1905_03525_b200.alias import AllZeroWeights, EmptyInput, NegativeWeight, alias_sample
+from paper_1905_03525_b200.partition import (
+    PartitionPlan,
+    default_plan,
+    part_segments,
+    plan_tiles,
+    split_quadrant_counts,
+    tile_key,
+)
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+
+
+# ------------------------------------------------------------------ params
+def test_validate_normalises_and_is_idempotent():
+    p = validate(0.57, 0.19, 0.19, 0.05, 20)
+    assert p.a + p.b + p.c + p.d == 1.0
+    assert validate(*p.quadrants, 20) == p
+
+
+@pytest.mark.parametrize("bad", [(0, 0.5, 0.25, 0.25), (-0.1, 0.6, 0.25, 0.25),
+                                 (float("nan"), 0.5, 0.25, 0.25)])
+def test_validate_rejects_nonpositive(bad):
+    with pytest.raises(NegativeOrZeroWeight):
+        validate(*bad, 10)
+
+
+def test_validate_rejects_bad_sum():
+    with pytest.raises(SumOutOfTolerance):
+        validate(0.5, 0.2, 0.2, 0.2, 10)
+
+
+@pytest.mark.parametrize("k", [0, 63, -1, True, 2.0])
+def test_validate_rejects_bad_k(k):
+    with pytest.raises(BadExponent):
+        validate(*G500, k)
+
+
+def test_entropy_and_bound():
+    assert entropy(params_for(UNIFORM, 4)) == pytest.approx(2.0)
+    assert speedup_bound(params_for(G500, 4)) == pytest.approx(2 / 1.5888, rel=1e-3)
+
+
+# ------------------------------------------------------------------ alias
+def test_alias_reconstruction():
+    w = [0.57, 0.19, 0.19, 0.05]
+    t = build_alias(w)
+    np.testing.assert_allclose(t.reconstructed_probs(), w, atol=1e-15)
+
+
+def test_alias_errors():
+    with pytest.raises(EmptyInput):
+        build_alias([])
+    with pytest.raises(NegativeWeight):
+        build_alias([1.0, -1.0])
+    with pytest.raises(NegativeWeight):
+        build_alias([1.0, float("inf")])
+    with pytest.raises(AllZeroWeights):
+        build_alias([0.0, 0.0])
+
+
+def test_alias_sample_rule():
+    t = build_alias([0.5, 0.3, 0.15, 0.05])
+    for b in range(4):
+        assert alias_sample(t, (b, 0.0)) == b or t.threshold[b] == 0.0
+        assert alias_sample(t, (b, 0.999999999)) in (b, int(t.alias[b]))
+
+
+# ------------------------------------------------------------------ tables
+def test_variable_table_sizes_and_structure():
+    for size in (4, 7, 253, 1021, 1024, 4096):
+        t = variable_table(G500, size)
+        assert len(t) <= size
+        assert abs(float(t.probs.sum()) - 1.0) < 1e-12
+        # prefix-free and complete: Kraft equality over 4-ary depths
+        assert sum(4.0 ** -int(d) for d in t.depths) == pytest.approx(1.0)
+
+
+def test_table_errors():
+    p = params_for(G500, 4)
+    with pytest.raises(SizeLimitTooSmall):
+        build_variable_table(p, 3)
+    with pytest.raises(DepthOutOfRange):
+        build_variable_table(p, 100, depth_cap=0)
+    with pytest.raises(DepthOutOfRange):
+        build_fixed_table(p, 17)
+
+
+def test_table_stats_expected_depth_goldens():
+    # reference tests/test_table.py:217-230 (expected_depth of G500 S=1021 and skewed S=8191)
+    assert table_stats(variable_table(G500, 1021)).expected_depth == pytest.approx(6.073327, abs=1e-6)
+    st = table_stats(variable_table(SKEWED, 8191))
+    assert st.expected_depth == pytest.approx(19.641176, abs=1e-5)
+    assert st.expected_info == pytest.approx(12.157801, abs=1e-5)
+    assert st.mean_entry_info == pytest.approx(13.830778, abs=1e-5)
+    fs = table_stats(build_fixed_table(params_for(G500, 4), 5))
+    assert fs.expected_depth == 5.0 and fs.entry_count == 4**5
+    assert fs.min_prob == pytest.approx(0.05**5, rel=1e-9)
+
+
+def test_config_tables_geometry():
+    """SURVEY §8a table geometry: C3 max depth 16, C4 12, C5 2^16 18."""
+    assert variable_table(G500, 1 << 14).max_depth == 16
+    assert variable_table(LESS_SKEWED, 1 << 14).max_depth == 12
+    assert variable_table(G500, 1 << 16).max_depth == 18
+    assert variable_table(G500, 1 << 14).mean_depth == pytest.approx(8.5972, abs=1e-4)
+
+
+# ------------------------------------------------------------------ config / sharding
+def test_genconfig_errors():
+    p, t = params_for(G500, 10), variable_table(G500, 253)
+    with pytest.raises(ValueError):
+        GenConfig(params=p, table=t, edge_count=-1, seed=1)
+    with pytest.raises(ValueError):
+        GenConfig(params=p, table=t, edge_count=10, seed=1, block_size=0)
+    with pytest.raises(ValueError):
+        GenConfig(params=p, table=t, edge_count=10, seed=1, threads=0)
+    with pytest.raises(ValueError):
+        GenConfig(params=p, table=t, edge_count=10, seed=1, rng="mt19937")
+    assert GenConfig(params=p, table=t, edge_count=10, seed=1).stream_edges == 1024
+    assert GenConfig(params=p, table=t, edge_count=10, seed=1, rng="reference").stream_edges == 65536
+
+
+@pytest.mark.parametrize("m,block,world", [(0, 4, 3), (10, 4, 3), (123457, 1000, 8),
+                                           (1 << 20, 1024, 7), (5, 10, 4)])
+def test_shard_rows_tile_the_output(m, block, world):
+    pos = 0
+    streams = 0
+    for r in range(world):
+        s_lo, s_hi, r_lo, r_hi = shard_rows(m, block, r, world)
+        assert s_lo == streams and r_lo == pos and r_hi >= r_lo
+        assert r_lo == min(s_lo * block, m)
+        pos, streams = r_hi, s_hi
+    assert pos == m and streams == (m + block - 1) // block
+
+
+# ------------------------------------------------------------------ partition plans
+@pytest.mark.parametrize("case", GOLD["plans"], ids=lambda c: f"k{c['k']}t{c['t']}p{c['part']}")
+def test_plan_tiles_match_reference(case):
+    quads = LESS_SKEWED if case["quads"] == "less" else G500
+    p = validate(*quads, case["k"])
+    plan = default_plan(case["k"], case["t"], case["m"], case["seed"], case["parts"])
+    got = [[tc.tile_row, tc.tile_col, tc.count] for tc in plan_tiles(plan, p, case["part"])]
+    assert got == case["tiles"]
+
+
+def test_split_conserves_and_is_deterministic():
+    p = params_for(G500, 8)
+    for count in (0, 1, 17, 10**5):
+        parts = split_quadrant_counts(count, p, (9, count))
+        assert sum(parts) == count and min(parts) >= 0
+        assert parts == split_quadrant_counts(count, p, (9, count))
+
+
+def test_plan_parts_partition_the_whole():
+    p = validate(*LESS_SKEWED, 36)
+    whole = plan_tiles(default_plan(36, 3, 1 << 33, 1, 1), p, 0)
+    parts = [tc for part in range(8) for tc in plan_tiles(default_plan(36, 3, 1 << 33, 1, 8), p, part)]
+    assert sorted((t.tile_row, t.tile_col, t.count) for t in whole) == \
+        sorted((t.tile_row, t.tile_col, t.count) for t in parts)
+    assert sum(t.count for t in whole) == 1 << 33
+
+
+def test_partition_plan_rejects_bad_geometry():
+    with pytest.raises(ValueError):
+        PartitionPlan(k=4, t=5, m=10, seed=1, owner_rows=((0, 32),))
+    with pytest.raises(ValueError):
+        PartitionPlan(k=8, t=2, m=10, seed=1, owner_rows=((0, 2), (3, 4)))
+    with pytest.raises(ValueError):
+        default_plan(8, 2, 10, 1, 0)
+
+
+def test_part_segments_layout():
+    p = validate(*LESS_SKEWED, 36)
+    plan = default_plan(36, 3, 10**6, 5, 8)
+    tiles = plan_tiles(plan, p, 2)
+    segs, rows = part_segments(tiles, 36, 3, 1024)
+    assert rows == sum(t.count for t in tiles)
+    r = 0
+    it = iter(segs)
+    for tc in tiles:
+        if tc.count:
+            sid, cnt, out_row, rp, cp, tweak = next(it)
+            assert (sid, cnt, out_row) == (0, tc.count, r)
+            assert rp == tc.tile_row << 33 and cp == tc.tile_col << 33
+            assert tweak == tile_key((tc.tile_row << 3) | tc.tile_col)
+        r += tc.count
+    assert len({s[5] for s in segs}) == len(segs)  # distinct keys per tile
