@@ -85,6 +85,38 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t sel) {
   return r;
 }
 
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t mul_hi(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// Staging-ring accesses.  All of them are volatile asm so they keep their
+// program order with respect to each other without a compiler memory clobber.
+__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b));
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint64_t a, uint64_t b) {
+  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b));
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
 template <int FB> struct AEntry;
 template <> struct AEntry<16> { using T = uint2; };
 template <> struct AEntry<32> { using T = uint4; };
@@ -109,51 +141,54 @@ constexpr int kSmemThreads = 512;                   // packed_smem CTA size
 constexpr int kGlobalThreads = 256;                 // packed_global CTA size
 
 template <bool OUT64, int THREADS>
-__device__ __forceinline__ void flush_sector(char* gptr, const uint8_t* ring, uint32_t half,
+__device__ __noinline__ void flush_slots(char* gptr, uint32_t st, uint32_t lo, uint32_t hi) {
+  // Slot-by-slot stores of a partial sector (stream heads / tails; rare).
+  constexpr uint32_t EB = OUT64 ? 16 : 8;
+  constexpr uint32_t STRIDE = THREADS * EB;
+  for (uint32_t q = lo; q < hi; ++q) {
+    if (OUT64)
+      *reinterpret_cast<uint4*>(gptr + q * EB) = lds128(st + q * STRIDE);
+    else
+      *reinterpret_cast<uint2*>(gptr + q * EB) = lds64(st + q * STRIDE);
+  }
+}
+
+template <bool OUT64, int THREADS>
+__device__ __forceinline__ void flush_sector(char* gptr, uint32_t ring_sa, uint32_t half,
                                              uint32_t lo) {
+  // ring_sa: shared-space address of this thread's slot 0
   constexpr uint32_t EB = OUT64 ? 16 : 8;
   constexpr uint32_t G = kSectorBytes / EB;
   constexpr uint32_t STRIDE = THREADS * EB;
-  const uint8_t* st = ring + half * G * STRIDE;
+  const uint32_t st = ring_sa + half * G * STRIDE;
   if (lo == 0) {
     uint32_t v[8];
     if (OUT64) {
-      const uint4 e0 = *reinterpret_cast<const uint4*>(st);
-      const uint4 e1 = *reinterpret_cast<const uint4*>(st + STRIDE);
+      const uint4 e0 = lds128(st);
+      const uint4 e1 = lds128(st + STRIDE);
       v[0] = e0.x; v[1] = e0.y; v[2] = e0.z; v[3] = e0.w;
       v[4] = e1.x; v[5] = e1.y; v[6] = e1.z; v[7] = e1.w;
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint2 e = *reinterpret_cast<const uint2*>(st + q * STRIDE);
+        const uint2 e = lds64(st + q * STRIDE);
         v[2 * q] = e.x; v[2 * q + 1] = e.y;
       }
     }
     asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(gptr), "r"(v[0]),
                  "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
   } else {
-    for (uint32_t q = lo; q < G; ++q) {  // a stream's unaligned first sector
-      if (OUT64)
-        *reinterpret_cast<uint4*>(gptr + q * EB) = *reinterpret_cast<const uint4*>(st + q * STRIDE);
-      else
-        *reinterpret_cast<uint2*>(gptr + q * EB) = *reinterpret_cast<const uint2*>(st + q * STRIDE);
-    }
+    flush_slots<OUT64, THREADS>(gptr, st, lo, G);  // a stream's unaligned first sector
   }
 }
 
 template <bool OUT64, int THREADS>
-__device__ __forceinline__ void flush_tail(char* gptr, const uint8_t* ring, uint32_t half,
+__device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_t half,
                                            uint32_t lo, uint32_t hi) {
   constexpr uint32_t EB = OUT64 ? 16 : 8;
   constexpr uint32_t G = kSectorBytes / EB;
   constexpr uint32_t STRIDE = THREADS * EB;
-  const uint8_t* st = ring + half * G * STRIDE;
-  for (uint32_t q = lo; q < hi; ++q) {  // a stream's partial last sector
-    if (OUT64)
-      *reinterpret_cast<uint4*>(gptr + q * EB) = *reinterpret_cast<const uint4*>(st + q * STRIDE);
-    else
-      *reinterpret_cast<uint2*>(gptr + q * EB) = *reinterpret_cast<const uint2*>(st + q * STRIDE);
-  }
+  flush_slots<OUT64, THREADS>(gptr, ring_sa + half * G * STRIDE, lo, hi);  // partial last sector
 }
 
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT>
@@ -190,7 +225,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     baseB = reinterpret_cast<const uint8_t*>(tab.B);
     stage = smem;
   }
-  uint8_t* const ring = stage + threadIdx.x * EB;  // slot q at ring + q * STRIDE
+  // shared-space addresses: ring slot q of this thread = ring_sa + q * STRIDE
+  const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint32_t ring_sa = stage_sa + threadIdx.x * EB;
 
   const uint32_t k = g.k;
   const uint32_t kmask = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
@@ -218,7 +255,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     if (left == 0) {
       // Stream done: write its partial last sector, account nf, open the next.
       if ((roff / STRIDE & (G - 1)) > lo)
-        flush_tail<OUT64, THREADS>(gptr, ring, half, lo, roff / STRIDE & (G - 1));
+        flush_tail<OUT64, THREADS>(gptr, ring_sa, half, lo, roff / STRIDE & (G - 1));
       if (COUNT) {
         // nf (generator.py:255-257): the highest sample of call j-1 that
         // produced an edge this stream needed.
@@ -298,8 +335,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
         const uint32_t pw = 1u << d;
         const uint32_t tt = f + d;
-        const uint32_t vr = cur_r * pw + r, vrh = __umulhi(cur_r, pw);
-        const uint32_t vc = cur_c * pw + c, vch = __umulhi(cur_c, pw);
+        // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
+        const uint32_t vr = mad_lo(cur_r, pw, r), vrh = mul_hi(cur_r, pw);
+        const uint32_t vc = mad_lo(cur_c, pw, c), vch = mul_hi(cur_c, pw);
         const bool emit = tt >= k;
         const uint32_t over = emit ? tt - k : tt;
         cur_r = vr;
@@ -314,30 +352,33 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         }
         if (PREFIX) { u |= p.rpre; v |= p.cpre; }
         if (st) {
-          uint8_t* sp = stage + roff;
           if constexpr (OUT64) {
-            *reinterpret_cast<ulonglong2*>(sp) = make_ulonglong2(u, v);
+            sts128(stage_sa + roff, u, v);
           } else {
-            *reinterpret_cast<uint2*>(sp) = make_uint2((uint32_t)u, (uint32_t)v);
+            sts64(stage_sa + roff, (uint32_t)u, (uint32_t)v);
           }
           // next slot; the mask keeps this thread's column bits (tid * EB < STRIDE)
           roff = (roff + STRIDE) & (R * STRIDE - 1);
-          --left;
+          if (CAREFUL || OUT64) --left;
         }
         if (COUNT) ebits |= (uint32_t)st << t;
         if ((uint32_t)t % G == G - 1 && (roff / (G * STRIDE)) != half) {
           // At most G edges since the last check: the sector at gptr is complete.
-          flush_sector<OUT64, THREADS>(gptr, ring, half, lo);
+          flush_sector<OUT64, THREADS>(gptr, ring_sa, half, lo);
           gptr += kSectorBytes;
           half ^= 1;
           lo = 0;
         }
       }
     };
-    if (__all_sync(0xFFFFFFFFu, left >= 4))
+    if (__all_sync(0xFFFFFFFFu, left >= 4)) {
+      const uint32_t roff0 = roff;
       step(std::false_type{});
-    else
+      // u32 edges: <= 4 stores into an 8-slot ring, so the slot advance is exact
+      if (!OUT64) left -= ((roff - roff0) / STRIDE) & (R - 1);
+    } else {
       step(std::true_type{});
+    }
     ++j;
   }
   if (COUNT && g.samples_total && total_nf)

@@ -1,0 +1,95 @@
+"""The C-ABI boundary on CPU: the library loads, exports every symbol the header
+declares, and its structs match the ctypes mirrors byte for byte.  No compute
+call is made (no GPU here)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_1905_03525_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "rmat_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:rmat_status|const char\*|int)\s+(rmat_\w+)\(", src, re.M)))
+
+
+def test_header_declares_the_exports():
+    assert declared_functions() == sorted(N.EXPORTS)
+
+
+def test_library_builds_and_exports_every_symbol():
+    L = N.lib()
+    for name in declared_functions():
+        assert hasattr(L, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", N.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    for name in declared_functions():
+        assert re.search(rf"\bT {name}$", out, re.M), name
+
+
+def test_pure_host_entry_points():
+    L = N.lib()
+    assert L.rmat_abi_version() == 1
+    assert L.rmat_strerror(0) == b"ok"
+    assert L.rmat_strerror(2) == b"inconsistent fragment table"
+    # invalid arguments are rejected without touching a device
+    assert L.rmat_table_create(0, None, None) == 1
+    assert L.rmat_generate(None, None) == 1
+    assert L.rmat_generate_refstream(None, None) == 1
+    assert L.rmat_table_get_info(None, None) == 1
+
+
+def test_struct_layouts_match_header(tmp_path):
+    prog = tmp_path / "layout.c"
+    prog.write_text(f"""
+#include <stdio.h>
+#include <stddef.h>
+#include "{HEADER}"
+int main(void) {{
+  printf("%zu %zu %zu %zu %zu\\n", sizeof(rmat_table_desc), sizeof(rmat_table_info),
+         sizeof(rmat_segment), sizeof(rmat_gen_args), sizeof(rmat_refstream_args));
+  printf("%zu %zu %zu %zu\\n", offsetof(rmat_gen_args, out), offsetof(rmat_gen_args, kernel_used),
+         offsetof(rmat_refstream_args, row_prefix), offsetof(rmat_table_info, device));
+  return 0;
+}}
+""")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", str(prog), "-o", str(exe)], check=True)
+    lines = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    sizes = [int(x) for x in lines[0].split()]
+    offs = [int(x) for x in lines[1].split()]
+    assert sizes == [ctypes.sizeof(N.TableDesc), ctypes.sizeof(N.TableInfo),
+                     ctypes.sizeof(N.Segment), ctypes.sizeof(N.GenArgs), ctypes.sizeof(N.RefArgs)]
+    assert offs == [N.GenArgs.out.offset, N.GenArgs.kernel_used.offset,
+                    N.RefArgs.row_prefix.offset, N.TableInfo.device.offset]
+
+
+def test_product_path_fails_loudly_without_cuda():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present: the GPU tests cover the product path")
+    from paper_1905_03525_b200 import GenConfig, NativeUnavailable, generate
+    from conftest import G500, params_for, variable_table
+
+    cfg = GenConfig(params=params_for(G500, 10), table=variable_table(G500, 253), edge_count=10,
+                    seed=1)
+    with pytest.raises(NativeUnavailable):
+        generate(cfg)
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1905_03525_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "liboracle" not in text, f
