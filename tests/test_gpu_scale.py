@@ -1,0 +1,177 @@
+"""GPU parity at BASELINE.json sizes, partitioned mode, and ABI error paths.
+
+* C2 (k=24, S=2^12): oracle-mode bit-exact check of the first 2^20 edges of
+  64 streams (a dedicated 64 x 2^20 launch), plus 64 sampled streams of the
+  production m = 2^28 run.
+* C3 (k=28, S=2^14, m=2^32, 34 GB): sampled streams bit-exact, all endpoints
+  < 2^28, and the samples/edge figure against the table's expectation.
+* C4 (less-skewed, k=36, t=3): every tile of a part against the oracle, in
+  both stream modes; reference mode against the reference's own tile goldens.
+"""
+
+import hashlib
+import json
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import G500, LESS_SKEWED, params_for, table_for
+from paper_1905_03525_b200 import DOMAIN_BLOCK, DOMAIN_TILE, GenConfig, NativeError, generate_shard
+from paper_1905_03525_b200 import _native as N
+from paper_1905_03525_b200.device import device_table, launch_generate
+from paper_1905_03525_b200.partition import (default_plan, generate_part, generate_part_device,
+                                             generate_tile, plan_tiles, tile_key)
+
+pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+POOL = ThreadPoolExecutor(max_workers=os.cpu_count() or 4)  # ctypes releases the GIL
+
+
+def host(t):
+    t = t.cpu()
+    return t.numpy().astype(np.uint64) if t.dtype == torch.uint32 else t.numpy()
+
+
+def check_streams(out_host, ot, k, seed, E, first_stream, streams, domain=DOMAIN_BLOCK):
+    def one(s):
+        cnt = min(E, out_host.shape[0] - s * E)
+        want, _ = oracle.fast_stream(ot, k, cnt, seed, first_stream + s, domain)
+        return bool((out_host[s * E:s * E + cnt] == want).all())
+    return all(POOL.map(one, streams))
+
+
+def test_c2_oracle_64_streams_first_2pow20_edges(cuda):
+    k, E = 24, 1 << 20
+    table = table_for("v4096")
+    cfg = GenConfig(params=params_for(G500, k), table=table, edge_count=64 * E, seed=1,
+                    block_size=E)
+    out, _, _ = generate_shard(cfg)
+    assert check_streams(host(out), oracle_table_v("v4096"), k, 1, E, 0, range(64))
+
+
+def oracle_table_v(tag, quads=G500):
+    from conftest import oracle_table
+    return oracle_table(tag, quads)
+
+
+def test_c2_production_run_sampled_streams(cuda):
+    k, m, E = 24, 1 << 28, 1024
+    cfg = GenConfig(params=params_for(G500, k), table=table_for("v4096"), edge_count=m, seed=1,
+                    block_size=E)
+    out, _, s = generate_shard(cfg, count_samples=True)
+    nstreams = m // E
+    picks = np.linspace(0, nstreams - 1, 64).astype(int)
+    v = out.view(torch.int32)
+    rows = torch.cat([v[p * E:(p + 1) * E] for p in picks]).cpu().numpy().view(np.uint32)
+    rows = rows.astype(np.uint64)
+    ot = oracle_table_v("v4096")
+    for i, p in enumerate(picks):
+        want, _ = oracle.fast_stream(ot, k, E, 1, int(p))
+        assert (rows[i * E:(i + 1) * E] == want).all(), p
+    # samples/edge close to k / E[depth] (= 3.277 for this table)
+    spe = int(s.item()) / m
+    assert abs(spe - k / table_for("v4096").mean_depth) < 0.01
+
+
+def test_c3_full_size_properties(cuda):
+    k, m, E = 28, 1 << 32, 1024
+    table = table_for("v16384")
+    cfg = GenConfig(params=params_for(G500, k), table=table, edge_count=m, seed=1, block_size=E)
+    out, _, s = generate_shard(cfg, count_samples=True)
+    v = out.view(torch.int32)
+    assert int(v.min()) >= 0 and int(v.max()) < (1 << 28)  # k-bit endpoints
+    nstreams = m // E
+    picks = np.linspace(0, nstreams - 1, 64).astype(int)
+    ot = oracle_table_v("v16384")
+    for p in picks:
+        got = v[p * E:(p + 1) * E].cpu().numpy().view(np.uint32).astype(np.uint64)
+        want, _ = oracle.fast_stream(ot, k, E, 1, int(p))
+        assert (got == want).all(), p
+    spe = int(s.item()) / m
+    assert abs(spe - k / table.mean_depth) < 0.005  # 3.257 samples per edge
+    del out, v
+    torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- partitioned (C4 shape)
+@pytest.mark.parametrize("rng", ["philox4x32", "reference"])
+def test_c4_part_tiles_match_oracle(cuda, rng):
+    quads = LESS_SKEWED
+    k, t, m, seed, parts = 36, 3, 3_000_000, 7, 8
+    p = params_for(quads, k)
+    table = table_for("v16384", quads)
+    ot = oracle_table_v("v16384", quads)
+    plan = default_plan(k, t, m, seed, parts)
+    total = 0
+    for part in (0, 3, 7):
+        edges, tiles, samples = generate_part(plan, p, table, part, rng=rng)
+        assert edges.shape == (sum(tc.count for tc in tiles), 2)
+        r = 0
+        for tc in tiles:
+            payload = (tc.tile_row << t) | tc.tile_col
+            pre = (tc.tile_row << (k - t), tc.tile_col << (k - t))
+            if rng == "reference":
+                want, _ = oracle.ref_stream(ot, k - t, tc.count, (seed ^ DOMAIN_TILE), payload, *pre)
+            else:
+                want = np.empty((tc.count, 2), dtype=np.uint64)
+                E = 1024
+                for j in range((tc.count + E - 1) // E):
+                    cnt = min(E, tc.count - j * E)
+                    want[j * E:j * E + cnt], _ = oracle.fast_stream(
+                        ot, k - t, cnt, seed, j, DOMAIN_TILE ^ tile_key(payload), *pre)
+            assert (edges[r:r + tc.count] == want).all(), (part, tc)
+            # every edge inside its tile
+            assert ((edges[r:r + tc.count, 0] >> np.uint64(k - t)) == tc.tile_row).all()
+            r += tc.count
+        total += r
+    assert total > 0
+
+
+@pytest.mark.parametrize("case", GOLD["ref_tiles"], ids=lambda c: str(c["tile"]))
+def test_reference_mode_tile_matches_reference_golden(cuda, case):
+    quads = LESS_SKEWED if case["table"].startswith("less") else G500
+    tag = case["table"].split(":")[1]
+    p = params_for(quads, case["k"])
+    e = generate_tile(tuple(case["tile"]), case["count"], p, table_for(tag, quads), case["k"],
+                      case["t"], case["seed"], rng="reference")
+    assert hashlib.sha256(np.ascontiguousarray(e).tobytes()).hexdigest() == case["edges"]
+
+
+def test_part_fully_resolved_tiles(cuda):
+    # k == t: every edge is its tile's single cell (reference partition.py:147-151)
+    p = params_for(G500, 3)
+    plan = default_plan(3, 3, 5000, 2, 2)
+    out, tiles, _ = generate_part_device(plan, p, table_for("v1024"), 1)
+    e = host(out)
+    r = 0
+    for tc in tiles:
+        assert (e[r:r + tc.count] == [tc.tile_row, tc.tile_col]).all()
+        r += tc.count
+
+
+# ---------------------------------------------------------------- ABI error behaviour
+def test_abi_rejects_bad_launches(cuda):
+    dt = device_table(table_for("v1024"), cuda)
+    out = torch.empty((10, 2), dtype=torch.uint32, device=cuda)
+    with pytest.raises(NativeError):  # segment beyond the output
+        launch_generate(dt, 16, 1, DOMAIN_BLOCK, 4, [(0, 11, 0, 0, 0)], out)
+    with pytest.raises(NativeError):  # k = 40 does not fit 4-byte endpoints
+        launch_generate(dt, 40, 1, DOMAIN_BLOCK, 4, [(0, 10, 0, 0, 0)], out)
+    with pytest.raises(NativeError):  # packed kernel forced where ineligible (k < max depth)
+        launch_generate(dt, 3, 1, DOMAIN_BLOCK, 4, [(0, 10, 0, 0, 0)], out,
+                        kernel=N.KERNEL_PACKED_SMEM)
+    with pytest.raises(NativeError):  # prefix overlapping the k inner bits
+        launch_generate(dt, 16, 1, DOMAIN_BLOCK, 4, [(0, 10, 0, 1, 0)], out)
+
+
+def test_empty_and_single_edge(cuda):
+    from paper_1905_03525_b200 import emit_block, generate
+    cfg = GenConfig(params=params_for(G500, 10), table=table_for("v253"), edge_count=0, seed=1)
+    assert generate(cfg).shape == (0, 2)
+    e = emit_block(table_for("f4"), 4, 1, (7, 0))
+    want, nf = oracle.fast_stream(oracle_table_v("f4"), 4, 1, 7, 0)
+    assert (e == want).all() and nf == 1
