@@ -96,6 +96,7 @@ rmat::PackedTab packed_view(const rmat_table* t) {
   p.fm = (1u << rmat::scheme_p_fbits(t->lg)) - 1u;
   p.n = (uint32_t)t->n;
   p.fb = t->fb;
+  p.one = 1;
   return p;
 }
 
@@ -249,7 +250,7 @@ rmat_status rmat_table_create(int device, const rmat_table_desc* d, rmat_table**
     std::vector<uint32_t> B(n), tlo(n);
     for (uint64_t i = 0; i < n; ++i) {
       const uint32_t a = al[i];
-      B[i] = (T[i] & ~fm) | (uint32_t)dep[i] | ((uint32_t)dep[a] << 8);
+      B[i] = (~T[i] & ~fm) | (uint32_t)dep[i] | ((uint32_t)dep[a] << 8);
       tlo[i] = T[i] & fm;
     }
     if ((st = upload(B, &t->pB, &bytes)) || (st = upload(tlo, &t->ptlo, &bytes))) {

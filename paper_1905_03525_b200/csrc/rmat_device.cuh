@@ -22,9 +22,9 @@ struct SegDev {
 // ---------------------------------------------------------------------------
 // Packed bucket layout (scheme P tables only).  Bucket i is the alias bucket
 // hit by a sample whose word carries i in bits [2, 2+lg):
-//   B[i] = T_hi | (d_self - 1) | (d_alias - 1) << DB
+//   B[i] = (~T & ~fm) | d_alias << 8 | d_self
 //          T = thr32 clamped to 32 bits (alias forced to self when thr32 == 2^32),
-//          T_hi = T & ~(4n-1), DB = 4 (16-bit fields) or 5 (32-bit fields)
+//          fm = 2^F - 1, F = max(16, lg + 2) fraction bits below the compare
 //   A[i] = both candidate fragments, so one pair of independent loads resolves
 //          the sample without a dependent second lookup:
 //          FB=16: uint2 {row_self | row_alias << 16, col_self | col_alias << 16}
@@ -39,6 +39,7 @@ struct PackedTab {
   uint32_t fm;        // 4n - 1
   uint32_t n;
   uint32_t fb;        // 16 or 32
+  uint32_t one;       // 1 (a launch parameter so the IMAD-based compare is not folded)
 };
 
 // Generic layout: one record per fragment, any n / depth <= 62.

@@ -91,6 +91,12 @@ __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
   return r;
 }
 
+__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint32_t c) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"((uint64_t)c));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t mul_hi(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -232,6 +238,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   const uint32_t k = g.k;
   const uint32_t kmask = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
   const uint32_t idxmask4 = tab.idxmask4, fm = tab.fm;
+  const uint32_t one = tab.one;
   const uint64_t T = (uint64_t)gridDim.x * THREADS;
   uint64_t s = (uint64_t)blockIdx.x * THREADS + threadIdx.x;
 
@@ -242,14 +249,54 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   uint64_t total_nf = 0;
   uint32_t ebits = 0;                // COUNT: samples of the current call that produced an edge
   uint32_t left = (uint32_t)p.left;  // edges still to produce
-  // roff = ring slot of the next output row (row mod R) times STRIDE.  The
-  // first unflushed sector starts at gptr, occupies ring half `half`, and is
-  // valid from slot lo.
   // stage + roff = ring slot of the next edge; roff = slot * STRIDE + tid * EB
   uint32_t roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
+  // The first unflushed sector starts at gptr, occupies ring half `half`, and
+  // is valid from slot lo.
   uint32_t half = roff / (G * STRIDE);
   uint32_t lo = roff / STRIDE & (G - 1);
   char* gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+
+  // One call's worth of samples: words, bucket entries, byte selectors.
+  struct Batch {
+    uint32_t w[4], b[4], sel[4], seld[4];
+    AE a[4];
+    bool tie;
+  };
+  // Draw call jj of the current stream and resolve everything that does not
+  // depend on the bit accumulator (software-pipelined one call ahead).
+  auto fetch = [&](uint32_t jj) {
+    Batch q;
+    u32x4 w4;
+    if (PREFIX) {
+      w4 = stream_call(jj, 0, p.sid, p.k0, p.k1);  // tile segments: per-stream key
+    } else {
+      w4 = philox4x32_10_rk(jj, 0, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), g.rk);
+    }
+    q.w[0] = w4.x; q.w[1] = w4.y; q.w[2] = w4.z; q.w[3] = w4.w;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t a4 = q.w[t] & idxmask4;
+      q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
+      q.a[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
+    }
+    q.tie = false;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      // B = (~T & ~fm) | d_alias << 8 | d_self: the complemented threshold top
+      // bits above the depth fields.  With X = w | fm, the 64-bit sum X + B
+      // carries out exactly when the fraction's top bits H >= T_hi (alias),
+      // and its low word is < 2^F exactly when H == T_hi (a tie).  One IMAD
+      // on the FMA pipe replaces the compare/select chain on the ALU pipe.
+      const uint64_t sum = mad_wide(q.w[t] | fm, one, q.b[t]);
+      const uint32_t ge = (uint32_t)(sum >> 32);
+      q.tie |= (uint32_t)sum <= fm;
+      q.sel[t] = mad_lo(ge, 0x22u, 0x4410u);   // 0x4410 self / 0x4432 alias
+      q.seld[t] = ge + 0x4440u;                // 0x4440 self / 0x4441 alias
+    }
+    return q;
+  };
+  Batch nx = fetch(0);
 
   for (;;) {
     if (left == 0) {
@@ -272,66 +319,41 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       half = roff / (G * STRIDE);
       lo = roff / STRIDE & (G - 1);
       gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+      nx = fetch(0);
     }
-    u32x4 w4;
-    if (PREFIX) {
-      w4 = stream_call(j, 0, p.sid, p.k0, p.k1);  // tile segments: per-stream key
-    } else {
-      w4 = philox4x32_10_rk(j, 0, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), g.rk);
-    }
-    const uint32_t wq[4] = {w4.x, w4.y, w4.z, w4.w};
-    uint32_t bq[4];
-    AE aq[4];
-    // Fragment / depth byte selectors per sample (self: bytes 0-1 of A's
-    // halves and byte 0 of B; alias: bytes 2-3 and byte 1).  Kept as
-    // registers so no predicate has to survive the tie branch.
-    uint32_t selq[4], seldq[4];
-    bool tie = false;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const uint32_t a4 = wq[t] & idxmask4;
-      bq[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
-      aq[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      // B = T_hi | d_alias << 8 | d_self with the fields below T_hi (F >= 16
-      // bits): compare the fraction's top bits H = w & ~fm with T_hi.
-      const bool lt = (wq[t] | fm) < bq[t];           // H <  T_hi
-      tie |= ((wq[t] ^ bq[t]) & ~fm) == 0;           // H == T_hi
-      selq[t] = lt ? 0x4410u : 0x4432u;
-      seldq[t] = lt ? 0x4440u : 0x4441u;
-    }
-    if (tie) {
+    Batch cb = nx;
+    if (cb.tie) {
       // Rare (2^-(32-F) per sample): decide ties with the lazy word's low bits.
       const u32x4 z4 = PREFIX ? stream_call(j, 1, p.sid, p.k0, p.k1)
                               : philox4x32_10_rk(j, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), g.rk);
       const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (((wq[t] ^ bq[t]) & ~fm) == 0) {
-          const bool lt = (zq[t] & fm) < __ldg(tab.tlo + ((wq[t] & idxmask4) >> 2));
-          selq[t] = lt ? 0x4410u : 0x4432u;
-          seldq[t] = lt ? 0x4440u : 0x4441u;
+        if ((uint32_t)mad_wide(cb.w[t] | fm, one, cb.b[t]) <= fm) {
+          const bool lt = (zq[t] & fm) < __ldg(tab.tlo + ((cb.w[t] & idxmask4) >> 2));
+          cb.sel[t] = lt ? 0x4410u : 0x4432u;
+          cb.seld[t] = lt ? 0x4440u : 0x4441u;
         }
     }
-    // Edges needed by this stream cap what the 4 samples may store; in the
-    // common case (>= 4 left in every lane) the per-sample check disappears.
+    // Append the 4 fragments of `cb` while the next call is drawn.  Edges the
+    // stream still needs cap what may be stored; in the common case (>= 4
+    // left in every lane) the per-sample check disappears.
     auto step = [&](auto careful_tag) {
       constexpr bool CAREFUL = decltype(careful_tag)::value;
+      nx = fetch(j + 1);
       if (COUNT) ebits = 0;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         uint32_t r, c;
         if constexpr (FB == 16) {
-          r = prmt(aq[t].x, selq[t]);
-          c = prmt(aq[t].y, selq[t]);
+          r = prmt(cb.a[t].x, cb.sel[t]);
+          c = prmt(cb.a[t].y, cb.sel[t]);
         } else {
-          const bool lt = selq[t] == 0x4410u;
-          r = lt ? aq[t].x : aq[t].y;
-          c = lt ? aq[t].z : aq[t].w;
+          const bool lt = cb.sel[t] == 0x4410u;
+          r = lt ? cb.a[t].x : cb.a[t].y;
+          c = lt ? cb.a[t].z : cb.a[t].w;
         }
-        const uint32_t d = prmt(bq[t], seldq[t]);
+        const uint32_t d = prmt(cb.b[t], cb.seld[t]);
         // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
         const uint32_t pw = 1u << d;
         const uint32_t tt = f + d;
