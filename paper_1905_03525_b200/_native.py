@@ -13,7 +13,7 @@ from functools import lru_cache
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "_build", "librmat_b200.so")
+LIB_PATH = os.environ.get("RMAT_LIB") or os.path.join(_PKG, "_build", "librmat_b200.so")
 _SOURCES = [os.path.join(_PKG, "csrc", f) for f in
             ("rmat_capi.cu", "rmat_kernels.cuh", "rmat_refstream.cuh", "rmat_device.cuh",
              "philox.cuh")] + [os.path.join(_ROOT, "include", "rmat_b200.h")]
@@ -34,8 +34,18 @@ class NativeError(RuntimeError):
         super().__init__(f"{what}: {strerror(status)} (status {status})")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
     """Compile csrc/ into _build/librmat_b200.so for sm_100a with nvcc."""
+    if os.environ.get("RMAT_LIB") and out is None:
+        return LIB_PATH  # an explicitly chosen prebuilt library (experiments)
+    if out is not None:
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines],
+               os.path.join(_PKG, "csrc", "rmat_capi.cu"), "-o", out]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed:\n{res.stderr}")
+        return out
     newest = max(os.path.getmtime(p) for p in _SOURCES)
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH

@@ -97,6 +97,7 @@ rmat::PackedTab packed_view(const rmat_table* t) {
   p.n = (uint32_t)t->n;
   p.fb = t->fb;
   p.one = 1;
+  p.zero = 0;
   return p;
 }
 

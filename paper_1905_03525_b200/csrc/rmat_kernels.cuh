@@ -141,9 +141,15 @@ template <> struct AEntry<32> { using T = uint4; };
 // at most one sector can have completed; it leaves as a single 32-byte
 // store, so DRAM sees whole sectors and the per-sample path has no branch.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kSectorBytes = 32;
-constexpr uint32_t kRingBytes = 2 * kSectorBytes;  // staging bytes per thread
-constexpr int kSmemThreads = 512;                   // packed_smem CTA size
+#ifndef RMAT_FLUSH_BYTES
+#define RMAT_FLUSH_BYTES 32
+#endif
+#ifndef RMAT_SMEM_THREADS
+#define RMAT_SMEM_THREADS 512
+#endif
+constexpr uint32_t kSectorBytes = RMAT_FLUSH_BYTES;  // bytes per flush store (16 or 32)
+constexpr uint32_t kRingBytes = 2 * kSectorBytes;   // staging bytes per thread
+constexpr int kSmemThreads = RMAT_SMEM_THREADS;     // packed_smem CTA size
 constexpr int kGlobalThreads = 256;                 // packed_global CTA size
 
 template <bool OUT64, int THREADS>
@@ -159,32 +165,38 @@ __device__ __noinline__ void flush_slots(char* gptr, uint32_t st, uint32_t lo, u
   }
 }
 
+// Predicated sector flush: G staged edges -> one 256-bit store, as
+// straight-line predicated code (no branch / reconvergence in the hot loop).
 template <bool OUT64, int THREADS>
-__device__ __forceinline__ void flush_sector(char* gptr, uint32_t ring_sa, uint32_t half,
-                                             uint32_t lo) {
-  // ring_sa: shared-space address of this thread's slot 0
+__device__ __forceinline__ void flush_full_pred(char* gptr, uint32_t st, bool pred) {
   constexpr uint32_t EB = OUT64 ? 16 : 8;
-  constexpr uint32_t G = kSectorBytes / EB;
   constexpr uint32_t STRIDE = THREADS * EB;
-  const uint32_t st = ring_sa + half * G * STRIDE;
-  if (lo == 0) {
-    uint32_t v[8];
-    if (OUT64) {
-      const uint4 e0 = lds128(st);
-      const uint4 e1 = lds128(st + STRIDE);
-      v[0] = e0.x; v[1] = e0.y; v[2] = e0.z; v[3] = e0.w;
-      v[4] = e1.x; v[5] = e1.y; v[6] = e1.z; v[7] = e1.w;
-    } else {
+  constexpr uint32_t G = kSectorBytes / EB;
+  uint32_t v[8];
+  if constexpr (EB == 8) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint2 e = lds64(st + q * STRIDE);
-        v[2 * q] = e.x; v[2 * q + 1] = e.y;
-      }
-    }
-    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(gptr), "r"(v[0]),
-                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+    for (uint32_t q = 0; q < G; ++q)
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p ld.shared.v2.u32 {%0,%1}, [%2];\n}"
+                   : "=r"(v[2 * q]), "=r"(v[2 * q + 1]) : "r"(st + q * STRIDE), "r"((uint32_t)pred));
   } else {
-    flush_slots<OUT64, THREADS>(gptr, st, lo, G);  // a stream's unaligned first sector
+#pragma unroll
+    for (uint32_t q = 0; q < G; ++q)
+      asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %5, 0;\n"
+                   " @p ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n}"
+                   : "=r"(v[4 * q]), "=r"(v[4 * q + 1]), "=r"(v[4 * q + 2]), "=r"(v[4 * q + 3])
+                   : "r"(st + q * STRIDE), "r"((uint32_t)pred));
+  }
+  if constexpr (kSectorBytes == 32) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %9, 0;\n"
+        " @p st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n}" ::"l"(gptr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"((uint32_t)pred));
+  } else {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %5, 0;\n"
+        " @p st.global.v4.b32 [%0], {%1,%2,%3,%4};\n}" ::"l"(gptr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"((uint32_t)pred));
   }
 }
 
@@ -239,6 +251,26 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   const uint32_t kmask = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
   const uint32_t idxmask4 = tab.idxmask4, fm = tab.fm;
   const uint32_t one = tab.one;
+  // Round keys as per-thread registers (tab.zero is 0 at run time but opaque
+  // to the compiler) so the Philox XORs read registers instead of reloading
+  // the constant bank every call.
+#ifndef RMAT_RK_REGS
+#define RMAT_RK_REGS 1
+#endif
+  uint32_t rk[20];
+  if (!RMAT_RK_REGS) {
+#pragma unroll
+    for (int i = 0; i < 20; ++i) rk[i] = g.rk[i];
+  } else {
+    uint32_t k0 = g.k0 + (threadIdx.x & tab.zero), k1 = g.k1 + (threadIdx.x & tab.zero);
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+      rk[2 * i] = k0;
+      rk[2 * i + 1] = k1;
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+  }
   const uint64_t T = (uint64_t)gridDim.x * THREADS;
   uint64_t s = (uint64_t)blockIdx.x * THREADS + threadIdx.x;
 
@@ -271,7 +303,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     if (PREFIX) {
       w4 = stream_call(jj, 0, p.sid, p.k0, p.k1);  // tile segments: per-stream key
     } else {
-      w4 = philox4x32_10_rk(jj, 0, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), g.rk);
+      w4 = philox4x32_10_rk(jj, 0, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
     }
     q.w[0] = w4.x; q.w[1] = w4.y; q.w[2] = w4.z; q.w[3] = w4.w;
 #pragma unroll
@@ -296,10 +328,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
     return q;
   };
-  Batch nx = fetch(0);
-
   for (;;) {
-    if (left == 0) {
+    // Warp-uniform: in the common case every lane has >= 4 edges left, no
+    // stream ends during this call and the per-sample cap disappears.
+    const bool roomy = __all_sync(0xFFFFFFFFu, left >= 4);
+    if (!roomy && left == 0) {
       // Stream done: write its partial last sector, account nf, open the next.
       if ((roff / STRIDE & (G - 1)) > lo)
         flush_tail<OUT64, THREADS>(gptr, ring_sa, half, lo, roff / STRIDE & (G - 1));
@@ -319,13 +352,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       half = roff / (G * STRIDE);
       lo = roff / STRIDE & (G - 1);
       gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
-      nx = fetch(0);
     }
-    Batch cb = nx;
-    if (cb.tie) {
+    Batch cb = fetch(j);
+    if (__any_sync(0xFFFFFFFFu, cb.tie)) {
       // Rare (2^-(32-F) per sample): decide ties with the lazy word's low bits.
       const u32x4 z4 = PREFIX ? stream_call(j, 1, p.sid, p.k0, p.k1)
-                              : philox4x32_10_rk(j, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), g.rk);
+                              : philox4x32_10_rk(j, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
       const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -335,12 +367,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           cb.seld[t] = lt ? 0x4440u : 0x4441u;
         }
     }
-    // Append the 4 fragments of `cb` while the next call is drawn.  Edges the
+    // Append the 4 fragments of `cb`.  Edges the
     // stream still needs cap what may be stored; in the common case (>= 4
     // left in every lane) the per-sample check disappears.
     auto step = [&](auto careful_tag) {
       constexpr bool CAREFUL = decltype(careful_tag)::value;
-      nx = fetch(j + 1);
       if (COUNT) ebits = 0;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -381,23 +412,27 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           }
           // next slot; the mask keeps this thread's column bits (tid * EB < STRIDE)
           roff = (roff + STRIDE) & (R * STRIDE - 1);
-          if (CAREFUL || OUT64) --left;
+          if (CAREFUL || R <= 4) --left;
         }
         if (COUNT) ebits |= (uint32_t)st << t;
-        if ((uint32_t)t % G == G - 1 && (roff / (G * STRIDE)) != half) {
-          // At most G edges since the last check: the sector at gptr is complete.
-          flush_sector<OUT64, THREADS>(gptr, ring_sa, half, lo);
-          gptr += kSectorBytes;
-          half ^= 1;
-          lo = 0;
+        if ((uint32_t)t % G == G - 1) {
+          // At most G edges since the last check: the sector at gptr is
+          // complete when the next slot has left its ring half.
+          const bool full = (roff / (G * STRIDE)) != half;
+          flush_full_pred<OUT64, THREADS>(gptr, ring_sa + half * G * STRIDE, full && lo == 0);
+          if (__any_sync(0xFFFFFFFFu, full && lo != 0) && full && lo != 0)  // unaligned stream head
+            flush_slots<OUT64, THREADS>(gptr, ring_sa + half * G * STRIDE, lo, G);
+          gptr += full ? kSectorBytes : 0;
+          half ^= (uint32_t)full;
+          lo = full ? 0 : lo;
         }
       }
     };
-    if (__all_sync(0xFFFFFFFFu, left >= 4)) {
+    if (roomy) {
       const uint32_t roff0 = roff;
       step(std::false_type{});
-      // u32 edges: <= 4 stores into an 8-slot ring, so the slot advance is exact
-      if (!OUT64) left -= ((roff - roff0) / STRIDE) & (R - 1);
+      // <= 4 stores into a ring of > 4 slots: the slot advance is exact
+      if (R > 4) left -= ((roff - roff0) / STRIDE) & (R - 1);
     } else {
       step(std::true_type{});
     }
