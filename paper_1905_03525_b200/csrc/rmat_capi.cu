@@ -122,7 +122,7 @@ rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaS
   size_t smem = 0;
   if (SMEM) {
     threads = rmat::kSmemThreads;
-    smem = t->packed_bytes + (size_t)threads * rmat::kRingBytes;
+    smem = t->packed_bytes + (size_t)rmat::kSmemStrideThreads * rmat::kRingBytes;
     blocks = sms;
   } else {
     threads = rmat::kGlobalThreads;
@@ -282,7 +282,7 @@ rmat_status rmat_table_create(int device, const rmat_table_desc* d, rmat_table**
     t->fb = fb;
     t->packed_bytes = n * (fb == 16 ? 12ull : 20ull);
     t->packed_smem =
-        t->packed_bytes + (uint64_t)rmat::kSmemThreads * rmat::kRingBytes <=
+        t->packed_bytes + (uint64_t)rmat::kSmemStrideThreads * rmat::kRingBytes <=
             (uint64_t)max_smem_optin(device) ? 1u : 0u;
   }
   t->device_bytes = bytes;

@@ -147,9 +147,17 @@ template <> struct AEntry<32> { using T = uint4; };
 #ifndef RMAT_SMEM_THREADS
 #define RMAT_SMEM_THREADS 512
 #endif
+#ifndef RMAT_RING_FACTOR
+#define RMAT_RING_FACTOR 2
+#endif
 constexpr uint32_t kSectorBytes = RMAT_FLUSH_BYTES;  // bytes per flush store (16 or 32)
-constexpr uint32_t kRingBytes = 2 * kSectorBytes;   // staging bytes per thread
+// Ring = kRingFactor sectors per thread: 2 -> sector checks once per G
+// samples; 1 -> a check after every stored edge (half the shared memory).
+constexpr uint32_t kRingFactor = RMAT_RING_FACTOR;
+constexpr uint32_t kRingBytes = kRingFactor * kSectorBytes;  // staging bytes per thread
 constexpr int kSmemThreads = RMAT_SMEM_THREADS;     // packed_smem CTA size
+// slot-major ring addressing wants a power-of-two thread stride
+constexpr int kSmemStrideThreads = kSmemThreads <= 256 ? 256 : kSmemThreads <= 512 ? 512 : 1024;
 constexpr int kGlobalThreads = 256;                 // packed_global CTA size
 
 template <bool OUT64, int THREADS>
@@ -214,10 +222,11 @@ __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, 1)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
   constexpr int THREADS = SMEM ? kSmemThreads : kGlobalThreads;
+  constexpr int STHREADS = SMEM ? kSmemStrideThreads : kGlobalThreads;  // ring stride
   constexpr uint32_t EB = OUT64 ? 16 : 8;       // bytes per edge
   constexpr uint32_t G = kSectorBytes / EB;     // edges per sector (4 or 2)
-  constexpr uint32_t R = 2 * G;                 // ring slots
-  constexpr uint32_t STRIDE = THREADS * EB;     // slot-major ring
+  constexpr uint32_t R = kRingFactor * G;       // ring slots
+  constexpr uint32_t STRIDE = STHREADS * EB;    // slot-major ring
   extern __shared__ __align__(16) uint8_t smem[];
 
   const uint8_t* baseA;
@@ -335,7 +344,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     if (!roomy && left == 0) {
       // Stream done: write its partial last sector, account nf, open the next.
       if ((roff / STRIDE & (G - 1)) > lo)
-        flush_tail<OUT64, THREADS>(gptr, ring_sa, half, lo, roff / STRIDE & (G - 1));
+        flush_tail<OUT64, STHREADS>(gptr, ring_sa, half, lo, roff / STRIDE & (G - 1));
       if (COUNT) {
         // nf (generator.py:255-257): the highest sample of call j-1 that
         // produced an edge this stream needed.
@@ -415,15 +424,18 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           if (CAREFUL || R <= 4) --left;
         }
         if (COUNT) ebits |= (uint32_t)st << t;
-        if ((uint32_t)t % G == G - 1) {
-          // At most G edges since the last check: the sector at gptr is
-          // complete when the next slot has left its ring half.
-          const bool full = (roff / (G * STRIDE)) != half;
-          flush_full_pred<OUT64, THREADS>(gptr, ring_sa + half * G * STRIDE, full && lo == 0);
+        if (R == G || (uint32_t)t % G == G - 1) {
+          // Two-sector ring: at most G edges since the last check, the sector
+          // at gptr is complete when the next slot has left its ring half.
+          // One-sector ring: checked after every sample; complete when the
+          // slot index has just wrapped.
+          const bool full = R == G ? (st && (roff / STRIDE & (R - 1)) == 0)
+                                   : (roff / (G * STRIDE)) != half;
+          flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full && lo == 0);
           if (__any_sync(0xFFFFFFFFu, full && lo != 0) && full && lo != 0)  // unaligned stream head
-            flush_slots<OUT64, THREADS>(gptr, ring_sa + half * G * STRIDE, lo, G);
+            flush_slots<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, lo, G);
           gptr += full ? kSectorBytes : 0;
-          half ^= (uint32_t)full;
+          if (R > G) half ^= (uint32_t)full;
           lo = full ? 0 : lo;
         }
       }

@@ -1,0 +1,83 @@
+"""Throughput of the other §8 rows on one B200 (device-resident, CUDA events):
+
+* reference-stream mode (byte-identical to rmatgen.generate) at C3 shape;
+* partitioned mode C4: less-skewed (0.45,0.22,0.22,0.11), k=36, m=2^33, t=3,
+  8 parts, uint64 output -- each part timed alone on this GPU (its rows only);
+* the generic kernel forced on C3 (for reference).
+
+    python tools/bench_modes.py > profiles/rNN_modes.json
+"""
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1905_03525_b200 import GenConfig, build_variable_table, validate  # noqa: E402
+from paper_1905_03525_b200 import _native as N  # noqa: E402
+from paper_1905_03525_b200.generator import generate_shard  # noqa: E402
+from paper_1905_03525_b200.partition import default_plan, generate_part_device  # noqa: E402
+
+
+def timed(fn, reps=3, warm=2):
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3)
+    return float(np.median(ts))
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    res = {}
+    p = validate(0.57, 0.19, 0.19, 0.05, 28)
+    t = build_variable_table(p, 1 << 14)
+    m = 1 << 30
+    cfg = GenConfig(params=p, table=t, edge_count=m, seed=1, rng="reference")
+    out, _, _ = generate_shard(cfg, device=dev)
+    dt = timed(lambda: generate_shard(cfg, device=dev, out=out))
+    res["reference_stream_c3_shape"] = {"edges": m, "seconds": dt, "edges_per_s": m / dt,
+                                        "note": "numpy Philox4x64 blocks of 2^16, CTA per block"}
+    cfg = GenConfig(params=p, table=t, edge_count=m, seed=1, block_size=1024)
+    dt = timed(lambda: generate_shard(cfg, device=dev, out=out, kernel=N.KERNEL_GENERIC))
+    res["generic_kernel_c3_shape"] = {"edges": m, "seconds": dt, "edges_per_s": m / dt}
+    del out
+    torch.cuda.empty_cache()
+
+    pl = validate(0.45, 0.22, 0.22, 0.11, 36)
+    tl = build_variable_table(pl, 1 << 14)
+    plan = default_plan(36, 3, 1 << 33, 1, 8)
+    parts = []
+    for part in range(8):
+        o, tiles, _ = generate_part_device(plan, pl, tl, part, device=dev)
+        rows = o.shape[0]
+        del o
+        torch.cuda.empty_cache()
+        dt = timed(lambda: generate_part_device(plan, pl, tl, part, device=dev), reps=2, warm=1)
+        parts.append({"part": part, "edges": rows, "seconds": dt, "edges_per_s": rows / dt,
+                      "gb_per_s": rows * 16 / dt / 1e9})
+        torch.cuda.empty_cache()
+    tot = sum(x["edges"] for x in parts)
+    res["c4_partitioned"] = {"parts": parts, "total_edges": tot,
+                             "max_part_seconds": max(x["seconds"] for x in parts),
+                             "aggregate_edges_per_s_8gpu_estimate":
+                                 tot / max(x["seconds"] for x in parts),
+                             "note": "each part timed alone on one B200 (uint64 pairs, 16 B/edge); "
+                                     "the 8-GPU job time is the slowest part"}
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
