@@ -343,6 +343,12 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
 
   const bool out64 = a->out_width == 8;
   const bool count = a->samples_total || a->samples_per_stream;
+  // The non-PREFIX fast path assumes every stream starts on a 32-byte sector;
+  // anything else (tiles, odd stream lengths) takes the general variant.
+  const uint64_t G = out64 ? 2 : 4;
+  bool aligned = (E % G) == 0;
+  for (uint32_t i = 0; i < a->n_segments; ++i) aligned = aligned && (a->segments[i].out_row % G) == 0;
+  prefix = prefix || !aligned;
   int kernel = a->kernel;
   // one edge per sample at most (dmax <= k), 33-bit accumulators, and a
   // 32-bit Philox call index: E * k / dmin samples < 2^34.

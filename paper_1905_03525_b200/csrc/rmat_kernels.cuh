@@ -289,14 +289,19 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   uint32_t cur_r = 0, cur_c = 0, f = 0;
   uint64_t total_nf = 0;
   uint32_t ebits = 0;                // COUNT: samples of the current call that produced an edge
-  uint32_t left = (uint32_t)p.left;  // edges still to produce
-  // stage + roff = ring slot of the next edge; roff = slot * STRIDE + tid * EB
+  // Output bookkeeping.  stage + roff = ring slot of the next edge (roff =
+  // slot * STRIDE + tid * EB, slot = output row mod R).  The first unflushed
+  // sector starts at gptr, occupies ring half `half` and is valid from slot
+  // `lo` (only a tile stream's first sector can start mid-sector; block
+  // streams are sector-aligned, checked by the host).  L = edges of the
+  // stream not yet flushed; the edges still to produce are L - staged.
+  uint32_t L = (uint32_t)p.left;
   uint32_t roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
-  // The first unflushed sector starts at gptr, occupies ring half `half`, and
-  // is valid from slot lo.
   uint32_t half = roff / (G * STRIDE);
   uint32_t lo = roff / STRIDE & (G - 1);
+  L += lo;  // count the head's missing slots as already "staged"
   char* gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+  auto staged = [&]() { return ((roff / STRIDE) - half * G) & (R - 1); };
 
   // One call's worth of samples: words, bucket entries, byte selectors.
   struct Batch {
@@ -337,14 +342,103 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
     return q;
   };
+  // Rare (2^-(32-F) per sample): decide fraction ties with the lazy word.
+  auto resolve_ties = [&](Batch& cb) {
+    if (!cb.tie) return;
+    const u32x4 z4 = PREFIX ? stream_call(j, 1, p.sid, p.k0, p.k1)
+                            : philox4x32_10_rk(j, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
+    const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if ((uint32_t)mad_wide(cb.w[t] | fm, one, cb.b[t]) <= fm) {
+        const bool lt = (zq[t] & fm) < __ldg(tab.tlo + ((cb.w[t] & idxmask4) >> 2));
+        cb.sel[t] = lt ? 0x4410u : 0x4432u;
+        cb.seld[t] = lt ? 0x4440u : 0x4441u;
+      }
+  };
+  // Fragments of one call appended to the accumulators; stores into the ring
+  // and completed sectors flushed.  CAREFUL caps stores at `left`.
+  auto step = [&](Batch& cb, auto careful_tag, uint32_t& left) {
+    constexpr bool CAREFUL = decltype(careful_tag)::value;
+    if (COUNT) ebits = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      uint32_t r, c;
+      if constexpr (FB == 16) {
+        r = prmt(cb.a[t].x, cb.sel[t]);
+        c = prmt(cb.a[t].y, cb.sel[t]);
+      } else {
+        const bool lt = cb.sel[t] == 0x4410u;
+        r = lt ? cb.a[t].x : cb.a[t].y;
+        c = lt ? cb.a[t].z : cb.a[t].w;
+      }
+      const uint32_t d = prmt(cb.b[t], cb.seld[t]);
+      // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
+      const uint32_t pw = 1u << d;
+      const uint32_t tt = f + d;
+      // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
+      const uint32_t vr = mad_lo(cur_r, pw, r), vrh = mul_hi(cur_r, pw);
+      const uint32_t vc = mad_lo(cur_c, pw, c), vch = mul_hi(cur_c, pw);
+      const bool emit = tt >= k;
+      const uint32_t over = emit ? tt - k : tt;
+      cur_r = vr;
+      cur_c = vc;
+      f = over;
+      const bool st = CAREFUL ? (emit && left != 0) : emit;
+      uint64_t u = __funnelshift_r(vr, vrh, over) & kmask;
+      uint64_t v = __funnelshift_r(vc, vch, over) & kmask;
+      if constexpr (OUT64) {
+        u |= (uint64_t)((vrh >> over) & (k > 32 ? 1u : 0u)) << 32;  // k <= 33
+        v |= (uint64_t)((vch >> over) & (k > 32 ? 1u : 0u)) << 32;
+      }
+      if (PREFIX) { u |= p.rpre; v |= p.cpre; }
+      if (st) {
+        if constexpr (OUT64) {
+          sts128(stage_sa + roff, u, v);
+        } else {
+          sts64(stage_sa + roff, (uint32_t)u, (uint32_t)v);
+        }
+        // next slot; the mask keeps this thread's column bits (tid * EB < STRIDE)
+        roff = (roff + STRIDE) & (R * STRIDE - 1);
+        if (CAREFUL) --left;
+      }
+      if (COUNT) ebits |= (uint32_t)st << t;
+      if ((uint32_t)t % G == G - 1) {
+        // At most G edges since the last check: the sector at gptr is
+        // complete when the next slot has left its ring half.
+        const bool full = (roff / (G * STRIDE)) != half;
+        if constexpr (PREFIX) {
+          flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full && lo == 0);
+          if (__any_sync(0xFFFFFFFFu, full && lo != 0) && full && lo != 0)  // unaligned head
+            flush_slots<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, lo, G);
+          lo = full ? 0 : lo;
+        } else {
+          flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full);
+        }
+        gptr += full ? kSectorBytes : 0;
+        half ^= (uint32_t)full;
+        L -= full ? G : 0;
+      }
+    }
+  };
+
   for (;;) {
-    // Warp-uniform: in the common case every lane has >= 4 edges left, no
-    // stream ends during this call and the per-sample cap disappears.
-    const bool roomy = __all_sync(0xFFFFFFFFu, left >= 4);
-    if (!roomy && left == 0) {
+    // Warp-uniform fast path: every lane has >= 4 edges still to produce
+    // (L - staged >= L - (R - 1)), so no stream ends during this call and
+    // stores need no cap.
+    if (__all_sync(0xFFFFFFFFu, L >= 4 + R - 1)) {
+      Batch cb = fetch(j);
+      if (__any_sync(0xFFFFFFFFu, cb.tie)) resolve_ties(cb);
+      uint32_t unused = 0;
+      step(cb, std::false_type{}, unused);
+      ++j;
+      continue;
+    }
+    uint32_t left = L - staged();
+    if (left == 0) {
       // Stream done: write its partial last sector, account nf, open the next.
-      if ((roff / STRIDE & (G - 1)) > lo)
-        flush_tail<OUT64, STHREADS>(gptr, ring_sa, half, lo, roff / STRIDE & (G - 1));
+      const uint32_t hi_slot = roff / STRIDE & (G - 1);
+      if (hi_slot > lo) flush_tail<OUT64, STHREADS>(gptr, ring_sa, half, lo, hi_slot);
       if (COUNT) {
         // nf (generator.py:255-257): the highest sample of call j-1 that
         // produced an edge this stream needed.
@@ -356,98 +450,17 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       p = open_stream(g, s);
       if (!p.valid) break;
       j = 0; cur_r = cur_c = f = 0;
-      left = (uint32_t)p.left;
+      L = (uint32_t)p.left;
       roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
       half = roff / (G * STRIDE);
       lo = roff / STRIDE & (G - 1);
+      L += lo;
       gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+      continue;
     }
     Batch cb = fetch(j);
-    if (__any_sync(0xFFFFFFFFu, cb.tie)) {
-      // Rare (2^-(32-F) per sample): decide ties with the lazy word's low bits.
-      const u32x4 z4 = PREFIX ? stream_call(j, 1, p.sid, p.k0, p.k1)
-                              : philox4x32_10_rk(j, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
-      const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if ((uint32_t)mad_wide(cb.w[t] | fm, one, cb.b[t]) <= fm) {
-          const bool lt = (zq[t] & fm) < __ldg(tab.tlo + ((cb.w[t] & idxmask4) >> 2));
-          cb.sel[t] = lt ? 0x4410u : 0x4432u;
-          cb.seld[t] = lt ? 0x4440u : 0x4441u;
-        }
-    }
-    // Append the 4 fragments of `cb`.  Edges the
-    // stream still needs cap what may be stored; in the common case (>= 4
-    // left in every lane) the per-sample check disappears.
-    auto step = [&](auto careful_tag) {
-      constexpr bool CAREFUL = decltype(careful_tag)::value;
-      if (COUNT) ebits = 0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        uint32_t r, c;
-        if constexpr (FB == 16) {
-          r = prmt(cb.a[t].x, cb.sel[t]);
-          c = prmt(cb.a[t].y, cb.sel[t]);
-        } else {
-          const bool lt = cb.sel[t] == 0x4410u;
-          r = lt ? cb.a[t].x : cb.a[t].y;
-          c = lt ? cb.a[t].z : cb.a[t].w;
-        }
-        const uint32_t d = prmt(cb.b[t], cb.seld[t]);
-        // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
-        const uint32_t pw = 1u << d;
-        const uint32_t tt = f + d;
-        // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
-        const uint32_t vr = mad_lo(cur_r, pw, r), vrh = mul_hi(cur_r, pw);
-        const uint32_t vc = mad_lo(cur_c, pw, c), vch = mul_hi(cur_c, pw);
-        const bool emit = tt >= k;
-        const uint32_t over = emit ? tt - k : tt;
-        cur_r = vr;
-        cur_c = vc;
-        f = over;
-        const bool st = CAREFUL ? (emit && left != 0) : emit;
-        uint64_t u = __funnelshift_r(vr, vrh, over) & kmask;
-        uint64_t v = __funnelshift_r(vc, vch, over) & kmask;
-        if constexpr (OUT64) {
-          u |= (uint64_t)((vrh >> over) & (k > 32 ? 1u : 0u)) << 32;  // k <= 33
-          v |= (uint64_t)((vch >> over) & (k > 32 ? 1u : 0u)) << 32;
-        }
-        if (PREFIX) { u |= p.rpre; v |= p.cpre; }
-        if (st) {
-          if constexpr (OUT64) {
-            sts128(stage_sa + roff, u, v);
-          } else {
-            sts64(stage_sa + roff, (uint32_t)u, (uint32_t)v);
-          }
-          // next slot; the mask keeps this thread's column bits (tid * EB < STRIDE)
-          roff = (roff + STRIDE) & (R * STRIDE - 1);
-          if (CAREFUL || R <= 4) --left;
-        }
-        if (COUNT) ebits |= (uint32_t)st << t;
-        if (R == G || (uint32_t)t % G == G - 1) {
-          // Two-sector ring: at most G edges since the last check, the sector
-          // at gptr is complete when the next slot has left its ring half.
-          // One-sector ring: checked after every sample; complete when the
-          // slot index has just wrapped.
-          const bool full = R == G ? (st && (roff / STRIDE & (R - 1)) == 0)
-                                   : (roff / (G * STRIDE)) != half;
-          flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full && lo == 0);
-          if (__any_sync(0xFFFFFFFFu, full && lo != 0) && full && lo != 0)  // unaligned stream head
-            flush_slots<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, lo, G);
-          gptr += full ? kSectorBytes : 0;
-          if (R > G) half ^= (uint32_t)full;
-          lo = full ? 0 : lo;
-        }
-      }
-    };
-    if (roomy) {
-      const uint32_t roff0 = roff;
-      step(std::false_type{});
-      // <= 4 stores into a ring of > 4 slots: the slot advance is exact
-      if (R > 4) left -= ((roff - roff0) / STRIDE) & (R - 1);
-    } else {
-      step(std::true_type{});
-    }
+    if (__any_sync(__activemask(), cb.tie)) resolve_ties(cb);
+    step(cb, std::true_type{}, left);
     ++j;
   }
   if (COUNT && g.samples_total && total_nf)
