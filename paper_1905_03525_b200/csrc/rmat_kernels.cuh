@@ -285,6 +285,20 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 
   StreamPos p = open_stream(g, s);
   if (!p.valid) return;
+  // Tile segments carry their own key: rebuild the round keys per stream.
+  auto stream_keys = [&]() {
+    if (PREFIX) {
+      uint32_t k0 = p.k0, k1 = p.k1;
+#pragma unroll
+      for (int i = 0; i < 10; ++i) {
+        rk[2 * i] = k0;
+        rk[2 * i + 1] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+      }
+    }
+  };
+  stream_keys();
   uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
   uint32_t cur_r = 0, cur_c = 0, f = 0;
   uint64_t total_nf = 0;
@@ -313,12 +327,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // depend on the bit accumulator (software-pipelined one call ahead).
   auto fetch = [&](uint32_t jj) {
     Batch q;
-    u32x4 w4;
-    if (PREFIX) {
-      w4 = stream_call(jj, 0, p.sid, p.k0, p.k1);  // tile segments: per-stream key
-    } else {
-      w4 = philox4x32_10_rk(jj, 0, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
-    }
+    const u32x4 w4 = philox4x32_10_rk(jj, 0, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
     q.w[0] = w4.x; q.w[1] = w4.y; q.w[2] = w4.z; q.w[3] = w4.w;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -345,8 +354,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // Rare (2^-(32-F) per sample): decide fraction ties with the lazy word.
   auto resolve_ties = [&](Batch& cb) {
     if (!cb.tie) return;
-    const u32x4 z4 = PREFIX ? stream_call(j, 1, p.sid, p.k0, p.k1)
-                            : philox4x32_10_rk(j, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
+    const u32x4 z4 = philox4x32_10_rk(j, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
     const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
     for (int t = 0; t < 4; ++t)
@@ -409,8 +417,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         const bool full = (roff / (G * STRIDE)) != half;
         if constexpr (PREFIX) {
           flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full && lo == 0);
-          if (__any_sync(0xFFFFFFFFu, full && lo != 0) && full && lo != 0)  // unaligned head
-            flush_slots<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, lo, G);
+          // unaligned stream head (rare).  No warp vote here: on the careful
+          // path other lanes may be elsewhere in the loop.
+          if (full && lo != 0) flush_slots<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, lo, G);
           lo = full ? 0 : lo;
         } else {
           flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full);
@@ -449,6 +458,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       s += T;
       p = open_stream(g, s);
       if (!p.valid) break;
+      stream_keys();
       j = 0; cur_r = cur_c = f = 0;
       L = (uint32_t)p.left;
       roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;

@@ -175,3 +175,31 @@ def test_empty_and_single_edge(cuda):
     e = emit_block(table_for("f4"), 4, 1, (7, 0))
     want, nf = oracle.fast_stream(oracle_table_v("f4"), 4, 1, 7, 0)
     assert (e == want).all() and nf == 1
+
+
+# ---------------------------------------------------------------- divergence / alignment stress
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("E", [1023, 1021, 6])
+def test_unaligned_streams_at_scale(cuda, E):
+    """Streams not starting on 32-byte sectors take the general variant, whose
+    head/tail paths diverge inside the warp; must neither hang nor differ."""
+    k, m = 24, 3_000_001
+    table = table_for("v4096")
+    cfg = GenConfig(params=params_for(G500, k), table=table, edge_count=m, seed=3, block_size=E)
+    out, _, s = generate_shard(cfg, count_samples=True)
+    h = host(out)
+    nstreams = (m + E - 1) // E
+    picks = sorted(set(np.linspace(0, nstreams - 1, 24).astype(int).tolist()))
+    assert check_streams(h, oracle_table_v("v4096"), k, 3, E, 0, picks)
+
+
+@pytest.mark.timeout(300)
+def test_c4_scale_part_no_hang(cuda):
+    quads = LESS_SKEWED
+    k, t = 36, 3
+    p = params_for(quads, k)
+    plan = default_plan(k, t, 1 << 30, 1, 8)
+    out, tiles, s = generate_part_device(plan, p, table_for("v16384", quads), 0, count_samples=True)
+    assert out.shape[0] == sum(tc.count for tc in tiles)
+    v = out.view(torch.int64)
+    assert int((v[:, 0] >> (k - t)).max()) == 0  # part 0 owns tile row 0
