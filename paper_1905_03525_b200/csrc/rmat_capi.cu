@@ -442,6 +442,14 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
   const rmat_table* t = a->table;
   DeviceGuard guard(t->device);
   if (!guard.ok) return RMAT_ERR_DEVICE;
+  // packed shared-memory variant for power-of-two tables with 16-bit fragments
+  if (t->fb == 16 && t->scheme_p) {
+    const rmat::PackedTab pv = packed_view(t);
+    // static smem of the kernel (~300 B) stays well inside the 1 KiB margin
+    return rmat::launch_refstream(generic_view(t), t->dmax, *a,
+                                  reinterpret_cast<cudaStream_t>(cuda_stream), &pv,
+                                  num_sms(t->device), (size_t)max_smem_optin(t->device) - 1024);
+  }
   return rmat::launch_refstream(generic_view(t), t->dmax, *a,
                                 reinterpret_cast<cudaStream_t>(cuda_stream));
 }

@@ -40,6 +40,18 @@ struct RefLaunch {
   uint64_t rpre, cpre;
 };
 
+__device__ __forceinline__ uint64_t mad_wide_ref(uint32_t a, uint32_t b, uint32_t c) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"((uint64_t)c));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t prmt_ref(uint32_t a, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(a), "r"(sel));
+  return r;
+}
+
 __device__ __forceinline__ uint64_t lowmask64(uint32_t w) {
   return w >= 64 ? ~0ull : ((1ull << w) - 1);
 }
@@ -210,8 +222,199 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Packed variant: power-of-two tables whose fragments fit 16 bits (every
+// BASELINE config).  Persistent CTAs of 1024 threads stage the packed bucket
+// arrays (rmat_device.cuh) in shared memory once and walk their blocks; the
+// alias decision is the kernels' IMAD compare on the top fraction bits, ties
+// (p = 2^-16) settled with the low bits from the global TLO array -- exact,
+// because reference words carry the full 32-bit fraction.
+// ---------------------------------------------------------------------------
+constexpr int kRefPThreads = 1024;
+constexpr int kRefPChunk = 4 * kRefPThreads;
+
+template <bool OUT64>
+__global__ void __launch_bounds__(kRefPThreads, 1)
+k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t n = tab.n;
+  const size_t abytes = (size_t)n * 8, bbytes = (size_t)n * 4;
+  {
+    const uint4* srcA = reinterpret_cast<const uint4*>(tab.A);
+    uint4* dstA = reinterpret_cast<uint4*>(smem);
+    for (size_t i = threadIdx.x; i < abytes / 16; i += kRefPThreads) dstA[i] = __ldg(srcA + i);
+    const uint4* srcB = reinterpret_cast<const uint4*>(tab.B);
+    uint4* dstB = reinterpret_cast<uint4*>(smem + abytes);
+    for (size_t i = threadIdx.x; i < bbytes / 16; i += kRefPThreads) dstB[i] = __ldg(srcB + i);
+  }
+  const uint2* sA = reinterpret_cast<const uint2*>(smem);
+  const uint32_t* sB = reinterpret_cast<const uint32_t*>(smem + abytes);
+  uint32_t* s_rc = reinterpret_cast<uint32_t*>(smem + abytes + bbytes);  // row | col << 16
+  uint32_t* s_end = s_rc + kRefPChunk;                                   // inclusive-end offsets
+  __shared__ uint32_t s_warp[kRefPThreads / 32];
+  __shared__ uint64_t s_carry_r, s_carry_c;
+  __shared__ uint32_t s_carry_len;
+  __syncthreads();
+
+  const uint32_t tid = threadIdx.x;
+  const uint32_t k = g.k;
+  const uint64_t kmask = lowmask64(k);
+  const uint32_t fm = tab.fm, one = tab.one, nmask = n - 1;
+
+  for (uint64_t bi = blockIdx.x; bi < n_blocks; bi += gridDim.x) {
+    const uint64_t b = g.first_block + bi;
+    const uint64_t count = min(g.B, g.m - b * g.B);
+    char* const outb = reinterpret_cast<char*>(g.out) + bi * g.B * (OUT64 ? 16 : 8);
+    if (tid == 0) { s_carry_r = 0; s_carry_c = 0; s_carry_len = 0; }
+    __syncthreads();
+    uint64_t emitted = 0, chunk_base = 0, nf = 0;
+    while (emitted < count) {
+      // 1. draw + select 4 fragments per thread
+      const uint64_t call = chunk_base / 4 + tid;  // numpy counter = call + 1
+      const u64x4 w4 = philox4x64_10(call + 1, call + 1 == 0 ? 1 : 0, 0, 0, g.key0, b);
+      uint32_t dq[4], dsum = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t w = q == 0 ? w4.x : q == 1 ? w4.y : q == 2 ? w4.z : w4.w;
+        const uint32_t idx = (uint32_t)(w >> 32) & nmask;
+        const uint32_t frac = (uint32_t)w;
+        const uint32_t bw = sB[idx];
+        const uint2 aw = sA[idx];
+        const uint64_t sum = mad_wide_ref(frac | fm, one, bw);
+        uint32_t ge = (uint32_t)(sum >> 32);
+        if ((uint32_t)sum <= fm) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
+        const uint32_t sel = ge ? 0x4432u : 0x4410u;
+        const uint32_t r = prmt_ref(aw.x, sel), c = prmt_ref(aw.y, sel);
+        dq[q] = prmt_ref(bw, 0x4440u + ge);
+        s_rc[4 * tid + q] = r | (c << 16);
+        dsum += dq[q];
+      }
+      // 2. CTA exclusive scan of the depths (plus the carried bits)
+      uint32_t incl = dsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((tid & 31) >= (uint32_t)o) incl += v;
+      }
+      if ((tid & 31) == 31) s_warp[tid >> 5] = incl;
+      __syncthreads();
+      if (tid < 32) {
+        uint32_t v = s_warp[tid], x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (tid >= (uint32_t)o) x += y;
+        }
+        s_warp[tid] = x - v;  // exclusive warp offsets
+      }
+      __syncthreads();
+      const uint32_t carry_len = s_carry_len;
+      uint32_t pos = carry_len + s_warp[tid >> 5] + incl - dsum;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        pos += dq[q];
+        s_end[4 * tid + q] = pos;
+      }
+      const uint64_t carry_r = s_carry_r, carry_c = s_carry_c;
+      __syncthreads();
+      // 3. cut edges (k-bit windows of the concatenated bit strings)
+      const uint32_t ltot = s_end[kRefPChunk - 1];
+      const uint64_t avail = min((uint64_t)(ltot / k), count - emitted);
+      for (uint64_t e = tid; e < avail; e += kRefPThreads) {
+        const uint32_t lo = (uint32_t)e * k, hi = lo + k;
+        uint64_t ur = 0, uc = 0;
+        uint32_t p = lo;
+        if (p < carry_len) {
+          const uint32_t w = min(hi, carry_len) - p;
+          const uint32_t sh = carry_len - (p + w);
+          ur = (carry_r >> sh) & lowmask64(w);
+          uc = (carry_c >> sh) & lowmask64(w);
+          p += w;
+        }
+        if (p < hi) {
+          int l = 0, h = kRefPChunk - 1;
+          while (l < h) {
+            const int mid = (l + h) >> 1;
+            if (s_end[mid] > p) h = mid; else l = mid + 1;
+          }
+          int sidx = l;
+          while (p < hi) {
+            const uint32_t end = s_end[sidx];
+            const uint32_t w = min(hi, end) - p;
+            const uint32_t sh = end - (p + w);
+            const uint32_t rc = s_rc[sidx];
+            const uint64_t msk = lowmask64(w);
+            ur = (ur << w) | (((uint64_t)(rc & 0xFFFFu) >> sh) & msk);
+            uc = (uc << w) | (((uint64_t)(rc >> 16) >> sh) & msk);
+            p += w;
+            ++sidx;
+          }
+        }
+        const uint64_t row = emitted + e;
+        if (OUT64) {
+          reinterpret_cast<ulonglong2*>(outb)[row] =
+              make_ulonglong2((ur & kmask) | g.rpre, (uc & kmask) | g.cpre);
+        } else {
+          reinterpret_cast<uint2*>(outb)[row] =
+              make_uint2((uint32_t)(ur | g.rpre), (uint32_t)(uc | g.cpre));
+        }
+      }
+      // 4. carry / nf (one thread), then advance
+      if (tid == 0) {
+        const uint32_t used = (uint32_t)avail * k;
+        if (emitted + avail == count) {
+          int l = 0, h = kRefPChunk - 1;
+          while (l < h) {
+            const int mid = (l + h) >> 1;
+            if (s_end[mid] >= used) h = mid; else l = mid + 1;
+          }
+          nf = chunk_base + l + 1;
+        } else {
+          uint64_t cr = 0, cc = 0;
+          uint32_t p = used;
+          if (p < carry_len) {
+            const uint32_t w = carry_len - p;
+            cr = carry_r & lowmask64(w);
+            cc = carry_c & lowmask64(w);
+            p = carry_len;
+          }
+          if (p < ltot) {
+            int l = 0, h = kRefPChunk - 1;
+            while (l < h) {
+              const int mid = (l + h) >> 1;
+              if (s_end[mid] > p) h = mid; else l = mid + 1;
+            }
+            for (int sidx = l; sidx < kRefPChunk; ++sidx) {
+              const uint32_t end = s_end[sidx];
+              const uint32_t w = end - p;
+              const uint64_t msk = lowmask64(w);
+              const uint32_t rc = s_rc[sidx];
+              cr = (cr << w) | ((uint64_t)(rc & 0xFFFFu) & msk);
+              cc = (cc << w) | ((uint64_t)(rc >> 16) & msk);
+              p = end;
+            }
+          }
+          s_carry_r = cr;
+          s_carry_c = cc;
+          s_carry_len = ltot - used;
+        }
+      }
+      emitted += avail;
+      chunk_base += kRefPChunk;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      if (g.samples_per_block) g.samples_per_block[bi] = nf;
+      if (g.samples_total) atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)nf);
+    }
+    __syncthreads();
+  }
+}
+
 inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
-                                    const rmat_refstream_args& a, cudaStream_t st) {
+                                    const rmat_refstream_args& a, cudaStream_t st,
+                                    const PackedTab* packed = nullptr, int sms = 148,
+                                    size_t packed_smem_limit = 0) {
   // Bit offsets within one chunk must fit 32 bits: carry (< k) + 1024 * dmax.
   (void)dmax;
   RefLaunch g;
@@ -226,6 +429,19 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
   g.rpre = a.row_prefix;
   g.cpre = a.col_prefix;
   const uint64_t nb = a.n_blocks;
+  if (packed) {
+    // shared memory: buckets + chunk buffers (s_rc, s_end)
+    const size_t smem = (size_t)packed->n * 12 + (size_t)kRefPChunk * 8;
+    if (smem <= packed_smem_limit) {
+      auto kern = a.out_width == 8 ? k_refstream_packed<true> : k_refstream_packed<false>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return RMAT_ERR_CUDA;
+      const unsigned grid = (unsigned)std::min<uint64_t>(nb, (uint64_t)sms);
+      kern<<<grid, kRefPThreads, smem, st>>>(*packed, g, nb);
+      return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+    }
+  }
   for (uint64_t done = 0; done < nb;) {
     const uint64_t cnt = std::min<uint64_t>(nb - done, 1u << 30);
     RefLaunch gg = g;
