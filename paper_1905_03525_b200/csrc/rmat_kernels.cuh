@@ -352,9 +352,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     return q;
   };
   // Rare (2^-(32-F) per sample): decide fraction ties with the lazy word.
-  auto resolve_ties = [&](Batch& cb) {
+  auto resolve_ties = [&](Batch& cb, uint32_t jj) {
     if (!cb.tie) return;
-    const u32x4 z4 = philox4x32_10_rk(j, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
+    const u32x4 z4 = philox4x32_10_rk(jj, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
     const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
     for (int t = 0; t < 4; ++t)
@@ -435,12 +435,25 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     // Warp-uniform fast path: every lane has >= 4 edges still to produce
     // (L - staged >= L - (R - 1)), so no stream ends during this call and
     // stores need no cap.
-    if (__all_sync(0xFFFFFFFFu, L >= 4 + R - 1)) {
-      Batch cb = fetch(j);
-      if (__any_sync(0xFFFFFFFFu, cb.tie)) resolve_ties(cb);
+#ifndef RMAT_CALLS_PER_ITER
+#define RMAT_CALLS_PER_ITER 2
+#endif
+    constexpr int CPI = RMAT_CALLS_PER_ITER;  // Philox calls drawn back to back (ILP)
+    if (__all_sync(0xFFFFFFFFu, L >= 4 * CPI + R - 1)) {
+      Batch cb[CPI];
+#pragma unroll
+      for (int c = 0; c < CPI; ++c) cb[c] = fetch(j + c);
+      bool anytie = false;
+#pragma unroll
+      for (int c = 0; c < CPI; ++c) anytie |= cb[c].tie;
+      if (__any_sync(0xFFFFFFFFu, anytie)) {
+#pragma unroll
+        for (int c = 0; c < CPI; ++c) resolve_ties(cb[c], j + c);
+      }
       uint32_t unused = 0;
-      step(cb, std::false_type{}, unused);
-      ++j;
+#pragma unroll
+      for (int c = 0; c < CPI; ++c) step(cb[c], std::false_type{}, unused);
+      j += CPI;
       continue;
     }
     uint32_t left = L - staged();
@@ -469,7 +482,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       continue;
     }
     Batch cb = fetch(j);
-    if (__any_sync(__activemask(), cb.tie)) resolve_ties(cb);
+    if (__any_sync(__activemask(), cb.tie)) resolve_ties(cb, j);
     step(cb, std::true_type{}, left);
     ++j;
   }
