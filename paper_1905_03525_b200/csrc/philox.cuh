@@ -94,6 +94,45 @@ RMAT_HD u32x4 philox4x32_10_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c
   return u32x4{c0, c1, c2, c3};
 }
 
+// Per-stream constant part of the first two rounds of a primary-class call
+// (counter = (j, 0, sid_lo, sid_hi)): only word 0 varies with j, so the other
+// half of round 1 and half of round 2 are computed once per stream.
+struct PhiloxPre {
+  uint32_t q1, q2, q3, p3;
+};
+
+RMAT_HD PhiloxPre philox_pre(uint32_t s0, uint32_t s1, const uint32_t* rk) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  uint32_t H1, L1, H0b, L0b;
+  mul_wide32(M1, s0, H1, L1);
+  const uint32_t p0 = H1 ^ rk[0];
+  mul_wide32(M0, p0, H0b, L0b);
+  return PhiloxPre{s1 ^ rk[1], L1 ^ rk[2], H0b ^ rk[3], L0b};
+}
+
+RMAT_HD u32x4 philox4x32_10_pre(uint32_t j, const PhiloxPre& pp, const uint32_t* rk) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  uint32_t h0, l0, h1, l1;
+  // round 1 (words 0/1 of its output are stream constants folded into pp)
+  mul_wide32(M0, j, h0, l0);
+  uint32_t c2 = h0 ^ pp.q1, c3 = l0;
+  // round 2
+  mul_wide32(M1, c2, h1, l1);
+  uint32_t c0 = h1 ^ pp.q2, c1 = l1;
+  c2 = c3 ^ pp.q3;
+  c3 = pp.p3;
+#pragma unroll
+  for (int r = 2; r < 10; ++r) {
+    uint32_t hi0, lo0, hi1, lo1;
+    mul_wide32(M0, c0, hi0, lo0);
+    mul_wide32(M1, c2, hi1, lo1);
+    uint32_t n0 = hi1 ^ c1 ^ rk[2 * r];
+    uint32_t n2 = hi0 ^ c3 ^ rk[2 * r + 1];
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  return u32x4{c0, c1, c2, c3};
+}
+
 RMAT_HD void philox4x32_key_schedule(uint32_t k0, uint32_t k1, uint32_t* rk) {
   for (int r = 0; r < 10; ++r) {
     rk[2 * r] = k0;
