@@ -299,6 +299,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
   };
   stream_keys();
+  PhiloxPre pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
   uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
   uint32_t cur_r = 0, cur_c = 0, f = 0;
   uint64_t total_nf = 0;
@@ -327,7 +328,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // depend on the bit accumulator (software-pipelined one call ahead).
   auto fetch = [&](uint32_t jj) {
     Batch q;
-    const u32x4 w4 = philox4x32_10_rk(jj, 0, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
+    // primary call: rounds 1-2 partly precomputed per stream (philox.cuh)
+    const u32x4 w4 = philox4x32_10_pre(jj, pre, rk);
     q.w[0] = w4.x; q.w[1] = w4.y; q.w[2] = w4.z; q.w[3] = w4.w;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -472,6 +474,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       p = open_stream(g, s);
       if (!p.valid) break;
       stream_keys();
+      pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
       j = 0; cur_r = cur_c = f = 0;
       L = (uint32_t)p.left;
       roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
