@@ -136,6 +136,27 @@ typedef struct {
 
 rmat_status rmat_generate_refstream(const rmat_refstream_args* args, void* cuda_stream);
 
+/* Per-edge post-processing (reference postprocess.py): canonicalise to the
+ * lower triangle (to_undirected, :26-35), then relabel both endpoints with the
+ * 4-round scramble permutation of [0, 2^k) (scramble, :82-93; round keys from
+ * make_scramble_key, :61-79, computed on the host); MIRROR writes (u, v) and
+ * (v, u) for every edge (mirrored, :38-43).  in == out is allowed without MIRROR. */
+enum { RMAT_POST_UNDIRECTED = 1, RMAT_POST_SCRAMBLE = 2, RMAT_POST_MIRROR = 4 };
+
+typedef struct {
+  uint32_t flags;
+  uint32_t k;            /* endpoint bits (1..62) */
+  uint32_t width;        /* bytes per endpoint: 4 or 8 */
+  uint64_t rows;
+  const void* in;        /* device, rows x 2 */
+  void* out;             /* device, rows x 2 (2*rows x 2 with MIRROR) */
+  uint64_t mult[4];      /* scramble rounds: odd multiplier, xor-shift, rotation */
+  uint32_t xshift[4];
+  uint32_t rot[4];
+} rmat_post_args;
+
+rmat_status rmat_postprocess(const rmat_post_args* args, int device, void* cuda_stream);
+
 const char* rmat_strerror(rmat_status status);
 int rmat_abi_version(void);
 

@@ -49,6 +49,25 @@ from .table import (
     table_stats,
 )
 from ._native import NativeError, NativeUnavailable
+from .partition import (
+    MAX_TILE_BITS,
+    CountOverflowsTile,
+    PartitionPlan,
+    TileCount,
+    default_plan,
+    generate_part,
+    generate_tile,
+    plan_tiles,
+    split_quadrant_counts,
+)
+from .postprocess import (
+    ScrambleKey,
+    make_scramble_key,
+    mirrored,
+    scramble,
+    scramble_edges,
+    to_undirected,
+)
 
 __version__ = "0.1.0"
 
@@ -62,4 +81,8 @@ __all__ = [
     "DEFAULT_DEPTH_CAP", "MAX_FIXED_DEPTH", "DepthOutOfRange", "FragmentTable", "PathEntry",
     "SizeLimitTooSmall", "TableStats", "build_fixed_table", "build_variable_table",
     "table_stats", "NativeError", "NativeUnavailable", "__version__",
+    "MAX_TILE_BITS", "CountOverflowsTile", "PartitionPlan", "TileCount", "default_plan",
+    "generate_part", "generate_tile", "plan_tiles", "split_quadrant_counts",
+    "ScrambleKey", "make_scramble_key", "mirrored", "scramble", "scramble_edges",
+    "to_undirected",
 ]

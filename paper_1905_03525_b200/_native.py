@@ -16,7 +16,7 @@ _ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.environ.get("RMAT_LIB") or os.path.join(_PKG, "_build", "librmat_b200.so")
 _SOURCES = [os.path.join(_PKG, "csrc", f) for f in
             ("rmat_capi.cu", "rmat_kernels.cuh", "rmat_refstream.cuh", "rmat_device.cuh",
-             "philox.cuh")] + [os.path.join(_ROOT, "include", "rmat_b200.h")]
+             "rmat_post.cuh", "philox.cuh")] + [os.path.join(_ROOT, "include", "rmat_b200.h")]
 
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
@@ -101,12 +101,22 @@ class RefArgs(ctypes.Structure):
                 ("row_prefix", ctypes.c_uint64), ("col_prefix", ctypes.c_uint64)]
 
 
+class PostArgs(ctypes.Structure):
+    _fields_ = [("flags", ctypes.c_uint32), ("k", ctypes.c_uint32), ("width", ctypes.c_uint32),
+                ("rows", ctypes.c_uint64), ("in_", ctypes.c_void_p), ("out", ctypes.c_void_p),
+                ("mult", ctypes.c_uint64 * 4), ("xshift", ctypes.c_uint32 * 4),
+                ("rot", ctypes.c_uint32 * 4)]
+
+
+POST_UNDIRECTED, POST_SCRAMBLE, POST_MIRROR = 1, 2, 4
+
 KERNEL_AUTO, KERNEL_PACKED_SMEM, KERNEL_PACKED_GLOBAL, KERNEL_GENERIC = 0, 1, 2, 3
 KERNEL_NAMES = {1: "packed_smem", 2: "packed_global", 3: "generic"}
 
 #: symbols include/rmat_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
-           "rmat_replay_words", "rmat_generate_refstream", "rmat_strerror", "rmat_abi_version")
+           "rmat_replay_words", "rmat_generate_refstream", "rmat_postprocess", "rmat_strerror",
+           "rmat_abi_version")
 
 
 @lru_cache(maxsize=1)
@@ -131,11 +141,12 @@ def lib() -> ctypes.CDLL:
     L.rmat_replay_words.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                     ctypes.c_uint64, ctypes.c_uint64, vp, vp]
     L.rmat_generate_refstream.argtypes = [ctypes.POINTER(RefArgs), vp]
+    L.rmat_postprocess.argtypes = [ctypes.POINTER(PostArgs), ctypes.c_int, vp]
     L.rmat_strerror.argtypes = [ctypes.c_int]
     L.rmat_strerror.restype = ctypes.c_char_p
     L.rmat_abi_version.restype = ctypes.c_int
     for f in ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
-              "rmat_replay_words", "rmat_generate_refstream"):
+              "rmat_replay_words", "rmat_generate_refstream", "rmat_postprocess"):
         getattr(L, f).restype = ctypes.c_int
     return L
 

@@ -15,6 +15,7 @@
 #include "philox.cuh"
 #include "rmat_device.cuh"
 #include "rmat_kernels.cuh"
+#include "rmat_post.cuh"
 #include "rmat_refstream.cuh"
 
 struct rmat_table {
@@ -427,6 +428,21 @@ rmat_status rmat_replay_words(const rmat_table* t, uint64_t seed, uint64_t domai
   rmat::k_replay_words<<<blocks, threads, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       (int)t->scheme_p, t->lg, sid, (uint32_t)key, (uint32_t)(key >> 32), start, count, out);
   return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+}
+
+rmat_status rmat_postprocess(const rmat_post_args* a, int device, void* cuda_stream) {
+  if (!a || a->k < 1 || a->k > 62 || (a->width != 4 && a->width != 8) ||
+      (a->width == 4 && a->k > 32) || (a->flags & ~7u))
+    return RMAT_ERR_INVALID;
+  if (a->rows == 0) return RMAT_OK;
+  if (!a->in || !a->out) return RMAT_ERR_INVALID;
+  if ((a->flags & RMAT_POST_MIRROR) && a->in == a->out) return RMAT_ERR_INVALID;
+  if (a->flags & RMAT_POST_SCRAMBLE)
+    for (int r = 0; r < 4; ++r)
+      if (!(a->mult[r] & 1) || a->xshift[r] >= a->k || a->rot[r] >= a->k) return RMAT_ERR_INVALID;
+  DeviceGuard guard(device);
+  if (!guard.ok) return RMAT_ERR_DEVICE;
+  return rmat::launch_post(*a, num_sms(device), reinterpret_cast<cudaStream_t>(cuda_stream));
 }
 
 rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_stream) {

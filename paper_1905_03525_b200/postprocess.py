@@ -1,0 +1,167 @@
+"""Per-edge post-processing, same names and semantics as the
+reference's pkg/src/rmatgen/postprocess.py:
+
+* `to_undirected(edges)` -- (max, min) per edge (postprocess.py:26-35);
+* `mirrored(edges)` -- (u, v) then (v, u) (postprocess.py:38-43);
+* `make_scramble_key(seed, k)` / `scramble(values, key)` /
+  `scramble_edges(edges, key)` -- the seed-keyed 4-round bijection of
+  [0, 2^k) (postprocess.py:46-98), round keys derived on the host with the
+  splitmix64 finaliser exactly as the reference (_rng.py:41-50).
+
+Edge arrays may be device tensors (processed in HBM by `rmat_postprocess`)
+or host numpy arrays (copied through the GPU; same results).  Scalars go
+through the host formula.  `dedup_local` is not provided (§8 f2).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .device import require_cuda
+
+__all__ = ["ScrambleKey", "make_scramble_key", "scramble", "scramble_edges", "to_undirected",
+           "mirrored", "postprocess_device", "mix64"]
+
+_M64 = (1 << 64) - 1
+_GOLDEN = 0x9E3779B97F4A7C15
+
+
+def mix64(x: int) -> int:
+    """splitmix64 output function (reference _rng.py:41-50)."""
+    x &= _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+@dataclass(frozen=True)
+class ScrambleKey:
+    seed: int
+    k: int
+    round_keys: tuple[tuple[int, int, int], ...]
+
+
+def make_scramble_key(seed: int, k: int) -> ScrambleKey:
+    """Four (odd multiplier, xor-shift, rotation) rounds from (seed, k) (postprocess.py:61-79)."""
+    if not 1 <= k <= 62:
+        raise ValueError(f"k must be in [1, 62], got {k}")
+    mask = (1 << k) - 1
+    state = mix64((seed & _M64) ^ mix64(k))
+    rounds = []
+    for _ in range(4):
+        state = mix64((state + _GOLDEN) & _M64)
+        mult = (state & mask) | 1
+        state = mix64((state + _GOLDEN) & _M64)
+        xshift = 1 + state % (k - 1) if k > 1 else 0
+        state = mix64((state + _GOLDEN) & _M64)
+        rounds.append((mult, xshift, state % k))
+    return ScrambleKey(seed=seed, k=k, round_keys=tuple(rounds))
+
+
+def _scramble_int(x: int, key: ScrambleKey) -> int:
+    k, mask = key.k, (1 << key.k) - 1
+    for mult, xs, rot in key.round_keys:
+        x = (x * mult) & mask
+        if xs:
+            x ^= x >> xs
+        if rot:
+            x = ((x << rot) | (x >> (k - rot))) & mask
+    return x
+
+
+def postprocess_device(edges, *, k: int, undirected: bool = False, key: ScrambleKey | None = None,
+                       mirror: bool = False, out=None):
+    """Apply the selected steps to a device (rows, 2) tensor; returns the output tensor.
+
+    Order as the reference CLI (cli.py:246-251): undirected, then scramble;
+    `mirror` emits both orientations of each processed edge.
+    """
+    import torch
+
+    if edges.device.type != "cuda" or edges.dim() != 2 or edges.shape[1] != 2:
+        raise ValueError("edges must be a (rows, 2) CUDA tensor")
+    edges = edges.contiguous()
+    rows = edges.shape[0]
+    if out is None:
+        out = (torch.empty((2 * rows, 2), dtype=edges.dtype, device=edges.device) if mirror
+               else edges)
+    flags = (N.POST_UNDIRECTED if undirected else 0) | (N.POST_SCRAMBLE if key else 0) | \
+        (N.POST_MIRROR if mirror else 0)
+    args = N.PostArgs(flags=flags, k=k, width=edges.element_size(), rows=rows,
+                      in_=edges.data_ptr() if rows else None,
+                      out=out.data_ptr() if rows else None)
+    if key is not None:
+        if key.k != k:
+            raise ValueError(f"scramble key is for k={key.k}, edges are k={k}")
+        for r, (mult, xs, rot) in enumerate(key.round_keys):
+            args.mult[r], args.xshift[r], args.rot[r] = mult, xs, rot
+    with torch.cuda.device(edges.device):
+        N.check(N.lib().rmat_postprocess(ctypes.byref(args), edges.device.index,
+                                         torch.cuda.current_stream(edges.device).cuda_stream),
+                "rmat_postprocess")
+    return out
+
+
+def _host_roundtrip(edges: np.ndarray, k: int, **kw) -> np.ndarray:
+    import torch
+
+    dev = require_cuda()
+    arr = np.ascontiguousarray(edges)
+    if arr.dtype != np.uint64:
+        raise ValueError("host edge arrays must be uint64 (rows, 2) like the reference's")
+    width32 = k <= 32
+    t = torch.from_numpy(arr.astype(np.uint32) if width32 else arr.view(np.int64)).to(dev)
+    res = postprocess_device(t, k=k, **kw).cpu().numpy()
+    return res.astype(np.uint64) if width32 else res.view(np.uint64)
+
+
+def _bits(edges) -> int:
+    if hasattr(edges, "device"):
+        return 32 if edges.element_size() == 4 else 62
+    return 62
+
+
+def to_undirected(edges, k: int | None = None):
+    """(max, min) per edge; idempotent (reference postprocess.py:26-35)."""
+    kk = k or _bits(edges)
+    if isinstance(edges, np.ndarray):
+        if len(edges) == 0:
+            return edges.copy()
+        kk = k or max(1, int(edges.max()).bit_length())
+        return _host_roundtrip(edges, kk, undirected=True)
+    return postprocess_device(edges.clone(), k=kk, undirected=True)
+
+
+def mirrored(edges, k: int | None = None):
+    """Both orientations of every edge, (u, v) then (v, u) (reference postprocess.py:38-43)."""
+    if isinstance(edges, np.ndarray):
+        if len(edges) == 0:
+            return np.empty((0, 2), dtype=edges.dtype)
+        kk = k or max(1, int(edges.max()).bit_length())
+        return _host_roundtrip(edges, kk, mirror=True)
+    return postprocess_device(edges, k=k or _bits(edges), mirror=True)
+
+
+def scramble(values, key: ScrambleKey):
+    """Apply the key's permutation of [0, 2^k) to an int or a uint64 array."""
+    if not isinstance(values, np.ndarray):
+        return _scramble_int(int(values), key)
+    flat = np.ascontiguousarray(values, dtype=np.uint64).reshape(-1)
+    if flat.size == 0:
+        return flat.reshape(np.shape(values))
+    pad = flat if flat.size % 2 == 0 else np.append(flat, np.uint64(0))
+    out = _host_roundtrip(pad.reshape(-1, 2), key.k, key=key).reshape(-1)[:flat.size]
+    return out.reshape(np.shape(values))
+
+
+def scramble_edges(edges, key: ScrambleKey):
+    """Scramble both endpoints of an (m, 2) edge array (reference postprocess.py:96-98)."""
+    if isinstance(edges, np.ndarray):
+        if len(edges) == 0:
+            return edges.copy()
+        return _host_roundtrip(edges, key.k, key=key)
+    return postprocess_device(edges.clone(), k=key.k, key=key)

@@ -179,6 +179,20 @@ def main() -> None:
                       "table": "less:v16384" if k == 36 else "g500:v1024", "edges": sha(e)})
     out["ref_tiles"] = tiles
 
+    # ---- post-processing (f3): scramble keys and permutations, undirected, mirrored
+    from rmatgen.postprocess import make_scramble_key, mirrored, scramble, to_undirected
+    post = {"keys": [], "scramble": [], "undirected": None, "mirrored": None}
+    for seed, k in ((1, 1), (123, 5), (9, 13), (7, 20), (1, 28), (41, 33), (5, 62), (2**64 - 1, 36)):
+        key = make_scramble_key(seed, k)
+        post["keys"].append({"seed": seed, "k": k, "rounds": [list(r) for r in key.round_keys]})
+        vals = (np.arange(1 << min(k, 16), dtype=np.uint64) * np.uint64(2654435761)) & np.uint64((1 << k) - 1)
+        post["scramble"].append({"seed": seed, "k": k, "values": sha(vals), "image": sha(scramble(vals, key))})
+    rng = np.random.default_rng(5)
+    e = rng.integers(0, 1 << 20, size=(5000, 2), dtype=np.uint64)
+    post["undirected"] = {"input_seed": 5, "n": 5000, "bits": 20, "out": sha(to_undirected(e))}
+    post["mirrored"] = {"input_seed": 5, "n": 5000, "bits": 20, "out": sha(mirrored(e))}
+    out["postprocess"] = post
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", os.path.join(HERE, "golden.json"))
