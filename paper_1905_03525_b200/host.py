@@ -16,7 +16,7 @@ from .device import DeviceTable, device_table, launch_generate, launch_refstream
 from .generator import DOMAIN_BLOCK, GenConfig, edge_dtype, shard_rows
 from .params import check_k
 
-__all__ = ["generate_to_host", "DEFAULT_CHUNK_EDGES"]
+__all__ = ["generate_to_host", "write_edges", "DEFAULT_CHUNK_EDGES"]
 
 DEFAULT_CHUNK_EDGES = 1 << 28
 
@@ -97,3 +97,86 @@ def generate_to_host(config: GenConfig, out=None, *, rank: int = 0, world: int =
     if fresh_table:
         dt.close()
     return {"out": out, "r_lo": r_lo, "h2d_bytes": h2d}
+
+
+def write_edges(config: GenConfig, path: str, fmt: str = "binary", *, rank: int = 0,
+                world: int = 1, device=None, chunk_edges: int = DEFAULT_CHUNK_EDGES) -> dict:
+    """Stream rows of shard `rank`/`world` to `path` in the reference's file format.
+
+    binary: consecutive (u, v) records of two 64-bit little-endian uints, the
+    reference's `rmat generate --format binary` (cli.py:201-206); text: one
+    "u v" line per edge.  Written to a temporary file and renamed atomically
+    (cli.py:186-198).  Generation, widening to 64 bits, the device->host copy
+    and the file write overlap chunk by chunk.
+    """
+    import os
+    import threading
+
+    import torch
+
+    if fmt not in ("binary", "text"):
+        raise ValueError(f"fmt must be 'binary' or 'text', got {fmt!r}")
+    k = config.params.k
+    check_k(k)
+    dev = require_cuda(device)
+    B = config.stream_edges
+    s_lo, s_hi, r_lo, r_hi = shard_rows(config.edge_count, B, rank, world)
+    dt = device_table(config.table, dev)
+    streams_per_chunk = max(1, chunk_edges // B)
+    rows_per_chunk = streams_per_chunk * B
+    gen = torch.empty((min(rows_per_chunk, max(r_hi - r_lo, 1)), 2), dtype=edge_dtype(k), device=dev)
+    hosts = [torch.empty((gen.shape[0], 2), dtype=torch.int64, pin_memory=True) for _ in range(2)]
+    tmp = f"{path}.tmp.{os.getpid()}"
+    written = 0
+    err: list[BaseException] = []
+    try:
+        with open(tmp, "wb") as f:
+            writer = None
+            s = s_lo
+            i = 0
+            while s < s_hi:
+                ns = min(streams_per_chunk, s_hi - s)
+                c_lo, c_hi = s * B, min((s + ns) * B, config.edge_count)
+                n = c_hi - c_lo
+                buf = gen[:n]
+                if config.rng == "reference":
+                    launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, config.edge_count, s, ns,
+                                     buf)
+                else:
+                    launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B, [(s, n, 0, 0, 0)], buf)
+                wide = (buf.view(torch.int32).to(torch.int64) & 0xFFFFFFFF) if k <= 32 else \
+                    buf.view(torch.int64)
+                if writer is not None:
+                    writer.join()  # host buffer i % 2 is free again
+                    if err:
+                        raise err[0]
+                h = hosts[i % 2][:n]
+                h.copy_(wide, non_blocking=False)
+
+                def _write(h=h):
+                    try:
+                        arr = h.numpy()
+                        if fmt == "binary":
+                            f.write(memoryview(arr.astype("<i8", copy=False)).cast("B"))
+                        else:
+                            np.savetxt(f, arr.view(np.uint64), fmt="%d")
+                    except BaseException as exc:  # surfaced on the main thread
+                        err.append(exc)
+
+                writer = threading.Thread(target=_write)
+                writer.start()
+                written += n
+                s += ns
+                i += 1
+            if writer is not None:
+                writer.join()
+                if err:
+                    raise err[0]
+        os.replace(tmp, path)
+    except BaseException:
+        try:
+            os.unlink(tmp)
+        except OSError:
+            pass
+        raise
+    return {"path": path, "rows": written, "r_lo": r_lo}
