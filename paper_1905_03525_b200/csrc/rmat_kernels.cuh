@@ -440,7 +440,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #ifndef RMAT_CALLS_PER_ITER
 #define RMAT_CALLS_PER_ITER 2
 #endif
-    constexpr int CPI = RMAT_CALLS_PER_ITER;  // Philox calls drawn back to back (ILP)
+    // Philox calls drawn back to back (ILP).  Two calls fit the 128-register
+    // budget of the 512-thread shared-memory CTA only for the plain variant.
+    constexpr int CPI = (SMEM && (PREFIX || OUT64 || FB == 32)) ? 1 : RMAT_CALLS_PER_ITER;
     if (__all_sync(0xFFFFFFFFu, L >= 4 * CPI + R - 1)) {
       Batch cb[CPI];
 #pragma unroll

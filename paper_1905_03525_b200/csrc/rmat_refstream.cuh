@@ -260,6 +260,8 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
   const uint32_t k = g.k;
   const uint64_t kmask = lowmask64(k);
   const uint32_t fm = tab.fm, one = tab.one, nmask = n - 1;
+  // ceil(2^32 / k): exact ceil-division by k for the < 2^17 bit offsets of a chunk
+  const uint32_t kmagic = (uint32_t)((0x100000000ull + k - 1) / k);
 
   for (uint64_t bi = blockIdx.x; bi < n_blocks; bi += gridDim.x) {
     const uint64_t b = g.first_block + bi;
@@ -317,46 +319,54 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
       }
       const uint64_t carry_r = s_carry_r, carry_c = s_carry_c;
       __syncthreads();
-      // 3. cut edges (k-bit windows of the concatenated bit strings)
+      // 3. cut edges (k-bit windows of the concatenated bit strings).  Each
+      // thread cuts the edges that *start* in its own 4 fragments (thread 0
+      // also owns the carried bits), so no search is needed: the starting
+      // fragment is found among its registers, the walk continues in smem.
       const uint32_t ltot = s_end[kRefPChunk - 1];
       const uint64_t avail = min((uint64_t)(ltot / k), count - emitted);
-      for (uint64_t e = tid; e < avail; e += kRefPThreads) {
-        const uint32_t lo = (uint32_t)e * k, hi = lo + k;
-        uint64_t ur = 0, uc = 0;
-        uint32_t p = lo;
-        if (p < carry_len) {
-          const uint32_t w = min(hi, carry_len) - p;
-          const uint32_t sh = carry_len - (p + w);
-          ur = (carry_r >> sh) & lowmask64(w);
-          uc = (carry_c >> sh) & lowmask64(w);
-          p += w;
-        }
-        if (p < hi) {
-          int l = 0, h = kRefPChunk - 1;
-          while (l < h) {
-            const int mid = (l + h) >> 1;
-            if (s_end[mid] > p) h = mid; else l = mid + 1;
-          }
-          int sidx = l;
-          while (p < hi) {
-            const uint32_t end = s_end[sidx];
-            const uint32_t w = min(hi, end) - p;
-            const uint32_t sh = end - (p + w);
-            const uint32_t rc = s_rc[sidx];
-            const uint64_t msk = lowmask64(w);
-            ur = (ur << w) | (((uint64_t)(rc & 0xFFFFu) >> sh) & msk);
-            uc = (uc << w) | (((uint64_t)(rc >> 16) >> sh) & msk);
+      {
+        const uint32_t r_lo = tid == 0 ? 0u : pos - (dq[0] + dq[1] + dq[2] + dq[3]);
+        const uint32_t r_hi = pos;  // end of this thread's last fragment
+        // edges j with r_lo <= j*k < r_hi:  ceil(x / k) = umulhi(x + k - 1, ceil(2^32 / k))
+        uint32_t j = k == 1 ? r_lo : __umulhi(r_lo + k - 1, kmagic);  // (2^32 overflows at k=1)
+        uint32_t j_end = k == 1 ? r_hi : __umulhi(r_hi + k - 1, kmagic);
+        j_end = (uint32_t)min((uint64_t)j_end, avail);
+        for (; j < j_end; ++j) {
+          const uint32_t lo = j * k, hi = lo + k;
+          uint64_t ur = 0, uc = 0;
+          uint32_t p = lo;
+          if (p < carry_len) {
+            const uint32_t w = min(hi, carry_len) - p;
+            const uint32_t sh = carry_len - (p + w);
+            ur = (carry_r >> sh) & lowmask64(w);
+            uc = (carry_c >> sh) & lowmask64(w);
             p += w;
-            ++sidx;
           }
-        }
-        const uint64_t row = emitted + e;
-        if (OUT64) {
-          reinterpret_cast<ulonglong2*>(outb)[row] =
-              make_ulonglong2((ur & kmask) | g.rpre, (uc & kmask) | g.cpre);
-        } else {
-          reinterpret_cast<uint2*>(outb)[row] =
-              make_uint2((uint32_t)(ur | g.rpre), (uint32_t)(uc | g.cpre));
+          if (p < hi) {
+            // first of this thread's fragments ending after p
+            const uint32_t e0 = r_hi - dq[3] - dq[2] - dq[1], e1 = e0 + dq[1], e2 = e1 + dq[2];
+            int sidx = 4 * (int)tid + (p >= e0) + (p >= e1) + (p >= e2);
+            while (p < hi) {
+              const uint32_t end = s_end[sidx];
+              const uint32_t w = min(hi, end) - p;
+              const uint32_t sh = end - (p + w);
+              const uint32_t rc = s_rc[sidx];
+              const uint64_t msk = lowmask64(w);
+              ur = (ur << w) | (((uint64_t)(rc & 0xFFFFu) >> sh) & msk);
+              uc = (uc << w) | (((uint64_t)(rc >> 16) >> sh) & msk);
+              p += w;
+              ++sidx;
+            }
+          }
+          const uint64_t row = emitted + j;
+          if (OUT64) {
+            reinterpret_cast<ulonglong2*>(outb)[row] =
+                make_ulonglong2((ur & kmask) | g.rpre, (uc & kmask) | g.cpre);
+          } else {
+            reinterpret_cast<uint2*>(outb)[row] =
+                make_uint2((uint32_t)(ur | g.rpre), (uint32_t)(uc | g.cpre));
+          }
         }
       }
       // 4. carry / nf (one thread), then advance
