@@ -252,7 +252,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
   uint32_t* s_rc = reinterpret_cast<uint32_t*>(smem + abytes + bbytes);  // row | col << 16
   uint32_t* s_end = s_rc + kRefPChunk;                                   // inclusive-end offsets
   __shared__ uint32_t s_warp[kRefPThreads / 32];
-  __shared__ uint64_t s_carry_r, s_carry_c;
+  __shared__ uint64_t s_carry_r, s_carry_c, s_nf;
   __shared__ uint32_t s_carry_len;
   __syncthreads();
 
@@ -269,7 +269,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
     char* const outb = reinterpret_cast<char*>(g.out) + bi * g.B * (OUT64 ? 16 : 8);
     if (tid == 0) { s_carry_r = 0; s_carry_c = 0; s_carry_len = 0; }
     __syncthreads();
-    uint64_t emitted = 0, chunk_base = 0, nf = 0;
+    uint64_t emitted = 0, chunk_base = 0;
     while (emitted < count) {
       // 1. draw + select 4 fragments per thread
       const uint64_t call = chunk_base / 4 + tid;  // numpy counter = call + 1
@@ -331,9 +331,19 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
         // edges j with r_lo <= j*k < r_hi:  ceil(x / k) = umulhi(x + k - 1, ceil(2^32 / k))
         uint32_t j = k == 1 ? r_lo : __umulhi(r_lo + k - 1, kmagic);  // (2^32 overflows at k=1)
         uint32_t j_end = k == 1 ? r_hi : __umulhi(r_hi + k - 1, kmagic);
-        j_end = (uint32_t)min((uint64_t)j_end, avail);
+        // j == avail is the first incomplete edge: its bits so far become the
+        // next chunk's carry (cut by the thread whose range holds its start).
+        const bool final_chunk = emitted + avail == count;
+        j_end = (uint32_t)min((uint64_t)j_end, avail + (final_chunk ? 0 : 1));
+        // an empty carry starts exactly at ltot, outside every thread's range
+        if (!final_chunk && tid == kRefPThreads - 1 && avail * k == ltot) {
+          s_carry_r = 0;
+          s_carry_c = 0;
+          s_carry_len = 0;
+        }
         for (; j < j_end; ++j) {
-          const uint32_t lo = j * k, hi = lo + k;
+          const bool is_carry = j == avail;
+          const uint32_t lo = j * k, hi = is_carry ? ltot : lo + k;
           uint64_t ur = 0, uc = 0;
           uint32_t p = lo;
           if (p < carry_len) {
@@ -343,10 +353,11 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
             uc = (carry_c >> sh) & lowmask64(w);
             p += w;
           }
+          int sidx = 0;
           if (p < hi) {
             // first of this thread's fragments ending after p
             const uint32_t e0 = r_hi - dq[3] - dq[2] - dq[1], e1 = e0 + dq[1], e2 = e1 + dq[2];
-            int sidx = 4 * (int)tid + (p >= e0) + (p >= e1) + (p >= e2);
+            sidx = 4 * (int)tid + (p >= e0) + (p >= e1) + (p >= e2);
             while (p < hi) {
               const uint32_t end = s_end[sidx];
               const uint32_t w = min(hi, end) - p;
@@ -359,6 +370,15 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
               ++sidx;
             }
           }
+          if (is_carry) {
+            s_carry_r = ur;
+            s_carry_c = uc;
+            s_carry_len = ltot - lo;
+            continue;
+          }
+          // nf (generator.py:255-257): one past the fragment holding the last
+          // edge's last bit
+          if (final_chunk && j + 1 == avail) s_nf = chunk_base + sidx;
           const uint64_t row = emitted + j;
           if (OUT64) {
             reinterpret_cast<ulonglong2*>(outb)[row] =
@@ -369,51 +389,12 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
           }
         }
       }
-      // 4. carry / nf (one thread), then advance
-      if (tid == 0) {
-        const uint32_t used = (uint32_t)avail * k;
-        if (emitted + avail == count) {
-          int l = 0, h = kRefPChunk - 1;
-          while (l < h) {
-            const int mid = (l + h) >> 1;
-            if (s_end[mid] >= used) h = mid; else l = mid + 1;
-          }
-          nf = chunk_base + l + 1;
-        } else {
-          uint64_t cr = 0, cc = 0;
-          uint32_t p = used;
-          if (p < carry_len) {
-            const uint32_t w = carry_len - p;
-            cr = carry_r & lowmask64(w);
-            cc = carry_c & lowmask64(w);
-            p = carry_len;
-          }
-          if (p < ltot) {
-            int l = 0, h = kRefPChunk - 1;
-            while (l < h) {
-              const int mid = (l + h) >> 1;
-              if (s_end[mid] > p) h = mid; else l = mid + 1;
-            }
-            for (int sidx = l; sidx < kRefPChunk; ++sidx) {
-              const uint32_t end = s_end[sidx];
-              const uint32_t w = end - p;
-              const uint64_t msk = lowmask64(w);
-              const uint32_t rc = s_rc[sidx];
-              cr = (cr << w) | ((uint64_t)(rc & 0xFFFFu) & msk);
-              cc = (cc << w) | ((uint64_t)(rc >> 16) & msk);
-              p = end;
-            }
-          }
-          s_carry_r = cr;
-          s_carry_c = cc;
-          s_carry_len = ltot - used;
-        }
-      }
       emitted += avail;
       chunk_base += kRefPChunk;
       __syncthreads();
     }
     if (tid == 0) {
+      const uint64_t nf = s_nf;
       if (g.samples_per_block) g.samples_per_block[bi] = nf;
       if (g.samples_total) atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)nf);
     }
