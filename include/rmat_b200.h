@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define RMAT_ABI_VERSION 1
+#define RMAT_ABI_VERSION 2
 
 typedef enum {
   RMAT_OK = 0,
@@ -132,9 +132,54 @@ typedef struct {
   uint64_t* samples_total;    /* device, optional */
   uint64_t row_prefix;        /* OR'd into every endpoint (partition tiles), else 0 */
   uint64_t col_prefix;
+  uint64_t word_offset;       /* first word of every block stream consumed (0 = stream start);
+                                 a later `_emit` on the same numpy Generator continues there
+                                 (partition.py:156-159) */
 } rmat_refstream_args;
 
 rmat_status rmat_generate_refstream(const rmat_refstream_args* args, void* cuda_stream);
+
+/* Sum of the selected fragments' depths over words [word_begin, word_begin +
+ * word_count) of the reference stream keyed [key0, key1], added to *sum
+ * (device).  The reference's `_emit_general` draws words in batches until their
+ * depths cover count*k bits (generator.py:244-253); the caller replays that
+ * loop with these sums to know where the Generator stands afterwards. */
+rmat_status rmat_refstream_depth_sum(const rmat_table* table, uint64_t key0, uint64_t key1,
+                                     uint64_t word_begin, uint64_t word_count, uint64_t* sum,
+                                     void* cuda_stream);
+
+/* First-occurrence dedup of an edge batch against everything inserted into the
+ * same set since its last reset (reference postprocess.dedup_local,
+ * postprocess.py:101-126, applied incrementally as partition.py:155-160 does
+ * on concatenate([edges, more])).  Rows of `in` whose (u, v) has not been seen
+ * -- and is not repeated earlier in `in` -- are written to `out` in input
+ * order; *kept (device) receives their number.  `in` and `out` must not
+ * overlap.  Workspace: `set` of rmat_dedup_set_bytes(capacity) bytes (capacity
+ * a power of two above the number of distinct keys the set will hold; half
+ * full or less keeps probing short), `scratch` of rmat_dedup_scratch_bytes(rows).
+ * *status (device, optional) gets RMAT_DEDUP_STATUS_* bits OR'd in. */
+enum { RMAT_DEDUP_RESET = 1, RMAT_DEDUP_CHECK_RANGE = 2 };
+enum { RMAT_DEDUP_STATUS_RANGE = 1, RMAT_DEDUP_STATUS_FULL = 2 };
+
+typedef struct {
+  uint32_t flags;          /* RMAT_DEDUP_RESET: clear the set first; CHECK_RANGE: flag edges
+                              outside [row_lo, row_hi) x [col_lo, col_hi) */
+  uint32_t width;          /* bytes per endpoint: 4 or 8 */
+  uint64_t rows;
+  const void* in;          /* device, rows x 2 */
+  void* out;               /* device, up to rows x 2 */
+  uint64_t index_base;     /* priority of in[0]; must exceed every earlier row of this set */
+  void* set;               /* device workspace */
+  uint64_t capacity;       /* slots, power of two */
+  void* scratch;           /* device workspace */
+  uint64_t* kept;          /* device: rows written to out */
+  uint32_t* status;        /* device, optional */
+  uint64_t row_lo, row_hi, col_lo, col_hi;
+} rmat_dedup_args;
+
+uint64_t rmat_dedup_set_bytes(uint64_t capacity);
+uint64_t rmat_dedup_scratch_bytes(uint64_t rows);
+rmat_status rmat_dedup(const rmat_dedup_args* args, int device, void* cuda_stream);
 
 /* Per-edge post-processing (reference postprocess.py): canonicalise to the
  * lower triangle (to_undirected, :26-35), then relabel both endpoints with the

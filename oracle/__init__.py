@@ -70,6 +70,12 @@ def lib() -> ctypes.CDLL:
     L.oracle_ref_stream.argtypes = T + [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
                                         ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u64p]
     L.oracle_ref_stream.restype = ctypes.c_int64
+    L.oracle_ref_stream_from.argtypes = T + [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                             ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                             ctypes.c_uint64, _u64p]
+    L.oracle_ref_stream_from.restype = ctypes.c_int64
+    L.oracle_ref_depth_sum.argtypes = T + [ctypes.c_uint64] * 4
+    L.oracle_ref_depth_sum.restype = ctypes.c_uint64
     return L
 
 
@@ -81,19 +87,21 @@ def _p(a: np.ndarray, ptype):
 class OracleTable:
     """The compiled arrays the reference's kernels read (generator.py:114-130)."""
 
-    def __init__(self, thr32, alias, row, col, depth):
+    def __init__(self, thr32, alias, row, col, depth, mean_depth: float | None = None):
         self.thr32 = np.ascontiguousarray(thr32, dtype=np.uint64)
         self.alias = np.ascontiguousarray(alias, dtype=np.int64)
         self.row = np.ascontiguousarray(row, dtype=np.uint64)
         self.col = np.ascontiguousarray(col, dtype=np.uint64)
         self.depth = np.ascontiguousarray(depth, dtype=np.uint64)
         self.n = int(self.thr32.shape[0])
+        self.mean_depth = mean_depth
 
     @classmethod
     def from_fragment_table(cls, table) -> "OracleTable":
         """From any object with .sampler.threshold/.alias and .row_bits/.col_bits/.depths."""
         thr32 = np.ceil(np.asarray(table.sampler.threshold) * 2.0**32).astype(np.uint64)
-        return cls(thr32, table.sampler.alias, table.row_bits, table.col_bits, table.depths)
+        return cls(thr32, table.sampler.alias, table.row_bits, table.col_bits, table.depths,
+                   float(table.mean_depth) if hasattr(table, "mean_depth") else None)
 
     def args(self):
         return (self.n, _p(self.thr32, _u64p), _p(self.alias, _i64p), _p(self.row, _u64p),
@@ -199,3 +207,79 @@ def ref_generate(table: OracleTable, k: int, m: int, seed: int, block_size: int 
         out[b * B: b * B + cnt] = e
         total += nf
     return out, total
+
+
+# ---------------------------------------------------------------- continuation / distinct tiles
+MAX_WINDOW = 16  # reference generator.py:_MAX_WINDOW (fixed-kernel eligibility, :296)
+
+
+def ref_stream_from(table: OracleTable, k: int, count: int, key0: int, key1: int, start: int,
+                    row_prefix: int = 0, col_prefix: int = 0):
+    """A fresh `_emit` reading the reference stream from word `start` -> (edges, nf)."""
+    out = np.zeros((count, 2), dtype=np.uint64)
+    nf = lib().oracle_ref_stream_from(*table.args(), k, count, key0 & M64, key1 & M64, start,
+                                      row_prefix, col_prefix, _p(out, _u64p))
+    return out, int(nf)
+
+
+def ref_depth_sum(table: OracleTable, key0: int, key1: int, start: int, count: int) -> int:
+    return int(lib().oracle_ref_depth_sum(*table.args(), key0 & M64, key1 & M64, start, count))
+
+
+def ref_emit_words(table: OracleTable, k: int, count: int, key0: int, key1: int,
+                   start: int) -> int:
+    """How many words the reference's `_emit(comp, k, count, gen)` draws (generator.py:293-298).
+
+    Fixed-depth tables inside the window: nsuper * gf (generator.py:175-181).
+    Otherwise `_emit_general`'s batch loop (generator.py:244-253):
+    want = int(short / mean_depth * 1.05) + 16 until the depths cover count*k.
+    """
+    if count == 0:
+        return 0
+    dmin, dmax = int(table.depth.min()), int(table.depth.max())
+    if dmin == dmax and (k - 1) // dmin + 2 <= MAX_WINDOW:
+        g = k * dmin // np.gcd(k, dmin)
+        ge, gf = g // k, g // dmin
+        return ((count + ge - 1) // ge) * gf
+    if table.mean_depth is None:
+        raise ValueError("table.mean_depth is needed to replay _emit_general's draw loop")
+    short = count * k
+    drawn = 0
+    while short > 0:
+        want = int(short / table.mean_depth * 1.05) + 16
+        short -= ref_depth_sum(table, key0, key1, start + drawn, want)
+        drawn += want
+    return drawn
+
+
+def ref_tile(table: OracleTable, k: int, t: int, row: int, col: int, count: int, seed: int,
+             distinct: bool = False):
+    """The reference's `_tile_result` (partition.py:140-163) -> (edges, samples).
+
+    distinct: dedup_local, then resample `count - len` edges from the same
+    Generator (continuing after every word the previous `_emit` drew) until
+    `count` distinct edges remain.
+    """
+    from .post import dedup_local
+
+    inner = k - t
+    if distinct and count > 4 ** inner:
+        raise ValueError(f"{count} distinct edges cannot fit {4 ** inner} cells")
+    if inner == 0:
+        e = np.empty((count, 2), dtype=np.uint64)
+        e[:, 0], e[:, 1] = row, col
+        return e, 0
+    key0, key1 = (seed ^ DOMAIN_TILE) & M64, (row << t) | col
+    edges, samples = ref_stream_from(table, inner, count, key0, key1, 0)
+    pos = ref_emit_words(table, inner, count, key0, key1, 0)
+    if distinct:
+        edges = dedup_local(edges)
+        while len(edges) < count:
+            need = count - len(edges)
+            more, extra = ref_stream_from(table, inner, need, key0, key1, pos)
+            pos += ref_emit_words(table, inner, need, key0, key1, pos)
+            samples += extra
+            edges = dedup_local(np.concatenate([edges, more]))
+    edges[:, 0] |= np.uint64(row << inner)
+    edges[:, 1] |= np.uint64(col << inner)
+    return edges, samples

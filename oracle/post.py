@@ -2,7 +2,7 @@
 
 numpy restatement of the reference's per-edge post-processing
 (pkg/src/rmatgen/postprocess.py): `to_undirected` (:26-35), `mirrored`
-(:38-43), the scramble key derivation (`make_scramble_key`, :61-79, built on
+(:38-43), `dedup_local` (:101-126), the scramble key derivation (`make_scramble_key`, :61-79, built on
 the splitmix64 finaliser `mix64`, _rng.py:41-50) and `scramble` (:82-93).
 Pinned against reference outputs in tests/golden/golden.json ("postprocess").
 """
@@ -60,3 +60,14 @@ def mirrored(edges: np.ndarray) -> np.ndarray:
     out[0::2] = edges
     out[1::2] = edges[:, ::-1]
     return out
+
+
+def dedup_local(edges: np.ndarray) -> np.ndarray:
+    """First occurrence of every (u, v), input order kept (postprocess.py:122-126)."""
+    if len(edges) == 0:
+        return edges.copy()
+    e = np.ascontiguousarray(edges, dtype=np.uint64)
+    pairs = e.view([("u", np.uint64), ("v", np.uint64)]).ravel()
+    _, first = np.unique(pairs, return_index=True)
+    first.sort()
+    return e[first]

@@ -155,14 +155,15 @@ static int next_word(word_src* src, uint64_t i, uint64_t* w) {
 
 /* generator.py:324-356: acc = acc << d | bits; cut the top k bits while >= k
  * are held and edges remain.  Returns nf, or -1 if an array source ran dry. */
-static int64_t emit_core(const oracle_table* t, uint32_t k, uint64_t count, word_src* src,
-                         uint64_t* edges, uint64_t row_prefix, uint64_t col_prefix) {
+static int64_t emit_core_at(const oracle_table* t, uint32_t k, uint64_t count, word_src* src,
+                            uint64_t start, uint64_t* edges, uint64_t row_prefix,
+                            uint64_t col_prefix) {
   u128 racc = 0, cacc = 0;
   uint32_t len = 0;
   uint64_t emitted = 0, used = 0, w;
   const u128 kmask = (((u128)1) << k) - 1;
   while (emitted < count) {
-    if (!next_word(src, used, &w)) return -1;
+    if (!next_word(src, start + used, &w)) return -1;
     ++used;
     uint64_t e = select_entry(t, w);
     uint32_t d = (uint32_t)t->depth[e];
@@ -181,6 +182,11 @@ static int64_t emit_core(const oracle_table* t, uint32_t k, uint64_t count, word
     }
   }
   return (int64_t)used;
+}
+
+static int64_t emit_core(const oracle_table* t, uint32_t k, uint64_t count, word_src* src,
+                         uint64_t* edges, uint64_t row_prefix, uint64_t col_prefix) {
+  return emit_core_at(t, k, count, src, 0, edges, row_prefix, col_prefix);
 }
 
 #define TABLE_ARGS uint64_t n, const uint64_t *thr32, const int64_t *alias, const uint64_t *row, \
@@ -216,4 +222,31 @@ int64_t oracle_ref_stream(TABLE_ARGS, uint32_t k, uint64_t count, uint64_t key0,
   src.kind = 2; src.key0 = key0; src.key1 = key1; src.cache_blk = UINT64_MAX;
   if (count == 0) return 0;
   return emit_core(&t, k, count, &src, edges, row_prefix, col_prefix);
+}
+
+/* The same stream read from word `start` on: a second `_emit` on a numpy
+ * Generator continues after the words the first one drew (partition.py:156-159). */
+int64_t oracle_ref_stream_from(TABLE_ARGS, uint32_t k, uint64_t count, uint64_t key0,
+                               uint64_t key1, uint64_t start, uint64_t row_prefix,
+                               uint64_t col_prefix, uint64_t* edges) {
+  TABLE_INIT;
+  word_src src = {0};
+  src.kind = 2; src.key0 = key0; src.key1 = key1; src.cache_blk = UINT64_MAX;
+  if (count == 0) return 0;
+  return emit_core_at(&t, k, count, &src, start, edges, row_prefix, col_prefix);
+}
+
+/* Sum of selected depths over words [start, start+count) of a reference stream
+ * (the `short -= depths[sel].sum()` bookkeeping of generator.py:244-253). */
+uint64_t oracle_ref_depth_sum(TABLE_ARGS, uint64_t key0, uint64_t key1, uint64_t start,
+                              uint64_t count) {
+  TABLE_INIT;
+  word_src src = {0};
+  src.kind = 2; src.key0 = key0; src.key1 = key1; src.cache_blk = UINT64_MAX;
+  uint64_t sum = 0, w;
+  for (uint64_t i = 0; i < count; ++i) {
+    next_word(&src, start + i, &w);
+    sum += t.depth[select_entry(&t, w)];
+  }
+  return sum;
 }

@@ -61,7 +61,9 @@ from .partition import (
     split_quadrant_counts,
 )
 from .postprocess import (
+    EdgeOutsideDeclaredTile,
     ScrambleKey,
+    dedup_local,
     make_scramble_key,
     mirrored,
     scramble,
@@ -84,5 +86,5 @@ __all__ = [
     "MAX_TILE_BITS", "CountOverflowsTile", "PartitionPlan", "TileCount", "default_plan",
     "generate_part", "generate_tile", "plan_tiles", "split_quadrant_counts",
     "ScrambleKey", "make_scramble_key", "mirrored", "scramble", "scramble_edges",
-    "to_undirected",
+    "to_undirected", "dedup_local", "EdgeOutsideDeclaredTile",
 ]

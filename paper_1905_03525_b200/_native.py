@@ -98,7 +98,22 @@ class RefArgs(ctypes.Structure):
                 ("edge_count", ctypes.c_uint64), ("first_block", ctypes.c_uint64),
                 ("n_blocks", ctypes.c_uint64), ("out", ctypes.c_void_p),
                 ("samples_per_block", ctypes.c_void_p), ("samples_total", ctypes.c_void_p),
-                ("row_prefix", ctypes.c_uint64), ("col_prefix", ctypes.c_uint64)]
+                ("row_prefix", ctypes.c_uint64), ("col_prefix", ctypes.c_uint64),
+                ("word_offset", ctypes.c_uint64)]
+
+
+class DedupArgs(ctypes.Structure):
+    _fields_ = [("flags", ctypes.c_uint32), ("width", ctypes.c_uint32), ("rows", ctypes.c_uint64),
+                ("in_", ctypes.c_void_p), ("out", ctypes.c_void_p),
+                ("index_base", ctypes.c_uint64), ("set", ctypes.c_void_p),
+                ("capacity", ctypes.c_uint64), ("scratch", ctypes.c_void_p),
+                ("kept", ctypes.c_void_p), ("status", ctypes.c_void_p),
+                ("row_lo", ctypes.c_uint64), ("row_hi", ctypes.c_uint64),
+                ("col_lo", ctypes.c_uint64), ("col_hi", ctypes.c_uint64)]
+
+
+DEDUP_RESET, DEDUP_CHECK_RANGE = 1, 2
+DEDUP_STATUS_RANGE, DEDUP_STATUS_FULL = 1, 2
 
 
 class PostArgs(ctypes.Structure):
@@ -115,8 +130,11 @@ KERNEL_NAMES = {1: "packed_smem", 2: "packed_global", 3: "generic"}
 
 #: symbols include/rmat_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
-           "rmat_replay_words", "rmat_generate_refstream", "rmat_postprocess", "rmat_strerror",
-           "rmat_abi_version")
+           "rmat_replay_words", "rmat_generate_refstream", "rmat_refstream_depth_sum",
+           "rmat_dedup_set_bytes", "rmat_dedup_scratch_bytes", "rmat_dedup", "rmat_postprocess",
+           "rmat_strerror", "rmat_abi_version")
+
+ABI_VERSION = 2
 
 
 @lru_cache(maxsize=1)
@@ -142,11 +160,19 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_uint64, ctypes.c_uint64, vp, vp]
     L.rmat_generate_refstream.argtypes = [ctypes.POINTER(RefArgs), vp]
     L.rmat_postprocess.argtypes = [ctypes.POINTER(PostArgs), ctypes.c_int, vp]
+    L.rmat_refstream_depth_sum.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                           ctypes.c_uint64, vp, vp]
+    L.rmat_dedup_set_bytes.argtypes = [ctypes.c_uint64]
+    L.rmat_dedup_set_bytes.restype = ctypes.c_uint64
+    L.rmat_dedup_scratch_bytes.argtypes = [ctypes.c_uint64]
+    L.rmat_dedup_scratch_bytes.restype = ctypes.c_uint64
+    L.rmat_dedup.argtypes = [ctypes.POINTER(DedupArgs), ctypes.c_int, vp]
     L.rmat_strerror.argtypes = [ctypes.c_int]
     L.rmat_strerror.restype = ctypes.c_char_p
     L.rmat_abi_version.restype = ctypes.c_int
     for f in ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
-              "rmat_replay_words", "rmat_generate_refstream", "rmat_postprocess"):
+              "rmat_replay_words", "rmat_generate_refstream", "rmat_postprocess",
+              "rmat_refstream_depth_sum", "rmat_dedup"):
         getattr(L, f).restype = ctypes.c_int
     return L
 

@@ -17,6 +17,7 @@
 #include "rmat_kernels.cuh"
 #include "rmat_post.cuh"
 #include "rmat_refstream.cuh"
+#include "rmat_dedup.cuh"
 
 struct rmat_table {
   int device;
@@ -468,6 +469,99 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
   }
   return rmat::launch_refstream(generic_view(t), t->dmax, *a,
                                 reinterpret_cast<cudaStream_t>(cuda_stream));
+}
+
+rmat_status rmat_refstream_depth_sum(const rmat_table* t, uint64_t key0, uint64_t key1,
+                                     uint64_t word_begin, uint64_t word_count, uint64_t* sum,
+                                     void* cuda_stream) {
+  if (!t || !sum) return RMAT_ERR_INVALID;
+  if (word_count == 0) return RMAT_OK;
+  if (word_begin + word_count < word_begin) return RMAT_ERR_INVALID;
+  DeviceGuard guard(t->device);
+  if (!guard.ok) return RMAT_ERR_DEVICE;
+  const uint64_t calls = (word_begin + word_count + 3) / 4 - word_begin / 4;
+  const unsigned blocks =
+      (unsigned)std::min<uint64_t>((calls + 255) / 256, (uint64_t)num_sms(t->device) * 8);
+  rmat::k_ref_depth_sum<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      generic_view(t), key0, key1, word_begin, word_begin + word_count,
+      reinterpret_cast<unsigned long long*>(sum));
+  return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+}
+
+uint64_t rmat_dedup_set_bytes(uint64_t capacity) { return capacity * 24; }
+
+uint64_t rmat_dedup_scratch_bytes(uint64_t rows) {
+  const uint64_t tiles = (rows + rmat::kDedupTile - 1) / rmat::kDedupTile;
+  return rows * 8 + tiles * 8;
+}
+
+rmat_status rmat_dedup(const rmat_dedup_args* a, int device, void* cuda_stream) {
+  if (!a || (a->width != 4 && a->width != 8) || (a->flags & ~3u)) return RMAT_ERR_INVALID;
+  if (!a->set || a->capacity < 2 || (a->capacity & (a->capacity - 1)) || !a->kept)
+    return RMAT_ERR_INVALID;
+  if ((reinterpret_cast<uintptr_t>(a->set) & 15) != 0) return RMAT_ERR_INVALID;
+  if (a->rows && (!a->in || !a->out || !a->scratch)) return RMAT_ERR_INVALID;
+  if ((a->flags & RMAT_DEDUP_CHECK_RANGE) && !a->status) return RMAT_ERR_INVALID;
+  if (a->index_base + a->rows < a->index_base || a->index_base + a->rows == ~0ull)
+    return RMAT_ERR_INVALID;
+  const uintptr_t ib = reinterpret_cast<uintptr_t>(a->in), ob = reinterpret_cast<uintptr_t>(a->out);
+  const uint64_t bytes = a->rows * 2 * a->width;
+  if (a->rows && ib < ob + bytes && ob < ib + bytes) return RMAT_ERR_INVALID;  // overlap
+  DeviceGuard guard(device);
+  if (!guard.ok) return RMAT_ERR_DEVICE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  rmat::DedupLaunch g{};
+  g.width = a->width;
+  g.check_range = (a->flags & RMAT_DEDUP_CHECK_RANGE) ? 1u : 0u;
+  g.rows = a->rows;
+  g.in = a->in;
+  g.out = a->out;
+  g.base = a->index_base;
+  g.keys = reinterpret_cast<ulonglong2*>(a->set);
+  g.first = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a->set) +
+                                                  a->capacity * 16);
+  g.mask = a->capacity - 1;
+  g.slot_of = reinterpret_cast<uint64_t*>(a->scratch);
+  g.ntiles = (a->rows + rmat::kDedupTile - 1) / rmat::kDedupTile;
+  g.tile_off = g.slot_of + a->rows;
+  g.kept = a->kept;
+  g.status = a->status;
+  g.row_lo = a->row_lo; g.row_hi = a->row_hi; g.col_lo = a->col_lo; g.col_hi = a->col_hi;
+  if (a->flags & RMAT_DEDUP_RESET) {
+    if (cudaMemsetAsync(a->set, 0xFF, rmat_dedup_set_bytes(a->capacity), st) != cudaSuccess)
+      return RMAT_ERR_CUDA;
+  }
+  if (a->rows == 0) {
+    return cudaMemsetAsync(a->kept, 0, 8, st) == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+  }
+  const unsigned ins_blocks =
+      (unsigned)std::min<uint64_t>((a->rows + 255) / 256, (uint64_t)num_sms(device) * 8);
+  rmat::k_dedup_insert<<<ins_blocks, 256, 0, st>>>(g);
+  for (uint64_t done = 0; done < g.ntiles;) {  // grid.x limit
+    const uint64_t n = std::min<uint64_t>(g.ntiles - done, 1u << 30);
+    rmat::DedupLaunch gg = g;
+    // tiles [done, done+n): shift the row window, keep priorities global
+    gg.in = reinterpret_cast<const char*>(g.in) + done * rmat::kDedupTile * 2 * g.width;
+    gg.slot_of = g.slot_of + done * rmat::kDedupTile;
+    gg.base = g.base + done * rmat::kDedupTile;
+    gg.rows = std::min<uint64_t>(g.rows - done * rmat::kDedupTile, n * rmat::kDedupTile);
+    gg.tile_off = g.tile_off + done;
+    rmat::k_dedup_count<<<(unsigned)n, rmat::kDedupThreads, 0, st>>>(gg);
+    done += n;
+  }
+  rmat::k_dedup_scan<<<1, rmat::kDedupThreads, 0, st>>>(g);
+  for (uint64_t done = 0; done < g.ntiles;) {
+    const uint64_t n = std::min<uint64_t>(g.ntiles - done, 1u << 30);
+    rmat::DedupLaunch gg = g;
+    gg.in = reinterpret_cast<const char*>(g.in) + done * rmat::kDedupTile * 2 * g.width;
+    gg.slot_of = g.slot_of + done * rmat::kDedupTile;
+    gg.base = g.base + done * rmat::kDedupTile;
+    gg.rows = std::min<uint64_t>(g.rows - done * rmat::kDedupTile, n * rmat::kDedupTile);
+    gg.tile_off = g.tile_off + done;
+    rmat::k_dedup_scatter<<<(unsigned)n, rmat::kDedupThreads, 0, st>>>(gg);
+    done += n;
+  }
+  return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
 }
 
 }  // extern "C"

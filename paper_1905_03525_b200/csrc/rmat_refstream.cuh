@@ -38,6 +38,7 @@ struct RefLaunch {
   uint64_t* samples_per_block;
   uint64_t* samples_total;
   uint64_t rpre, cpre;
+  uint64_t w0;    // first word of every block stream (continuation after an earlier _emit)
 };
 
 __device__ __forceinline__ uint64_t mad_wide_ref(uint32_t a, uint32_t b, uint32_t c) {
@@ -79,7 +80,8 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
   __syncthreads();
 
   uint64_t emitted = 0;  // edges of this block already written
-  uint64_t chunk_base = 0;  // sample index of this chunk's first fragment
+  // word index of this chunk's first fragment; words before w0 get depth 0
+  uint64_t chunk_base = g.w0 & ~3ull;
   uint64_t nf = 0;
   while (emitted < count) {
     // 1. draw + select 4 fragments per thread
@@ -93,7 +95,7 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
       const uint32_t hi = (uint32_t)(w >> 32);
       const uint32_t idx = pow2 ? (hi & (n - 1)) : (hi % n);
       const uint32_t e = ((uint32_t)w < __ldg(tab.T + idx)) ? idx : __ldg(tab.alias + idx);
-      dq[q] = __ldg(tab.depth + e);
+      dq[q] = chunk_base + 4 * tid + q < g.w0 ? 0u : __ldg(tab.depth + e);
       s_r[4 * tid + q] = __ldg(tab.row + e);
       s_c[4 * tid + q] = __ldg(tab.col + e);
       dsum += dq[q];
@@ -177,9 +179,9 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
             const int mid = (l + h) >> 1;
             if (s_end[mid] >= used) h = mid; else l = mid + 1;
           }
-          nf = chunk_base + l + 1;
+          nf = chunk_base + l + 1 - g.w0;
         } else {
-          nf = chunk_base;  // finished inside the carry: no fragment of this chunk used
+          nf = chunk_base - g.w0;  // finished inside the carry: no fragment of this chunk used
         }
       } else {
         // keep bits [used, ltot)
@@ -269,7 +271,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
     char* const outb = reinterpret_cast<char*>(g.out) + bi * g.B * (OUT64 ? 16 : 8);
     if (tid == 0) { s_carry_r = 0; s_carry_c = 0; s_carry_len = 0; }
     __syncthreads();
-    uint64_t emitted = 0, chunk_base = 0;
+    uint64_t emitted = 0, chunk_base = g.w0 & ~3ull;  // words before w0 get depth 0
     while (emitted < count) {
       // 1. draw + select 4 fragments per thread
       const uint64_t call = chunk_base / 4 + tid;  // numpy counter = call + 1
@@ -287,7 +289,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
         if ((uint32_t)sum <= fm) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
         const uint32_t sel = ge ? 0x4432u : 0x4410u;
         const uint32_t r = prmt_ref(aw.x, sel), c = prmt_ref(aw.y, sel);
-        dq[q] = prmt_ref(bw, 0x4440u + ge);
+        dq[q] = chunk_base + 4 * tid + q < g.w0 ? 0u : prmt_ref(bw, 0x4440u + ge);
         s_rc[4 * tid + q] = r | (c << 16);
         dsum += dq[q];
       }
@@ -378,7 +380,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
           }
           // nf (generator.py:255-257): one past the fragment holding the last
           // edge's last bit
-          if (final_chunk && j + 1 == avail) s_nf = chunk_base + sidx;
+          if (final_chunk && j + 1 == avail) s_nf = chunk_base + sidx - g.w0;
           const uint64_t row = emitted + j;
           if (OUT64) {
             reinterpret_cast<ulonglong2*>(outb)[row] =
@@ -402,6 +404,36 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
   }
 }
 
+// Sum of the selected fragments' depths over words [w_begin, w_begin + w_count)
+// of one reference stream: the draw-loop bookkeeping of the reference's
+// `_emit_general` (generator.py:244-253: `short -= depths[sel].sum()`), which
+// fixes how far the numpy Generator advanced -- the start of the next `_emit`
+// on the same stream (partition.py:156-159, distinct resampling).
+__global__ void __launch_bounds__(256)
+k_ref_depth_sum(const GenericTab tab, uint64_t key0, uint64_t key1, uint64_t w_begin,
+                uint64_t w_end, unsigned long long* out) {
+  const uint32_t n = tab.n;
+  const bool pow2 = (n & (n - 1)) == 0;
+  uint64_t acc = 0;
+  const uint64_t c_lo = w_begin / 4, c_hi = (w_end + 3) / 4;
+  for (uint64_t c = c_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < c_hi;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const u64x4 w4 = philox4x64_10(c + 1, c + 1 == 0 ? 1 : 0, 0, 0, key0, key1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = 4 * c + q;
+      const uint64_t w = q == 0 ? w4.x : q == 1 ? w4.y : q == 2 ? w4.z : w4.w;
+      const uint32_t hi = (uint32_t)(w >> 32);
+      const uint32_t idx = pow2 ? (hi & (n - 1)) : (hi % n);
+      const uint32_t e = ((uint32_t)w < __ldg(tab.T + idx)) ? idx : __ldg(tab.alias + idx);
+      if (i >= w_begin && i < w_end) acc += __ldg(tab.depth + e);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+
 inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
                                     const rmat_refstream_args& a, cudaStream_t st,
                                     const PackedTab* packed = nullptr, int sms = 148,
@@ -419,6 +451,7 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
   g.samples_total = a.samples_total;
   g.rpre = a.row_prefix;
   g.cpre = a.col_prefix;
+  g.w0 = a.word_offset;
   const uint64_t nb = a.n_blocks;
   if (packed) {
     // shared memory: buckets + chunk buffers (s_rc, s_end)

@@ -20,7 +20,7 @@ from .alias import threshold_to_u32
 from .table import FragmentTable
 
 __all__ = ["DeviceTable", "device_table", "launch_generate", "launch_refstream",
-           "replay_words", "require_cuda", "Segment"]
+           "replay_words", "require_cuda", "Segment", "refstream_depth_sum", "DedupSet"]
 
 Segment = N.Segment
 
@@ -134,7 +134,7 @@ def launch_generate(dt: DeviceTable, k: int, seed: int, domain: int, edges_per_s
 def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size: int,
                      edge_count: int, first_block: int, n_blocks: int, out, *,
                      samples_per_block=None, samples_total=None, row_prefix: int = 0,
-                     col_prefix: int = 0) -> None:
+                     col_prefix: int = 0, word_offset: int = 0) -> None:
     import torch
 
     assert out.device == dt.device and out.is_contiguous()
@@ -145,7 +145,7 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
         samples_per_block=(samples_per_block.data_ptr()
                            if samples_per_block is not None else None),
         samples_total=samples_total.data_ptr() if samples_total is not None else None,
-        row_prefix=row_prefix, col_prefix=col_prefix)
+        row_prefix=row_prefix, col_prefix=col_prefix, word_offset=word_offset)
     with torch.cuda.device(dt.device):
         N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), _stream_ptr(dt.device)),
                 "rmat_generate_refstream")
@@ -161,3 +161,81 @@ def replay_words(dt: DeviceTable, seed: int, domain: int, sid: int, count: int, 
                                           count, out.data_ptr() if count else None,
                                           _stream_ptr(dt.device)), "rmat_replay_words")
     return out
+
+
+def refstream_depth_sum(dt: DeviceTable, key0: int, key1: int, word_begin: int, word_count: int,
+                        out=None):
+    """rmat_refstream_depth_sum into a device int64 scalar tensor (accumulates into `out`)."""
+    import torch
+
+    if out is None:
+        out = torch.zeros(1, dtype=torch.int64, device=dt.device)
+    with torch.cuda.device(dt.device):
+        N.check(N.lib().rmat_refstream_depth_sum(dt.handle, key0 & (2**64 - 1), key1 & (2**64 - 1),
+                                                 word_begin, word_count, out.data_ptr(),
+                                                 _stream_ptr(dt.device)),
+                "rmat_refstream_depth_sum")
+    return out
+
+
+class DedupSet:
+    """Device hash set for first-occurrence dedup (rmat_dedup); `capacity` >= 2x the keys held."""
+
+    def __init__(self, keys: int, device=None):
+        import torch
+
+        self.device = require_cuda(device)
+        cap = 2
+        while cap < 2 * max(int(keys), 1):
+            cap <<= 1
+        self.capacity = cap
+        nbytes = int(N.lib().rmat_dedup_set_bytes(cap))
+        self._set = torch.empty(nbytes // 8, dtype=torch.int64, device=self.device)
+        self._kept = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._scratch = None
+        self.next_index = 0
+        self._fresh = True
+
+    def reset(self) -> None:
+        self.next_index = 0
+        self._fresh = True
+
+    def append(self, edges, out, *, check_range=None) -> int:
+        """Write the rows of `edges` (device (rows, 2)) unseen so far to `out`; returns their count.
+
+        check_range: ((row_lo, row_hi), (col_lo, col_hi)) half-open; rows outside raise
+        EdgeOutsideDeclaredTile after the call.
+        """
+        import torch
+
+        rows = edges.shape[0]
+        need = int(N.lib().rmat_dedup_scratch_bytes(rows))
+        if self._scratch is None or self._scratch.numel() * 8 < need:
+            self._scratch = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)
+        flags = N.DEDUP_RESET if self._fresh else 0
+        rl = rh = cl = ch = 0
+        if check_range is not None:
+            flags |= N.DEDUP_CHECK_RANGE
+            (rl, rh), (cl, ch) = check_range
+        self._status.zero_()
+        args = N.DedupArgs(flags=flags, width=edges.element_size(), rows=rows,
+                           in_=edges.data_ptr() if rows else None,
+                           out=out.data_ptr() if rows else None, index_base=self.next_index,
+                           set=self._set.data_ptr(), capacity=self.capacity,
+                           scratch=self._scratch.data_ptr(), kept=self._kept.data_ptr(),
+                           status=self._status.data_ptr(), row_lo=rl, row_hi=rh, col_lo=cl,
+                           col_hi=ch)
+        with torch.cuda.device(self.device):
+            N.check(N.lib().rmat_dedup(ctypes.byref(args), self.device.index,
+                                       _stream_ptr(self.device)), "rmat_dedup")
+        self._fresh = False
+        self.next_index += rows
+        kept = int(self._kept.item())
+        status = int(self._status.item())
+        if status & N.DEDUP_STATUS_FULL:
+            raise RuntimeError("dedup set overflowed its capacity")
+        if status & N.DEDUP_STATUS_RANGE:
+            from .postprocess import EdgeOutsideDeclaredTile
+            raise EdgeOutsideDeclaredTile("edge outside the declared tile ranges")
+        return kept

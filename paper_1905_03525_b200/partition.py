@@ -19,7 +19,19 @@ reference partition.py:140-163).  Tile streams:
   [seed ^ DOMAIN_TILE, payload] exactly as the reference, so
   `generate_part(..., rng="reference")` equals the reference bytes.
 
-`distinct=True` (per-tile dedup + resampling) is out of scope.
+`distinct=True` (reference partition.py:144-160): the tile's edges are
+deduplicated on the device (first occurrence kept, order preserved:
+`rmat_dedup`, an incremental hash set) and `count - len` more are drawn until
+`count` distinct edges remain:
+
+* reference mode continues the tile's numpy Generator exactly where the
+  previous `_emit` left it -- after every word it DREW, not just the nf it
+  used: nsuper * gf words for fixed-depth tables (generator.py:175-181), the
+  batch loop `want = int(short / mean_depth * 1.05) + 16` otherwise
+  (generator.py:244-253), replayed here with device depth sums -- so the
+  bytes equal the reference's `generate_tile(..., distinct=True)`;
+* fast mode draws resampling round r >= 1 from the tile's stream ids
+  r * 2^40 + j (j = 0, 1, ... per E edges), disjoint from round 0's ids.
 """
 
 from __future__ import annotations
@@ -29,16 +41,20 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .device import device_table, launch_generate, launch_refstream, require_cuda
+from .device import (DedupSet, device_table, launch_generate, launch_refstream,
+                     refstream_depth_sum, require_cuda)
 from .generator import DOMAIN_NODE, DOMAIN_TILE, FAST_STREAM_EDGES, RNG_MODES, edge_dtype
 from .params import RmatParams, check_k
 from .table import FragmentTable
 
 __all__ = ["MAX_TILE_BITS", "CountOverflowsTile", "TileCount", "PartitionPlan", "default_plan",
            "split_quadrant_counts", "plan_tiles", "generate_tile", "generate_part",
-           "tile_key", "part_segments"]
+           "tile_key", "part_segments", "generate_part_device", "emit_words_drawn",
+           "RESAMPLE_SID_SHIFT"]
 
 MAX_TILE_BITS = 31
+MAX_WINDOW = 16  # reference generator.py:35 (fixed-kernel eligibility, :296)
+RESAMPLE_SID_SHIFT = 40  # fast mode: resampling round r uses stream ids r << 40 | j
 _M64 = (1 << 64) - 1
 
 
@@ -162,25 +178,86 @@ def part_segments(tiles, k: int, t: int, edges_per_stream: int):
     return segs, row
 
 
-def _check_distinct(distinct: bool) -> None:
-    if distinct:
-        raise NotImplementedError("distinct-edge tiles are not implemented on the GPU path "
-                                  "(SURVEY.md §8 f2)")
+def emit_words_drawn(table: FragmentTable, dt, k: int, count: int, key0: int, key1: int,
+                     start: int) -> int:
+    """Words the reference's `_emit(comp, k, count, gen)` draws from `gen` (generator.py:293-298).
+
+    Fixed-depth tables inside the window draw nsuper * gf words
+    (generator.py:175-181); every other table runs `_emit_general`'s batch loop
+    (generator.py:244-253), whose depth sums come from the device.
+    """
+    if count == 0:
+        return 0
+    dmin, dmax = int(table.depths.min()), int(table.depths.max())
+    if dmin == dmax and (k - 1) // dmin + 2 <= MAX_WINDOW:
+        g = k * dmin // np.gcd(k, dmin)
+        ge, gf = g // k, g // dmin
+        return int(((count + ge - 1) // ge) * gf)
+    short = count * k
+    drawn = 0
+    while short > 0:
+        want = int(short / table.mean_depth * 1.05) + 16
+        short -= int(refstream_depth_sum(dt, key0, key1, start + drawn, want).item())
+        drawn += want
+    return drawn
+
+
+def _emit_tile(dt, inner: int, seed: int, rng: str, row: int, col: int, t: int, count: int, out,
+               samples, *, round_: int = 0, word_offset: int = 0) -> None:
+    payload = (row << t) | col
+    rp, cp = row << inner, col << inner
+    if rng == "reference":
+        launch_refstream(dt, inner, seed, DOMAIN_TILE, count, (payload + 1) * count, payload, 1,
+                         out, samples_total=samples, row_prefix=rp, col_prefix=cp,
+                         word_offset=word_offset)
+    else:
+        launch_generate(dt, inner, seed, DOMAIN_TILE, FAST_STREAM_EDGES,
+                        [(round_ << RESAMPLE_SID_SHIFT, count, 0, rp, cp, tile_key(payload))], out,
+                        samples_total=samples)
+
+
+def _distinct_tile(dt, table: FragmentTable, k: int, t: int, row: int, col: int, count: int,
+                   seed: int, rng: str, out, samples, dset: DedupSet, tmp) -> None:
+    """`count` distinct edges of one tile into `out` (reference partition.py:144-162)."""
+    inner = k - t
+    payload = (row << t) | col
+    key0 = (seed ^ DOMAIN_TILE) & _M64
+    dset.reset()
+    have, pos, round_ = 0, 0, 0
+    while have < count:
+        need = count - have
+        buf = tmp[:need]
+        _emit_tile(dt, inner, seed, rng, row, col, t, need, buf, samples, round_=round_,
+                   word_offset=pos)
+        if rng == "reference":
+            pos += emit_words_drawn(table, dt, inner, need, key0, payload, pos)
+        have += dset.append(buf, out[have:have + need])
+        round_ += 1
+
+
+def _check_distinct_counts(tiles, k: int, t: int) -> None:
+    inner = k - t
+    for tc in tiles:
+        if tc.count > 4 ** inner:
+            raise CountOverflowsTile(f"{tc.count} distinct edges cannot fit {4 ** inner} cells")
 
 
 def generate_part_device(plan: PartitionPlan, params: RmatParams, table: FragmentTable,
                          part: int = 0, rng: str = "philox4x32", device=None,
-                         edges_per_stream: int = FAST_STREAM_EDGES, count_samples: bool = False):
+                         edges_per_stream: int = FAST_STREAM_EDGES, count_samples: bool = False,
+                         distinct: bool = False):
     """Edges of one part in HBM: (tensor (rows, 2), tiles, samples or None)."""
     import torch
 
     check_k(plan.k)
     if rng not in RNG_MODES:
         raise ValueError(f"rng must be one of {RNG_MODES}, got {rng!r}")
-    dev = require_cuda(device)
     tiles = plan_tiles(plan, params, part)
     k, t = plan.k, plan.t
     inner = k - t
+    if distinct:
+        _check_distinct_counts(tiles, k, t)
+    dev = require_cuda(device)
     rows = sum(tc.count for tc in tiles)
     out = torch.empty((rows, 2), dtype=edge_dtype(k), device=dev)
     samples = torch.zeros(1, dtype=torch.int64, device=dev) if count_samples else None
@@ -197,7 +274,17 @@ def generate_part_device(plan: PartitionPlan, params: RmatParams, table: Fragmen
             r += tc.count
         return out, tiles, samples
     dt = device_table(table, dev)
-    if rng == "reference":
+    if distinct:
+        biggest = max(tc.count for tc in tiles)
+        dset = DedupSet(biggest, dev)
+        tmp = torch.empty((biggest, 2), dtype=out.dtype, device=dev)
+        r = 0
+        for tc in tiles:
+            if tc.count:
+                _distinct_tile(dt, table, k, t, tc.tile_row, tc.tile_col, tc.count, plan.seed,
+                               rng, out[r:r + tc.count], samples, dset, tmp)
+            r += tc.count
+    elif rng == "reference":
         r = 0
         for tc in tiles:
             if tc.count:
@@ -224,9 +311,8 @@ def _host_u64(tensor) -> np.ndarray:
 def generate_part(plan: PartitionPlan, params: RmatParams, table: FragmentTable, part: int = 0,
                   distinct: bool = False, rng: str = "philox4x32", device=None):
     """All edges of one part -> (host (rows, 2) uint64, tiles, samples) (reference partition.py:198-222)."""
-    _check_distinct(distinct)
     out, tiles, samples = generate_part_device(plan, params, table, part, rng=rng, device=device,
-                                               count_samples=True)
+                                               count_samples=True, distinct=distinct)
     return _host_u64(out), tiles, int(samples.item())
 
 
@@ -234,7 +320,6 @@ def generate_tile(tile, count: int, params: RmatParams, table: FragmentTable, k:
                   seed: int, distinct: bool = False, rng: str = "philox4x32",
                   device=None) -> np.ndarray:
     """`count` edges inside one tile (reference partition.py:166-195)."""
-    _check_distinct(distinct)
     row, col = (tile.tile_row, tile.tile_col) if isinstance(tile, TileCount) else tile
     if not 0 <= t <= min(k, MAX_TILE_BITS):
         raise ValueError(f"t must be in [0, min(k, {MAX_TILE_BITS})], got {t}")
@@ -242,25 +327,27 @@ def generate_tile(tile, count: int, params: RmatParams, table: FragmentTable, k:
         raise ValueError(f"tile ({row}, {col}) outside the 2^{t} grid")
     if count < 0:
         raise ValueError(f"count must be >= 0, got {count}")
+    if rng not in RNG_MODES:
+        raise ValueError(f"rng must be one of {RNG_MODES}, got {rng!r}")
+    check_k(k)
+    inner = k - t
+    if distinct and count > 4 ** inner:
+        raise CountOverflowsTile(f"{count} distinct edges cannot fit {4 ** inner} cells")
     import torch
 
-    check_k(k)
     dev = require_cuda(device)
     out = torch.empty((count, 2), dtype=edge_dtype(k), device=dev)
     if count == 0:
         return np.empty((0, 2), dtype=np.uint64)
-    inner = k - t
     if inner == 0:
         h = np.empty((count, 2), dtype=np.uint64)
         h[:, 0] = row
         h[:, 1] = col
         return h
     dt = device_table(table, dev)
-    payload = (row << t) | col
-    if rng == "reference":
-        launch_refstream(dt, inner, seed, DOMAIN_TILE, count, (payload + 1) * count, payload, 1,
-                         out, row_prefix=row << inner, col_prefix=col << inner)
+    if distinct:
+        _distinct_tile(dt, table, k, t, row, col, count, seed, rng, out, None,
+                       DedupSet(count, dev), torch.empty_like(out))
     else:
-        segs, _ = part_segments([TileCount(row, col, count)], k, t, FAST_STREAM_EDGES)
-        launch_generate(dt, inner, seed, DOMAIN_TILE, FAST_STREAM_EDGES, segs, out)
+        _emit_tile(dt, inner, seed, rng, row, col, t, count, out, None)
     return _host_u64(out)

@@ -8,9 +8,13 @@ reference's pkg/src/rmatgen/postprocess.py:
   [0, 2^k) (postprocess.py:46-98), round keys derived on the host with the
   splitmix64 finaliser exactly as the reference (_rng.py:41-50).
 
-Edge arrays may be device tensors (processed in HBM by `rmat_postprocess`)
-or host numpy arrays (copied through the GPU; same results).  Scalars go
-through the host formula.  `dedup_local` is not provided (§8 f2).
+* `dedup_local(edges, row_range, col_range)` -- first occurrence of every
+  edge, order kept, optional declared-range check (postprocess.py:101-126),
+  on the device hash set of `rmat_dedup` (§8 f2).
+
+Edge arrays may be device tensors (processed in HBM by `rmat_postprocess` /
+`rmat_dedup`) or host numpy arrays (copied through the GPU; same results).
+Scalars go through the host formula.
 """
 
 from __future__ import annotations
@@ -24,10 +28,14 @@ from . import _native as N
 from .device import require_cuda
 
 __all__ = ["ScrambleKey", "make_scramble_key", "scramble", "scramble_edges", "to_undirected",
-           "mirrored", "postprocess_device", "mix64"]
+           "mirrored", "postprocess_device", "mix64", "dedup_local", "EdgeOutsideDeclaredTile"]
 
 _M64 = (1 << 64) - 1
 _GOLDEN = 0x9E3779B97F4A7C15
+
+
+class EdgeOutsideDeclaredTile(ValueError):
+    """dedup_local found an edge outside its declared row/column range (postprocess.py:22)."""
 
 
 def mix64(x: int) -> int:
@@ -165,3 +173,46 @@ def scramble_edges(edges, key: ScrambleKey):
             return edges.copy()
         return _host_roundtrip(edges, key.k, key=key)
     return postprocess_device(edges.clone(), k=key.k, key=key)
+
+
+def dedup_local(edges, row_range: tuple[int, int] | None = None,
+                col_range: tuple[int, int] | None = None):
+    """Drop duplicate edges, keeping first occurrences in order (reference postprocess.py:101-126).
+
+    Host numpy (m, 2) uint64 arrays are range-checked on the host (as the
+    reference) and deduplicated on the GPU; device tensors stay in HBM (the
+    range check runs inside the dedup kernel).  Returns the same kind of array.
+    """
+    import torch
+
+    from .device import DedupSet
+
+    if isinstance(edges, np.ndarray):
+        if row_range is not None and len(edges):
+            lo, hi = row_range
+            if int(edges[:, 0].min()) < lo or int(edges[:, 0].max()) >= hi:
+                raise EdgeOutsideDeclaredTile(f"row outside [{lo}, {hi})")
+        if col_range is not None and len(edges):
+            lo, hi = col_range
+            if int(edges[:, 1].min()) < lo or int(edges[:, 1].max()) >= hi:
+                raise EdgeOutsideDeclaredTile(f"col outside [{lo}, {hi})")
+        if len(edges) == 0:
+            return edges.copy()
+        dev = require_cuda()
+        arr = np.ascontiguousarray(edges, dtype=np.uint64)
+        t = torch.from_numpy(arr.view(np.int64)).to(dev)
+        out = torch.empty_like(t)
+        kept = DedupSet(len(arr), dev).append(t, out)
+        return out[:kept].cpu().numpy().view(np.uint64)
+    if edges.device.type != "cuda" or edges.dim() != 2 or edges.shape[1] != 2:
+        raise ValueError("edges must be a (rows, 2) CUDA tensor or a host numpy array")
+    edges = edges.contiguous()
+    if edges.shape[0] == 0:
+        return edges.clone()
+    rng = None
+    if row_range is not None or col_range is not None:
+        rng = (tuple(row_range) if row_range is not None else (0, _M64),
+               tuple(col_range) if col_range is not None else (0, _M64))
+    out = torch.empty_like(edges)
+    kept = DedupSet(edges.shape[0], edges.device).append(edges, out, check_range=rng)
+    return out[:kept]

@@ -193,6 +193,49 @@ def main() -> None:
     post["mirrored"] = {"input_seed": 5, "n": 5000, "bits": 20, "out": sha(mirrored(e))}
     out["postprocess"] = post
 
+    # ---- f2: where a second _emit on the same Generator starts (the stream
+    # position after `_emit` drew its words), distinct tiles, dedup_local
+    from rmatgen._rng import DOMAIN_TILE
+    from rmatgen.partition import _tile_result
+    from rmatgen.postprocess import dedup_local
+    cont = []
+    for tag, k, counts, key1 in (("g500:v1024", 6, (3000, 1200, 7), 9),
+                                 ("g500:f2", 8, (20000, 333, 1), 1),
+                                 ("less:v16384", 12, (200000, 17), 6),
+                                 ("g500:f4", 62, (50, 3), 2),
+                                 ("g500:v253", 3, (64, 9, 2), 1)):
+        comp = _compile(built[tag])
+        gen = keyed_stream(3, DOMAIN_TILE, key1)
+        rec = {"table": tag, "k": k, "key0": (3 ^ DOMAIN_TILE), "key1": key1, "emits": []}
+        for cnt in counts:
+            e, nf = _emit(comp, k, cnt, gen)
+            # the next word the Generator would hand out, i.e. word[position]
+            st = gen.bit_generator.state
+            nxt = int(gen.bit_generator.random_raw(1)[0])
+            gen.bit_generator.state = st
+            rec["emits"].append({"count": cnt, "nf": int(nf), "edges": sha(e), "next_word": nxt})
+        cont.append(rec)
+    out["continuation"] = cont
+    dist = []
+    for (tag, quads, k, t, r, c, cnt, seed) in (
+            ("g500:v1024", G500, 8, 2, 1, 2, 3000, 7), ("g500:f2", G500, 9, 1, 0, 0, 20000, 3),
+            ("less:v16384", LESS, 14, 2, 0, 0, 200000, 1), ("g500:v253", G500, 4, 1, 1, 1, 64, 5),
+            ("g500:v1024", G500, 36, 3, 2, 5, 1000, 1), ("g500:f4", G500, 5, 5, 3, 9, 1, 2)):
+        pp = rmatgen.validate(*quads, k)
+        e, samples = _tile_result(_compile(built[tag]), r, c, cnt, k, t, seed, True)
+        assert len(np.unique(e, axis=0)) == cnt
+        dist.append({"table": tag, "k": k, "t": t, "tile": [r, c], "count": cnt, "seed": seed,
+                     "samples": int(samples), "edges": sha(e)})
+    out["distinct_tiles"] = dist
+    rng = np.random.default_rng(11)
+    dd = []
+    for n, bits in ((5000, 6), (3000, 40), (1, 3), (20000, 9)):
+        e = rng.integers(0, 1 << bits, size=(n, 2), dtype=np.uint64)
+        d = dedup_local(e)
+        dd.append({"input_seed": 11, "n": n, "bits": bits, "input": sha(e), "rows": int(len(d)),
+                   "out": sha(d)})
+    out["dedup_local"] = dd
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", os.path.join(HERE, "golden.json"))

@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "rmat_b200.h")
 
 def declared_functions():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:rmat_status|const char\*|int)\s+(rmat_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:rmat_status|const char\*|int|uint64_t)\s+(rmat_\w+)\(", src, re.M)))
 
 
 def test_header_declares_the_exports():
@@ -36,7 +36,11 @@ def test_library_builds_and_exports_every_symbol():
 
 def test_pure_host_entry_points():
     L = N.lib()
-    assert L.rmat_abi_version() == 1
+    assert L.rmat_abi_version() == N.ABI_VERSION == 2
+    # workspace sizing of the dedup set / scratch (pure host arithmetic)
+    assert L.rmat_dedup_set_bytes(1 << 20) == 24 << 20
+    assert L.rmat_dedup_scratch_bytes(4096) == 4096 * 8 + 8
+    assert L.rmat_dedup_scratch_bytes(0) == 0
     assert L.rmat_strerror(0) == b"ok"
     assert L.rmat_strerror(2) == b"inconsistent fragment table"
     # invalid arguments are rejected without touching a device
@@ -44,6 +48,16 @@ def test_pure_host_entry_points():
     assert L.rmat_generate(None, None) == 1
     assert L.rmat_generate_refstream(None, None) == 1
     assert L.rmat_table_get_info(None, None) == 1
+    assert L.rmat_refstream_depth_sum(None, 0, 0, 0, 1, None, None) == 1
+    assert L.rmat_dedup(None, 0, None) == 1
+    # argument validation happens before any CUDA call
+    a = N.DedupArgs(width=4, rows=0, set=64, capacity=3, kept=64)  # capacity not a power of 2
+    assert L.rmat_dedup(ctypes.byref(a), 0, None) == 1
+    a = N.DedupArgs(width=2, rows=0, set=64, capacity=4, kept=64)  # bad width
+    assert L.rmat_dedup(ctypes.byref(a), 0, None) == 1
+    a = N.DedupArgs(width=8, rows=10, in_=4096, out=4096 + 16, set=64, capacity=4, scratch=64,
+                    kept=64)  # overlapping in/out
+    assert L.rmat_dedup(ctypes.byref(a), 0, None) == 1
 
 
 def test_struct_layouts_match_header(tmp_path):
