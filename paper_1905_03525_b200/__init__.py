@@ -54,6 +54,7 @@ from .partition import (
     CountOverflowsTile,
     PartitionPlan,
     TileCount,
+    balanced_tiles,
     default_plan,
     generate_part,
     generate_tile,
@@ -84,7 +85,7 @@ __all__ = [
     "SizeLimitTooSmall", "TableStats", "build_fixed_table", "build_variable_table",
     "table_stats", "NativeError", "NativeUnavailable", "__version__",
     "MAX_TILE_BITS", "CountOverflowsTile", "PartitionPlan", "TileCount", "default_plan",
-    "generate_part", "generate_tile", "plan_tiles", "split_quadrant_counts",
+    "generate_part", "generate_tile", "plan_tiles", "split_quadrant_counts", "balanced_tiles",
     "ScrambleKey", "make_scramble_key", "mirrored", "scramble", "scramble_edges",
     "to_undirected", "dedup_local", "EdgeOutsideDeclaredTile",
 ]

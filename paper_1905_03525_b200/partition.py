@@ -50,7 +50,7 @@ from .table import FragmentTable
 __all__ = ["MAX_TILE_BITS", "CountOverflowsTile", "TileCount", "PartitionPlan", "default_plan",
            "split_quadrant_counts", "plan_tiles", "generate_tile", "generate_part",
            "tile_key", "part_segments", "generate_part_device", "emit_words_drawn",
-           "RESAMPLE_SID_SHIFT"]
+           "RESAMPLE_SID_SHIFT", "balanced_tiles"]
 
 MAX_TILE_BITS = 31
 MAX_WINDOW = 16  # reference generator.py:35 (fixed-kernel eligibility, :296)
@@ -159,6 +159,36 @@ def plan_tiles(plan: PartitionPlan, params: RmatParams, part: int = 0) -> list[T
     return tiles
 
 
+def balanced_tiles(plan: PartitionPlan, params: RmatParams, parts: int) -> list[list[TileCount]]:
+    """Count-balanced tile ownership (NOT the reference's contiguous rows).
+
+    The reference deals contiguous tile rows to parts (partition.py:71-83), so
+    a skewed R-MAT leaves part 0 with the heaviest rows (C4: max/mean 2.41).
+    Here every tile of the whole 2^t x 2^t grid (counts from the same seeded
+    splits, `plan_tiles`) goes to the currently lightest part, heaviest tile
+    first (LPT; ties by Z-order index, then part index), and each part emits
+    its tiles in Z-order.  Deterministic from (plan, params, parts): every
+    rank derives the same assignment without communicating.  The union of the
+    parts' edges is the same multiset as the contiguous-row plan's with the
+    same t; only which GPU produces which tile changes.
+    """
+    import heapq
+
+    if parts < 1:
+        raise ValueError(f"parts must be >= 1, got {parts}")
+    whole = PartitionPlan(k=plan.k, t=plan.t, m=plan.m, seed=plan.seed,
+                          owner_rows=((0, 1 << plan.t),))
+    tiles = plan_tiles(whole, params, 0)
+    order = sorted(range(len(tiles)), key=lambda i: (-tiles[i].count, i))
+    heap = [(0, p) for p in range(parts)]
+    owned: list[list[int]] = [[] for _ in range(parts)]
+    for i in order:
+        load, p = heapq.heappop(heap)
+        owned[p].append(i)
+        heapq.heappush(heap, (load + tiles[i].count, p))
+    return [[tiles[i] for i in sorted(ix)] for ix in owned]
+
+
 def tile_key(payload: int) -> int:
     """Key tweak of a tile's fast-mode streams: an odd-multiplier bijection of the payload."""
     return (payload * 0x9E3779B97F4A7C15) & _M64
@@ -245,14 +275,19 @@ def _check_distinct_counts(tiles, k: int, t: int) -> None:
 def generate_part_device(plan: PartitionPlan, params: RmatParams, table: FragmentTable,
                          part: int = 0, rng: str = "philox4x32", device=None,
                          edges_per_stream: int = FAST_STREAM_EDGES, count_samples: bool = False,
-                         distinct: bool = False):
-    """Edges of one part in HBM: (tensor (rows, 2), tiles, samples or None)."""
+                         distinct: bool = False, tiles=None):
+    """Edges of one part in HBM: (tensor (rows, 2), tiles, samples or None).
+
+    tiles: an explicit tile list for this part (e.g. `balanced_tiles(...)[part]`)
+    instead of the plan's contiguous rows.
+    """
     import torch
 
     check_k(plan.k)
     if rng not in RNG_MODES:
         raise ValueError(f"rng must be one of {RNG_MODES}, got {rng!r}")
-    tiles = plan_tiles(plan, params, part)
+    if tiles is None:
+        tiles = plan_tiles(plan, params, part)
     k, t = plan.k, plan.t
     inner = k - t
     if distinct:
@@ -309,10 +344,10 @@ def _host_u64(tensor) -> np.ndarray:
 
 
 def generate_part(plan: PartitionPlan, params: RmatParams, table: FragmentTable, part: int = 0,
-                  distinct: bool = False, rng: str = "philox4x32", device=None):
+                  distinct: bool = False, rng: str = "philox4x32", device=None, tiles=None):
     """All edges of one part -> (host (rows, 2) uint64, tiles, samples) (reference partition.py:198-222)."""
     out, tiles, samples = generate_part_device(plan, params, table, part, rng=rng, device=device,
-                                               count_samples=True, distinct=distinct)
+                                               count_samples=True, distinct=distinct, tiles=tiles)
     return _host_u64(out), tiles, int(samples.item())
 
 

@@ -203,3 +203,31 @@ def test_c4_scale_part_no_hang(cuda):
     assert out.shape[0] == sum(tc.count for tc in tiles)
     v = out.view(torch.int64)
     assert int((v[:, 0] >> (k - t)).max()) == 0  # part 0 owns tile row 0
+
+
+@pytest.mark.parametrize("rng", ["philox4x32", "reference"])
+def test_c4_balanced_parts_emit_the_same_tiles(cuda, rng):
+    """Balanced ownership moves whole tiles between parts; every tile's bytes stay the same."""
+    from paper_1905_03525_b200.partition import balanced_tiles
+
+    quads = LESS_SKEWED
+    k, t, m, seed, parts = 36, 3, 2_000_000, 9, 8
+    p = params_for(quads, k)
+    table = table_for("v16384", quads)
+    plan = default_plan(k, t, m, seed, parts)
+    by_tile = {}
+    for part in range(parts):
+        e, tiles, _ = generate_part(plan, p, table, part, rng=rng)
+        r = 0
+        for tc in tiles:
+            by_tile[(tc.tile_row, tc.tile_col)] = e[r:r + tc.count]
+            r += tc.count
+    total = 0
+    for part, tl in enumerate(balanced_tiles(plan, p, parts)):
+        e, tiles, _ = generate_part(plan, p, table, part, rng=rng, tiles=tl)
+        r = 0
+        for tc in tiles:
+            assert (e[r:r + tc.count] == by_tile[(tc.tile_row, tc.tile_col)]).all()
+            r += tc.count
+        total += r
+    assert total == m

@@ -29,6 +29,7 @@ from paper_1905_03525_b200 import (
 from paper_1905_03525_b200.alias import AllZeroWeights, EmptyInput, NegativeWeight, alias_sample
 from paper_1905_03525_b200.partition import (
     PartitionPlan,
+    balanced_tiles,
     default_plan,
     part_segments,
     plan_tiles,
@@ -187,6 +188,27 @@ def test_plan_parts_partition_the_whole():
     assert sorted((t.tile_row, t.tile_col, t.count) for t in whole) == \
         sorted((t.tile_row, t.tile_col, t.count) for t in parts)
     assert sum(t.count for t in whole) == 1 << 33
+
+
+@pytest.mark.parametrize("t,parts", [(3, 8), (4, 8), (2, 3), (6, 8), (0, 2)])
+def test_balanced_tiles_partition_the_same_tiles(t, parts):
+    p = validate(*LESS_SKEWED, 36)
+    plan = default_plan(36, t, 1 << 33, 1, 1)
+    whole = plan_tiles(plan, p, 0)
+    bal = balanced_tiles(plan, p, parts)
+    assert len(bal) == parts
+    got = sorted((tc.tile_row, tc.tile_col, tc.count) for part in bal for tc in part)
+    assert got == sorted((tc.tile_row, tc.tile_col, tc.count) for tc in whole)
+    zpos = {(tc.tile_row, tc.tile_col): i for i, tc in enumerate(whole)}
+    loads = [sum(tc.count for tc in part) for part in bal]
+    for part in bal:  # Z-order inside a part
+        idx = [zpos[(tc.tile_row, tc.tile_col)] for tc in part]
+        assert idx == sorted(idx)
+    # LPT bound: no part exceeds the mean by more than the largest tile
+    assert max(loads) <= sum(loads) / parts + max(tc.count for tc in whole)
+    assert balanced_tiles(plan, p, parts) == bal  # deterministic
+    if t == 3 and parts == 8:  # C4: contiguous rows give max/mean 2.41, balanced ~1.007
+        assert max(loads) / (sum(loads) / parts) < 1.01
 
 
 def test_partition_plan_rejects_bad_geometry():

@@ -3,6 +3,8 @@
 * reference-stream mode (byte-identical to rmatgen.generate) at C3 shape;
 * partitioned mode C4: less-skewed (0.45,0.22,0.22,0.11), k=36, m=2^33, t=3,
   8 parts, uint64 output -- each part timed alone on this GPU (its rows only);
+* C4 with count-balanced tile ownership (`balanced_tiles`, same t=3 tiles and
+  bytes, LPT over parts instead of contiguous tile rows);
 * the generic kernel forced on C3 (for reference).
 
     python tools/bench_modes.py > profiles/rNN_modes.json
@@ -21,7 +23,8 @@ import torch  # noqa: E402
 from paper_1905_03525_b200 import GenConfig, build_variable_table, validate  # noqa: E402
 from paper_1905_03525_b200 import _native as N  # noqa: E402
 from paper_1905_03525_b200.generator import generate_shard  # noqa: E402
-from paper_1905_03525_b200.partition import default_plan, generate_part_device  # noqa: E402
+from paper_1905_03525_b200.partition import (balanced_tiles, default_plan,  # noqa: E402
+                                             generate_part_device)
 
 
 def timed(fn, reps=3, warm=2):
@@ -76,6 +79,25 @@ def main():
                                  tot / max(x["seconds"] for x in parts),
                              "note": "each part timed alone on one B200 (uint64 pairs, 16 B/edge); "
                                      "the 8-GPU job time is the slowest part"}
+    bal = balanced_tiles(plan, pl, 8)
+    bparts = []
+    for part in range(8):
+        o, tiles, _ = generate_part_device(plan, pl, tl, part, device=dev, tiles=bal[part])
+        rows = o.shape[0]
+        del o
+        torch.cuda.empty_cache()
+        dt = timed(lambda: generate_part_device(plan, pl, tl, part, device=dev, tiles=bal[part]),
+                   reps=2, warm=1)
+        bparts.append({"part": part, "tiles": len(bal[part]), "edges": rows, "seconds": dt,
+                       "edges_per_s": rows / dt})
+        torch.cuda.empty_cache()
+    tot = sum(x["edges"] for x in bparts)
+    res["c4_balanced"] = {"parts": bparts, "total_edges": tot,
+                          "max_part_seconds": max(x["seconds"] for x in bparts),
+                          "aggregate_edges_per_s_8gpu_estimate":
+                              tot / max(x["seconds"] for x in bparts),
+                          "note": "same 64 tiles and bytes as c4_partitioned; tiles dealt to "
+                                  "parts by LPT on their counts (balanced_tiles)"}
     print(json.dumps(res, indent=1))
 
 
