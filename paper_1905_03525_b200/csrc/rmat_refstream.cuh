@@ -235,7 +235,10 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
 constexpr int kRefPThreads = 1024;
 constexpr int kRefPChunk = 4 * kRefPThreads;
 
-template <bool OUT64>
+// W32: k <= 32, so an edge (and the carry) fits one 32-bit word per side and
+// a fragment piece lands with a single shift: bits of a fragment ending at
+// stream offset `end` sit at (hi - end) in the window ending at `hi`.
+template <bool OUT64, bool W32>
 __global__ void __launch_bounds__(kRefPThreads, 1)
 k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -251,8 +254,8 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
   }
   const uint2* sA = reinterpret_cast<const uint2*>(smem);
   const uint32_t* sB = reinterpret_cast<const uint32_t*>(smem + abytes);
-  uint32_t* s_rc = reinterpret_cast<uint32_t*>(smem + abytes + bbytes);  // row | col << 16
-  uint32_t* s_end = s_rc + kRefPChunk;                                   // inclusive-end offsets
+  // per fragment of the chunk: {end bit offset (exclusive), row | col << 16}
+  uint2* s_frag = reinterpret_cast<uint2*>(smem + abytes + bbytes);
   __shared__ uint32_t s_warp[kRefPThreads / 32];
   __shared__ uint64_t s_carry_r, s_carry_c, s_nf;
   __shared__ uint32_t s_carry_len;
@@ -276,7 +279,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
       // 1. draw + select 4 fragments per thread
       const uint64_t call = chunk_base / 4 + tid;  // numpy counter = call + 1
       const u64x4 w4 = philox4x64_10(call + 1, call + 1 == 0 ? 1 : 0, 0, 0, g.key0, b);
-      uint32_t dq[4], dsum = 0;
+      uint32_t dq[4], rcq[4], dsum = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint64_t w = q == 0 ? w4.x : q == 1 ? w4.y : q == 2 ? w4.z : w4.w;
@@ -290,7 +293,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
         const uint32_t sel = ge ? 0x4432u : 0x4410u;
         const uint32_t r = prmt_ref(aw.x, sel), c = prmt_ref(aw.y, sel);
         dq[q] = chunk_base + 4 * tid + q < g.w0 ? 0u : prmt_ref(bw, 0x4440u + ge);
-        s_rc[4 * tid + q] = r | (c << 16);
+        rcq[q] = r | (c << 16);
         dsum += dq[q];
       }
       // 2. CTA exclusive scan of the depths (plus the carried bits)
@@ -317,7 +320,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         pos += dq[q];
-        s_end[4 * tid + q] = pos;
+        s_frag[4 * tid + q] = make_uint2(pos, rcq[q]);
       }
       const uint64_t carry_r = s_carry_r, carry_c = s_carry_c;
       __syncthreads();
@@ -325,7 +328,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
       // thread cuts the edges that *start* in its own 4 fragments (thread 0
       // also owns the carried bits), so no search is needed: the starting
       // fragment is found among its registers, the walk continues in smem.
-      const uint32_t ltot = s_end[kRefPChunk - 1];
+      const uint32_t ltot = s_frag[kRefPChunk - 1].x;
       const uint64_t avail = min((uint64_t)(ltot / k), count - emitted);
       {
         const uint32_t r_lo = tid == 0 ? 0u : pos - (dq[0] + dq[1] + dq[2] + dq[3]);
@@ -348,28 +351,55 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
           const uint32_t lo = j * k, hi = is_carry ? ltot : lo + k;
           uint64_t ur = 0, uc = 0;
           uint32_t p = lo;
-          if (p < carry_len) {
-            const uint32_t w = min(hi, carry_len) - p;
-            const uint32_t sh = carry_len - (p + w);
-            ur = (carry_r >> sh) & lowmask64(w);
-            uc = (carry_c >> sh) & lowmask64(w);
-            p += w;
-          }
           int sidx = 0;
-          if (p < hi) {
-            // first of this thread's fragments ending after p
-            const uint32_t e0 = r_hi - dq[3] - dq[2] - dq[1], e1 = e0 + dq[1], e2 = e1 + dq[2];
-            sidx = 4 * (int)tid + (p >= e0) + (p >= e1) + (p >= e2);
-            while (p < hi) {
-              const uint32_t end = s_end[sidx];
-              const uint32_t w = min(hi, end) - p;
-              const uint32_t sh = end - (p + w);
-              const uint32_t rc = s_rc[sidx];
-              const uint64_t msk = lowmask64(w);
-              ur = (ur << w) | (((uint64_t)(rc & 0xFFFFu) >> sh) & msk);
-              uc = (uc << w) | (((uint64_t)(rc >> 16) >> sh) & msk);
+          if constexpr (W32) {
+            uint32_t ar = 0, ac = 0;
+            if (p < carry_len) {  // carry bits end at carry_len <= hi, hi - carry_len < k
+              ar = (uint32_t)carry_r << (hi - carry_len);
+              ac = (uint32_t)carry_c << (hi - carry_len);
+              p = carry_len;
+            }
+            if (p < hi) {
+              const uint32_t e0 = r_hi - dq[3] - dq[2] - dq[1], e1 = e0 + dq[1], e2 = e1 + dq[2];
+              sidx = 4 * (int)tid + (p >= e0) + (p >= e1) + (p >= e2);
+              for (;;) {
+                const uint2 fr = s_frag[sidx++];
+                const uint32_t fr_r = fr.y & 0xFFFFu, fr_c = fr.y >> 16;
+                if (fr.x >= hi) {  // last piece: drop the bits after the window
+                  ar |= fr_r >> (fr.x - hi);
+                  ac |= fr_c >> (fr.x - hi);
+                  break;
+                }
+                ar |= fr_r << (hi - fr.x);
+                ac |= fr_c << (hi - fr.x);
+              }
+            }
+            const uint32_t wm = (hi - lo) >= 32 ? 0xFFFFFFFFu : (1u << (hi - lo)) - 1u;
+            ur = ar & wm;
+            uc = ac & wm;
+          } else {
+            if (p < carry_len) {
+              const uint32_t w = min(hi, carry_len) - p;
+              const uint32_t sh = carry_len - (p + w);
+              ur = (carry_r >> sh) & lowmask64(w);
+              uc = (carry_c >> sh) & lowmask64(w);
               p += w;
-              ++sidx;
+            }
+            if (p < hi) {
+              // first of this thread's fragments ending after p
+              const uint32_t e0 = r_hi - dq[3] - dq[2] - dq[1], e1 = e0 + dq[1], e2 = e1 + dq[2];
+              sidx = 4 * (int)tid + (p >= e0) + (p >= e1) + (p >= e2);
+              while (p < hi) {
+                const uint2 fr = s_frag[sidx];
+                const uint32_t end = fr.x;
+                const uint32_t w = min(hi, end) - p;
+                const uint32_t sh = end - (p + w);
+                const uint64_t msk = lowmask64(w);
+                ur = (ur << w) | (((uint64_t)(fr.y & 0xFFFFu) >> sh) & msk);
+                uc = (uc << w) | (((uint64_t)(fr.y >> 16) >> sh) & msk);
+                p += w;
+                ++sidx;
+              }
             }
           }
           if (is_carry) {
@@ -399,6 +429,167 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
       const uint64_t nf = s_nf;
       if (g.samples_per_block) g.samples_per_block[bi] = nf;
       if (g.samples_total) atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)nf);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scatter variant (k <= 32, every fragment depth <= k): instead of each edge
+// gathering its pieces, every fragment deposits its bits into the (at most
+// two) edge words it overlaps -- shared-memory atomicOr into per-chunk edge
+// arrays -- and the chunk's edges then leave with coalesced stores.  No
+// per-edge walk, no fragment buffer, no divergence beyond 1-vs-2 deposits.
+// The partial edge after the chunk's last complete one stays positioned in
+// its word and becomes edge 0 of the next chunk (the carry).
+// ---------------------------------------------------------------------------
+template <bool OUT64>
+__global__ void __launch_bounds__(kRefPThreads, 1)
+k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
+                    uint32_t max_edges) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t n = tab.n;
+  const size_t abytes = (size_t)n * 8, bbytes = (size_t)n * 4;
+  {
+    const uint4* srcA = reinterpret_cast<const uint4*>(tab.A);
+    uint4* dstA = reinterpret_cast<uint4*>(smem);
+    for (size_t i = threadIdx.x; i < abytes / 16; i += kRefPThreads) dstA[i] = __ldg(srcA + i);
+    const uint4* srcB = reinterpret_cast<const uint4*>(tab.B);
+    uint4* dstB = reinterpret_cast<uint4*>(smem + abytes);
+    for (size_t i = threadIdx.x; i < bbytes / 16; i += kRefPThreads) dstB[i] = __ldg(srcB + i);
+  }
+  const uint2* sA = reinterpret_cast<const uint2*>(smem);
+  const uint32_t* sB = reinterpret_cast<const uint32_t*>(smem + abytes);
+  uint32_t* s_er = reinterpret_cast<uint32_t*>(smem + abytes + bbytes);  // row words of the chunk
+  uint32_t* s_ec = s_er + max_edges;                                     // column words
+  __shared__ uint32_t s_warp[kRefPThreads / 32];
+  __shared__ uint32_t s_total, s_carry_r, s_carry_c, s_carry_len;
+  __shared__ uint64_t s_nf;
+  for (uint32_t i = threadIdx.x; i < 2 * max_edges; i += kRefPThreads) s_er[i] = 0;
+  if (threadIdx.x == 0) { s_carry_r = 0; s_carry_c = 0; s_carry_len = 0; }
+  __syncthreads();
+
+  const uint32_t tid = threadIdx.x;
+  const uint32_t k = g.k;
+  const uint32_t kmask32 = k >= 32 ? 0xFFFFFFFFu : (1u << k) - 1u;
+  const uint32_t fm = tab.fm, one = tab.one, nmask = n - 1;
+  // ceil(2^32 / k); floor(x / k) = umulhi(x + k, kmagic) - 1 for the < 2^17 offsets here
+  const uint32_t kmagic = (uint32_t)((0x100000000ull + k - 1) / k);
+
+  for (uint64_t bi = blockIdx.x; bi < n_blocks; bi += gridDim.x) {
+    const uint64_t b = g.first_block + bi;
+    const uint64_t count = min(g.B, g.m - b * g.B);
+    char* const outb = reinterpret_cast<char*>(g.out) + bi * g.B * (OUT64 ? 16 : 8);
+    uint64_t emitted = 0, chunk_base = g.w0 & ~3ull;  // words before w0 get depth 0
+    while (emitted < count) {
+      // 1. draw + select 4 fragments per thread
+      const uint64_t call = chunk_base / 4 + tid;  // numpy counter = call + 1
+      const u64x4 w4 = philox4x64_10(call + 1, call + 1 == 0 ? 1 : 0, 0, 0, g.key0, b);
+      uint32_t dq[4], rq[4], cq[4], dsum = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t w = q == 0 ? w4.x : q == 1 ? w4.y : q == 2 ? w4.z : w4.w;
+        const uint32_t idx = (uint32_t)(w >> 32) & nmask;
+        const uint32_t frac = (uint32_t)w;
+        const uint32_t bw = sB[idx];
+        const uint2 aw = sA[idx];
+        const uint64_t sum = mad_wide_ref(frac | fm, one, bw);
+        uint32_t ge = (uint32_t)(sum >> 32);
+        if ((uint32_t)sum <= fm) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
+        const uint32_t sel = ge ? 0x4432u : 0x4410u;
+        rq[q] = prmt_ref(aw.x, sel);
+        cq[q] = prmt_ref(aw.y, sel);
+        dq[q] = chunk_base + 4 * tid + q < g.w0 ? 0u : prmt_ref(bw, 0x4440u + ge);
+        dsum += dq[q];
+      }
+      // 2. CTA exclusive scan of the depths behind the carried bits
+      uint32_t incl = dsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((tid & 31) >= (uint32_t)o) incl += v;
+      }
+      if ((tid & 31) == 31) s_warp[tid >> 5] = incl;
+      if (tid == 0) {  // the carry is edge 0 of this chunk, already positioned
+        s_er[0] = s_carry_r;
+        s_ec[0] = s_carry_c;
+      }
+      __syncthreads();
+      if (tid < 32) {
+        uint32_t v = s_warp[tid], x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (tid >= (uint32_t)o) x += y;
+        }
+        s_warp[tid] = x - v;
+        if (tid == 31) s_total = x;
+      }
+      __syncthreads();
+      const uint32_t carry_len = s_carry_len;
+      const uint32_t ltot = carry_len + s_total;
+      const uint32_t nfull = ltot / k;
+      const uint64_t avail = min((uint64_t)nfull, count - emitted);
+      const bool final_chunk = emitted + avail == count;
+      const uint32_t target = (uint32_t)avail * k;  // last needed bit (final chunk)
+      // 3. deposit: fragment bits [start, end) into edge words floor(start/k) (and +1)
+      uint32_t start = carry_len + s_warp[tid >> 5] + incl - dsum;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t end = start + dq[q];
+        if (dq[q]) {
+          const uint32_t j = k == 1 ? start : __umulhi(start + k, kmagic) - 1;  // 2^32 wraps at k=1
+          const uint32_t jend = (j + 1) * k;  // end of edge j
+          if (end <= jend) {
+            const uint32_t sh = jend - end;
+            atomicOr(s_er + j, rq[q] << sh);
+            atomicOr(s_ec + j, cq[q] << sh);
+          } else {  // straddles into edge j + 1 (depth <= k: no further)
+            const uint32_t over = end - jend;
+            atomicOr(s_er + j, rq[q] >> over);
+            atomicOr(s_ec + j, cq[q] >> over);
+            if (k - over < 32) {
+              atomicOr(s_er + j + 1, rq[q] << (k - over));
+              atomicOr(s_ec + j + 1, cq[q] << (k - over));
+            }
+          }
+          // nf (generator.py:255-257): one past the fragment holding the last needed bit
+          if (final_chunk && start < target && target <= end)
+            s_nf = chunk_base + 4 * tid + q + 1 - g.w0;
+        }
+        start = end;
+      }
+      __syncthreads();
+      // 4. coalesced write-out; clear the words for the next chunk; keep the carry
+      for (uint32_t e = tid; e <= nfull; e += kRefPThreads) {
+        const uint32_t er = s_er[e], ec = s_ec[e];
+        s_er[e] = 0;
+        s_ec[e] = 0;
+        if (e < avail) {
+          const uint64_t row = emitted + e;
+          if (OUT64) {
+            reinterpret_cast<ulonglong2*>(outb)[row] =
+                make_ulonglong2((uint64_t)(er & kmask32) | g.rpre, (uint64_t)(ec & kmask32) | g.cpre);
+          } else {
+            reinterpret_cast<uint2*>(outb)[row] =
+                make_uint2((er & kmask32) | (uint32_t)g.rpre, (ec & kmask32) | (uint32_t)g.cpre);
+          }
+        } else if (e == nfull && !final_chunk) {
+          // partial edge: its bits sit at the top of the k-bit word
+          s_carry_r = er;
+          s_carry_c = ec;
+          s_carry_len = ltot - nfull * k;
+        }
+      }
+      emitted += avail;
+      chunk_base += kRefPChunk;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const uint64_t nf = s_nf;
+      if (g.samples_per_block) g.samples_per_block[bi] = nf;
+      if (g.samples_total) atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)nf);
+      s_carry_r = 0; s_carry_c = 0; s_carry_len = 0;
     }
     __syncthreads();
   }
@@ -438,8 +629,7 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
                                     const rmat_refstream_args& a, cudaStream_t st,
                                     const PackedTab* packed = nullptr, int sms = 148,
                                     size_t packed_smem_limit = 0) {
-  // Bit offsets within one chunk must fit 32 bits: carry (< k) + 1024 * dmax.
-  (void)dmax;
+  // Bit offsets within one chunk must fit 32 bits: carry (< k) + 4096 * dmax.
   RefLaunch g;
   g.k = a.k;
   g.key0 = a.seed ^ a.domain;
@@ -453,11 +643,27 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
   g.cpre = a.col_prefix;
   g.w0 = a.word_offset;
   const uint64_t nb = a.n_blocks;
+  if (packed && a.k <= 32 && dmax <= a.k) {
+    // scatter variant: buckets + this chunk's edge words (carry < k bits)
+    const uint32_t max_edges = (uint32_t)((a.k - 1 + (uint64_t)kRefPChunk * dmax) / a.k + 1);
+    const size_t smem = (size_t)packed->n * 12 + (size_t)max_edges * 8;
+    if (smem <= packed_smem_limit) {
+      auto kern = a.out_width == 8 ? k_refstream_scatter<true> : k_refstream_scatter<false>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return RMAT_ERR_CUDA;
+      const unsigned grid = (unsigned)std::min<uint64_t>(nb, (uint64_t)sms);
+      kern<<<grid, kRefPThreads, smem, st>>>(*packed, g, nb, max_edges);
+      return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+    }
+  }
   if (packed) {
-    // shared memory: buckets + chunk buffers (s_rc, s_end)
+    // shared memory: buckets + chunk buffer (s_frag)
     const size_t smem = (size_t)packed->n * 12 + (size_t)kRefPChunk * 8;
     if (smem <= packed_smem_limit) {
-      auto kern = a.out_width == 8 ? k_refstream_packed<true> : k_refstream_packed<false>;
+      auto kern = a.out_width == 8 ? (a.k <= 32 ? k_refstream_packed<true, true>
+                                                : k_refstream_packed<true, false>)
+                                   : k_refstream_packed<false, true>;
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess)
         return RMAT_ERR_CUDA;

@@ -231,3 +231,23 @@ def test_c4_balanced_parts_emit_the_same_tiles(cuda, rng):
             r += tc.count
         total += r
     assert total == m
+
+
+def test_c3_reference_mode_sampled_blocks(cuda):
+    """Reference-stream mode at C3 shape (k=28, S=2^14, 2^16-edge blocks): sampled
+    blocks bit-exact against the oracle's numpy-Philox restatement, samples too."""
+    from paper_1905_03525_b200 import generate_result
+
+    k, m, B = 28, 1 << 26, 1 << 16
+    table = table_for("v16384")
+    res = generate_result(GenConfig(params=params_for(G500, k), table=table, edge_count=m,
+                                    seed=1, rng="reference"))
+    ot = oracle_table_v("v16384")
+    nblocks = m // B
+    picks = sorted(set(np.linspace(0, nblocks - 1, 12).astype(int).tolist()))
+
+    def one(b):
+        want, nf = oracle.ref_block(ot, k, B, 1, b)
+        return bool((res.edges[b * B:(b + 1) * B] == want).all())
+    assert all(POOL.map(one, picks))
+    assert abs(res.samples_consumed / m - k / table.mean_depth) < 0.005
