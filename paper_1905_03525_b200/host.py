@@ -16,7 +16,11 @@ from .device import DeviceTable, device_table, launch_generate, launch_refstream
 from .generator import DOMAIN_BLOCK, GenConfig, edge_dtype, shard_rows
 from .params import check_k
 
-__all__ = ["generate_to_host", "write_edges", "DEFAULT_CHUNK_EDGES"]
+__all__ = ["generate_to_host", "write_edges", "DEFAULT_CHUNK_EDGES", "TABLESIZE_HEADER",
+           "bench_tablesize"]
+
+#: reference cli.py:45 -- the `rmat bench-tablesize` CSV header
+TABLESIZE_HEADER = "size,kind,edges_per_sec,samples_per_edge,expected_depth"
 
 DEFAULT_CHUNK_EDGES = 1 << 28
 
@@ -180,3 +184,65 @@ def write_edges(config: GenConfig, path: str, fmt: str = "binary", *, rank: int 
             pass
         raise
     return {"path": path, "rows": written, "r_lo": r_lo}
+
+
+def bench_tablesize(params, sizes, kind: str = "variable", m: int = 1 << 24, seed: int = 1,
+                    reps: int = 3, out: str | None = None, rng: str = "philox4x32",
+                    device=None, depth_cap: int | None = None) -> list[str]:
+    """Throughput versus fragment-table size, rows in the reference's CSV format.
+
+    Mirrors `rmat bench-tablesize` (reference cli.py:296-338): per size, build
+    the table (fixed: power-of-4 sizes, depth log4(size); variable: the
+    max-probability expansion), one warm-up, then the median of `reps` timed
+    generations; samples_per_edge = k / depth for fixed tables (the
+    reference's arithmetic identity), measured samples / m otherwise.  The
+    timed region is the device generation of all m edges into HBM (CUDA
+    events around `generate_shard`), table build excluded as in the reference
+    (cli.py:227-228).  Returns the lines; writes them to `out` if given.
+    """
+    import math
+
+    import torch
+
+    from .generator import generate_shard
+    from .table import DEFAULT_DEPTH_CAP, build_fixed_table, build_variable_table
+
+    if kind not in ("fixed", "variable"):
+        raise ValueError(f"kind must be 'fixed' or 'variable', got {kind!r}")
+    if not sizes:
+        raise ValueError("bench_tablesize requires sizes")
+    dev = require_cuda(device)
+    k = params.k
+    rows = [TABLESIZE_HEADER]
+    for size in sizes:
+        if kind == "fixed":
+            depth = round(math.log(size, 4))
+            if 4 ** depth != size:
+                raise ValueError(f"fixed tables need power-of-4 sizes, got {size}")
+            table = build_fixed_table(params, depth)
+        else:
+            table = build_variable_table(params, size,
+                                         depth_cap=depth_cap or DEFAULT_DEPTH_CAP)
+        cfg = GenConfig(params=params, table=table, edge_count=m, seed=seed, rng=rng)
+        buf, _, cnt = generate_shard(cfg, device=dev, count_samples=True)  # warm-up
+        samples = int(cnt.item())
+        times = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            a.record()
+            generate_shard(cfg, device=dev, out=buf)
+            b.record()
+            torch.cuda.synchronize(dev)
+            times.append(max(a.elapsed_time(b) / 1e3, 1e-9))
+        rate = m / sorted(times)[len(times) // 2]
+        spe = k / table.max_depth if kind == "fixed" else samples / max(m, 1)
+        rows.append(f"{size},{kind},{rate:.3f},{spe:.6f},{table.mean_depth:.6f}")
+        del buf
+    if out is not None:
+        import os
+        tmp = f"{out}.tmp.{os.getpid()}"
+        with open(tmp, "w") as f:
+            f.write("\n".join(rows) + "\n")
+        os.replace(tmp, out)
+    return rows

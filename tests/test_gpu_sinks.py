@@ -6,7 +6,7 @@ import pytest
 import torch
 
 from conftest import G500, params_for, table_for
-from paper_1905_03525_b200 import GenConfig, generate
+from paper_1905_03525_b200 import GenConfig, generate, validate
 from paper_1905_03525_b200.host import generate_to_host, write_edges
 
 pytestmark = pytest.mark.gpu
@@ -42,3 +42,22 @@ def test_generate_to_host_matches_generate(cuda):
     got = res["out"].numpy().view(np.uint32).astype(np.uint64)
     assert res["h2d_bytes"] > 0
     assert (got == generate(cfg)).all()
+
+
+def test_bench_tablesize_csv_format(cuda, tmp_path):
+    """Reference `rmat bench-tablesize` CSV (cli.py:45, 317-338): header, one row per size."""
+    from paper_1905_03525_b200.host import TABLESIZE_HEADER, bench_tablesize
+
+    p = validate(0.57, 0.19, 0.19, 0.05, 26)
+    path = str(tmp_path / "ts.csv")
+    rows = bench_tablesize(p, [256, 1024], kind="variable", m=1 << 22, reps=2, out=path)
+    assert open(path).read().splitlines() == rows
+    assert rows[0] == TABLESIZE_HEADER == "size,kind,edges_per_sec,samples_per_edge,expected_depth"
+    for line, size in zip(rows[1:], (256, 1024)):
+        s, kind, rate, spe, ed = line.split(",")
+        assert int(s) == size and kind == "variable" and float(rate) > 1e8
+        assert abs(float(spe) - 26 / float(ed)) < 0.05
+    fixed = bench_tablesize(p, [256, 4096], kind="fixed", m=1 << 20, reps=1)
+    assert [r.split(",")[3] for r in fixed[1:]] == [f"{26 / 4:.6f}", f"{26 / 6:.6f}"]
+    with pytest.raises(ValueError):
+        bench_tablesize(p, [1000], kind="fixed", m=1 << 10)
