@@ -36,6 +36,9 @@ typedef enum {
 
 typedef struct rmat_table rmat_table; /* opaque; device-resident fragment table */
 
+/* post-processing flags (rmat_postprocess; UNDIRECTED also fuses into generation) */
+enum { RMAT_POST_UNDIRECTED = 1, RMAT_POST_SCRAMBLE = 2, RMAT_POST_MIRROR = 4 };
+
 /* Table description: exactly the reference's `_Compiled` arrays
  * (generator.py:114-130), host pointers, n entries each. */
 typedef struct {
@@ -100,6 +103,8 @@ typedef struct {
   uint64_t* samples_per_stream; /* device, optional: nf of every stream, global stream order */
   int kernel;                 /* rmat_kernel; AUTO picks the fastest eligible */
   int* kernel_used;           /* host, optional: receives the variant launched */
+  uint32_t post_flags;        /* 0 or RMAT_POST_UNDIRECTED: edges leave as (max, min), fused
+                                 into the store (reference postprocess.py:26-35) */
 } rmat_gen_args;
 
 /* Replaces the `_emit` loop over blocks / tiles (generator.py:447-456,
@@ -135,6 +140,7 @@ typedef struct {
   uint64_t word_offset;       /* first word of every block stream consumed (0 = stream start);
                                  a later `_emit` on the same numpy Generator continues there
                                  (partition.py:156-159) */
+  uint32_t post_flags;        /* 0 or RMAT_POST_UNDIRECTED (as rmat_gen_args) */
 } rmat_refstream_args;
 
 rmat_status rmat_generate_refstream(const rmat_refstream_args* args, void* cuda_stream);
@@ -186,7 +192,6 @@ rmat_status rmat_dedup(const rmat_dedup_args* args, int device, void* cuda_strea
  * 4-round scramble permutation of [0, 2^k) (scramble, :82-93; round keys from
  * make_scramble_key, :61-79, computed on the host); MIRROR writes (u, v) and
  * (v, u) for every edge (mirrored, :38-43).  in == out is allowed without MIRROR. */
-enum { RMAT_POST_UNDIRECTED = 1, RMAT_POST_SCRAMBLE = 2, RMAT_POST_MIRROR = 4 };
 
 typedef struct {
   uint32_t flags;

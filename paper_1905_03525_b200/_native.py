@@ -88,7 +88,8 @@ class GenArgs(ctypes.Structure):
                 ("segments", ctypes.POINTER(Segment)), ("n_segments", ctypes.c_uint32),
                 ("out", ctypes.c_void_p), ("out_rows", ctypes.c_uint64),
                 ("samples_total", ctypes.c_void_p), ("samples_per_stream", ctypes.c_void_p),
-                ("kernel", ctypes.c_int), ("kernel_used", ctypes.POINTER(ctypes.c_int))]
+                ("kernel", ctypes.c_int), ("kernel_used", ctypes.POINTER(ctypes.c_int)),
+                ("post_flags", ctypes.c_uint32)]
 
 
 class RefArgs(ctypes.Structure):
@@ -99,7 +100,7 @@ class RefArgs(ctypes.Structure):
                 ("n_blocks", ctypes.c_uint64), ("out", ctypes.c_void_p),
                 ("samples_per_block", ctypes.c_void_p), ("samples_total", ctypes.c_void_p),
                 ("row_prefix", ctypes.c_uint64), ("col_prefix", ctypes.c_uint64),
-                ("word_offset", ctypes.c_uint64)]
+                ("word_offset", ctypes.c_uint64), ("post_flags", ctypes.c_uint32)]
 
 
 class DedupArgs(ctypes.Structure):

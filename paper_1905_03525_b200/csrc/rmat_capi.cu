@@ -116,9 +116,9 @@ rmat::GenericTab generic_view(const rmat_table* t) {
   return g;
 }
 
-template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT>
+template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND>
 rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT>;
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND>;
   const int sms = num_sms(t->device);
   int threads, blocks;
   size_t smem = 0;
@@ -145,21 +145,29 @@ rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaS
   return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
 }
 
-template <int FB, bool SMEM>
-rmat_status launch_packed_fb(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
+template <int FB, bool SMEM, bool UND>
+rmat_status launch_packed_fu(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
                              bool count, cudaStream_t st) {
   if (out64) {
     if (prefix)
-      return count ? launch_packed_t<FB, SMEM, true, true, true>(t, g, st)
-                   : launch_packed_t<FB, SMEM, true, true, false>(t, g, st);
-    return count ? launch_packed_t<FB, SMEM, true, false, true>(t, g, st)
-                 : launch_packed_t<FB, SMEM, true, false, false>(t, g, st);
+      return count ? launch_packed_t<FB, SMEM, true, true, true, UND>(t, g, st)
+                   : launch_packed_t<FB, SMEM, true, true, false, UND>(t, g, st);
+    return count ? launch_packed_t<FB, SMEM, true, false, true, UND>(t, g, st)
+                 : launch_packed_t<FB, SMEM, true, false, false, UND>(t, g, st);
   }
   if (prefix)
-    return count ? launch_packed_t<FB, SMEM, false, true, true>(t, g, st)
-                 : launch_packed_t<FB, SMEM, false, true, false>(t, g, st);
-  return count ? launch_packed_t<FB, SMEM, false, false, true>(t, g, st)
-               : launch_packed_t<FB, SMEM, false, false, false>(t, g, st);
+    return count ? launch_packed_t<FB, SMEM, false, true, true, UND>(t, g, st)
+                 : launch_packed_t<FB, SMEM, false, true, false, UND>(t, g, st);
+  return count ? launch_packed_t<FB, SMEM, false, false, true, UND>(t, g, st)
+               : launch_packed_t<FB, SMEM, false, false, false, UND>(t, g, st);
+}
+
+template <int FB, bool SMEM>
+rmat_status launch_packed_fb(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
+                             bool count, cudaStream_t st) {
+  return (g.post & RMAT_POST_UNDIRECTED)
+             ? launch_packed_fu<FB, SMEM, true>(t, g, out64, prefix, count, st)
+             : launch_packed_fu<FB, SMEM, false>(t, g, out64, prefix, count, st);
 }
 
 rmat_status launch_generic(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
@@ -318,6 +326,7 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
   if (!a || !a->table || a->k < 1 || a->k > 62 || (a->out_width != 4 && a->out_width != 8) ||
       a->edges_per_stream < 1 || (a->n_segments && !a->segments))
     return RMAT_ERR_INVALID;
+  if (a->post_flags & ~(uint32_t)RMAT_POST_UNDIRECTED) return RMAT_ERR_UNSUPPORTED;
   const rmat_table* t = a->table;
   int cur = -1;
   if (cudaGetDevice(&cur) != cudaSuccess) return RMAT_ERR_CUDA;
@@ -377,6 +386,7 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
     g.out = a->out;
     g.samples_total = a->samples_total;
     g.samples_per_stream = a->samples_per_stream;
+    g.post = a->post_flags;
     uint32_t nseg = 0;
     const uint64_t launch_begin = stream_begin;
     for (uint32_t i = s0; i < a->n_segments && nseg < (uint32_t)rmat::kMaxSegsPerLaunch; ++i) {
@@ -451,6 +461,7 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
       a->block_size < 1)
     return RMAT_ERR_INVALID;
   if (a->out_width == 4 && a->k > 32) return RMAT_ERR_INVALID;
+  if (a->post_flags & ~(uint32_t)RMAT_POST_UNDIRECTED) return RMAT_ERR_UNSUPPORTED;
   if (a->n_blocks == 0) return RMAT_OK;
   if (!a->out) return RMAT_ERR_INVALID;
   const uint64_t nblocks_all = (a->edge_count + a->block_size - 1) / a->block_size;

@@ -65,6 +65,7 @@ struct GenLaunch {
   void* out;
   uint64_t* samples_total;
   uint64_t* samples_per_stream;
+  uint32_t post;        // RMAT_POST_UNDIRECTED: fused to_undirected
   SegDev segs[kMaxSegsPerLaunch];
 };
 

@@ -68,7 +68,13 @@ __device__ __forceinline__ StreamPos open_stream(const GenLaunch& g, uint64_t s)
 }
 
 template <bool OUT64>
-__device__ __forceinline__ void store_edge(void* out, uint64_t row, uint64_t u, uint64_t v) {
+__device__ __forceinline__ void store_edge(void* out, uint64_t row, uint64_t u, uint64_t v,
+                                           bool und = false) {
+  if (und) {  // fused to_undirected (postprocess.py:26-35)
+    const uint64_t hi = u > v ? u : v;
+    v = u > v ? v : u;
+    u = hi;
+  }
   if (OUT64) {
     ulonglong2 e = make_ulonglong2(u, v);
     reinterpret_cast<ulonglong2*>(out)[row] = e;
@@ -217,7 +223,9 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
   flush_slots<OUT64, THREADS>(gptr, ring_sa + half * G * STRIDE, lo, hi);  // partial last sector
 }
 
-template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT>
+// UND: fused to_undirected (reference postprocess.py:26-35): every edge leaves
+// as (max(u, v), min(u, v)), two integer min/max per edge before staging.
+template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, 1)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
@@ -402,6 +410,17 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         v |= (uint64_t)((vch >> over) & (k > 32 ? 1u : 0u)) << 32;
       }
       if (PREFIX) { u |= p.rpre; v |= p.cpre; }
+      if constexpr (UND) {
+        if constexpr (OUT64) {
+          const uint64_t hi = u > v ? u : v;
+          v = u > v ? v : u;
+          u = hi;
+        } else {  // 32-bit endpoints: two VIMNMX
+          const uint32_t a = (uint32_t)u, b = (uint32_t)v;
+          u = max(a, b);
+          v = min(a, b);
+        }
+      }
       if (st) {
         if constexpr (OUT64) {
           sts128(stage_sa + roff, u, v);
@@ -545,7 +564,7 @@ k_generic(const GenericTab tab, const __grid_constant__ GenLaunch g) {
         const uint32_t over = len - k;
         const uint64_t u = (uint64_t)((racc >> over) & kmask) | p.rpre;
         const uint64_t v = (uint64_t)((cacc >> over) & kmask) | p.cpre;
-        store_edge<OUT64>(g.out, outrow++, u, v);
+        store_edge<OUT64>(g.out, outrow++, u, v, g.post & RMAT_POST_UNDIRECTED);
         const u128 keep = (((u128)1) << over) - 1;
         racc &= keep;
         cacc &= keep;

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "../../include/rmat_b200.h"
 
 namespace rmat {
@@ -19,8 +21,27 @@ struct PostLaunch {
   uint64_t mult[4];
   uint32_t xshift[4], rot[4];
   uint64_t mask;
+  uint32_t aligned;  // in and out 16-byte aligned
 };
 
+// PTX shifts clamp (a shift by >= the width gives 0), which makes the
+// rotation branch-free: rot = 0 -> (x | x >> k) & mask = x.
+__device__ __forceinline__ uint32_t shl_c(uint32_t x, uint32_t s) {
+  uint32_t r; asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s)); return r;
+}
+__device__ __forceinline__ uint32_t shr_c(uint32_t x, uint32_t s) {
+  uint32_t r; asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s)); return r;
+}
+__device__ __forceinline__ uint64_t shl_c(uint64_t x, uint32_t s) {
+  uint64_t r; asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(s)); return r;
+}
+__device__ __forceinline__ uint64_t shr_c(uint64_t x, uint32_t s) {
+  uint64_t r; asm("shr.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(s)); return r;
+}
+
+// Every xor-shift is >= 1 for k >= 2 (make_scramble_key: 1 + s % (k - 1));
+// k = 1 is the identity (odd multiplier mod 2, no shift, no rotation) and is
+// dropped on the host.
 template <typename U>
 __device__ __forceinline__ U scramble1(U x, const PostLaunch& g) {
   const U mask = (U)g.mask;
@@ -28,47 +49,97 @@ __device__ __forceinline__ U scramble1(U x, const PostLaunch& g) {
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     x = (x * (U)g.mult[r]) & mask;               // odd multiplier: bijective mod 2^k
-    if (g.xshift[r]) x ^= x >> g.xshift[r];
+    x ^= shr_c(x, g.xshift[r]);
     const uint32_t rt = g.rot[r];
-    if (rt) x = ((x << rt) | (x >> (k - rt))) & mask;
+    x = (shl_c(x, rt) | shr_c(x, k - rt)) & mask;
   }
   return x;
 }
 
-template <typename U>
+template <typename U, bool UND, bool SCR>
 __device__ __forceinline__ void post_edge(U& u, U& v, const PostLaunch& g) {
-  if (g.flags & RMAT_POST_UNDIRECTED) {
+  if constexpr (UND) {
     const U a = u > v ? u : v, b = u > v ? v : u;
     u = a;
     v = b;
   }
-  if (g.flags & RMAT_POST_SCRAMBLE) {
+  if constexpr (SCR) {
     u = scramble1<U>(u, g);
     v = scramble1<U>(v, g);
   }
 }
 
-template <typename U>
+// 16-byte vectors: two uint32 edges or one uint64 edge per load/store, EPV
+// edges per vector, several independent endpoints in flight per thread.
+template <typename U, bool UND, bool SCR, bool MIR>
 __global__ void __launch_bounds__(256) k_post(const PostLaunch g) {
+  constexpr int EPV = 16 / (2 * sizeof(U));
+  using W = typename std::conditional<sizeof(U) == 4, uint4, ulonglong2>::type;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const U* in = reinterpret_cast<const U*>(g.in);
-  U* out = reinterpret_cast<U*>(g.out);
-  const bool mirror = g.flags & RMAT_POST_MIRROR;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.rows; i += stride) {
-    U u = in[2 * i], v = in[2 * i + 1];
-    post_edge<U>(u, v, g);
-    if (mirror) {
-      out[4 * i] = u; out[4 * i + 1] = v;      // (u, v) then (v, u)
-      out[4 * i + 2] = v; out[4 * i + 3] = u;
-    } else {
-      out[2 * i] = u; out[2 * i + 1] = v;
+  if (!g.aligned) {  // rows not on 16-byte boundaries (sliced tensors): scalar path
+    const U* ins = reinterpret_cast<const U*>(g.in);
+    U* outs = reinterpret_cast<U*>(g.out);
+    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < g.rows; r += stride) {
+      U u = ins[2 * r], v = ins[2 * r + 1];
+      post_edge<U, UND, SCR>(u, v, g);
+      if (MIR) { outs[4 * r] = u; outs[4 * r + 1] = v; outs[4 * r + 2] = v; outs[4 * r + 3] = u; }
+      else { outs[2 * r] = u; outs[2 * r + 1] = v; }
     }
+    return;
+  }
+  const uint64_t nvec = g.rows / EPV;
+  const W* in = reinterpret_cast<const W*>(g.in);
+  W* out = reinterpret_cast<W*>(g.out);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    W w = in[i];
+    U e[2 * EPV];
+    if constexpr (EPV == 2) { e[0] = w.x; e[1] = w.y; e[2] = w.z; e[3] = w.w; }
+    else { e[0] = w.x; e[1] = w.y; }
+#pragma unroll
+    for (int q = 0; q < EPV; ++q) post_edge<U, UND, SCR>(e[2 * q], e[2 * q + 1], g);
+    if constexpr (MIR) {  // (u, v) then (v, u) for every edge
+      if constexpr (EPV == 2) {
+        out[2 * i] = make_uint4(e[0], e[1], e[1], e[0]);
+        out[2 * i + 1] = make_uint4(e[2], e[3], e[3], e[2]);
+      } else {
+        out[2 * i] = make_ulonglong2(e[0], e[1]);
+        out[2 * i + 1] = make_ulonglong2(e[1], e[0]);
+      }
+    } else {
+      if constexpr (EPV == 2) out[i] = make_uint4(e[0], e[1], e[2], e[3]);
+      else out[i] = make_ulonglong2(e[0], e[1]);
+    }
+  }
+  // odd last uint32 edge
+  if (EPV == 2 && (g.rows & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint64_t r = g.rows - 1;
+    const U* ins = reinterpret_cast<const U*>(g.in);
+    U* outs = reinterpret_cast<U*>(g.out);
+    U u = ins[2 * r], v = ins[2 * r + 1];
+    post_edge<U, UND, SCR>(u, v, g);
+    if (MIR) { outs[4 * r] = u; outs[4 * r + 1] = v; outs[4 * r + 2] = v; outs[4 * r + 3] = u; }
+    else { outs[2 * r] = u; outs[2 * r + 1] = v; }
+  }
+}
+
+template <typename U>
+inline void launch_post_t(const PostLaunch& g, unsigned blocks, cudaStream_t st) {
+  const uint32_t f = g.flags & 7u;
+  switch (f) {
+    case 0: k_post<U, false, false, false><<<blocks, 256, 0, st>>>(g); break;
+    case 1: k_post<U, true, false, false><<<blocks, 256, 0, st>>>(g); break;
+    case 2: k_post<U, false, true, false><<<blocks, 256, 0, st>>>(g); break;
+    case 3: k_post<U, true, true, false><<<blocks, 256, 0, st>>>(g); break;
+    case 4: k_post<U, false, false, true><<<blocks, 256, 0, st>>>(g); break;
+    case 5: k_post<U, true, false, true><<<blocks, 256, 0, st>>>(g); break;
+    case 6: k_post<U, false, true, true><<<blocks, 256, 0, st>>>(g); break;
+    default: k_post<U, true, true, true><<<blocks, 256, 0, st>>>(g); break;
   }
 }
 
 inline rmat_status launch_post(const rmat_post_args& a, int sms, cudaStream_t st) {
   PostLaunch g;
-  g.flags = a.flags;
+  g.flags = a.k == 1 ? (a.flags & ~(uint32_t)RMAT_POST_SCRAMBLE) : a.flags;  // k=1: identity
   g.k = a.k;
   g.rows = a.rows;
   g.in = a.in;
@@ -79,13 +150,14 @@ inline rmat_status launch_post(const rmat_post_args& a, int sms, cudaStream_t st
     g.rot[r] = a.rot[r];
   }
   g.mask = a.k >= 64 ? ~0ull : ((1ull << a.k) - 1);
+  g.aligned = ((reinterpret_cast<uintptr_t>(a.in) | reinterpret_cast<uintptr_t>(a.out)) & 15) == 0;
   const int threads = 256;
-  const uint64_t need = (a.rows + threads - 1) / threads;
-  const unsigned blocks = (unsigned)(need < (uint64_t)sms * 16 ? need : (uint64_t)sms * 16);
+  const uint64_t need = (a.rows / (a.width == 8 ? 1 : 2) + threads) / threads;
+  const unsigned blocks = (unsigned)(need < (uint64_t)sms * 8 ? need : (uint64_t)sms * 8);
   if (a.width == 8)
-    k_post<uint64_t><<<blocks, threads, 0, st>>>(g);
+    launch_post_t<uint64_t>(g, blocks, st);
   else
-    k_post<uint32_t><<<blocks, threads, 0, st>>>(g);
+    launch_post_t<uint32_t>(g, blocks, st);
   return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
 }
 

@@ -39,7 +39,23 @@ struct RefLaunch {
   uint64_t* samples_total;
   uint64_t rpre, cpre;
   uint64_t w0;    // first word of every block stream (continuation after an earlier _emit)
+  uint32_t post;  // RMAT_POST_UNDIRECTED: fused to_undirected
 };
+
+// one output edge, optionally canonicalised (max, min) (postprocess.py:26-35)
+template <bool OUT64>
+__device__ __forceinline__ void ref_store(char* outb, uint64_t row, uint64_t u, uint64_t v,
+                                          uint32_t post) {
+  if (post & RMAT_POST_UNDIRECTED) {
+    const uint64_t hi = u > v ? u : v;
+    v = u > v ? v : u;
+    u = hi;
+  }
+  if (OUT64)
+    reinterpret_cast<ulonglong2*>(outb)[row] = make_ulonglong2(u, v);
+  else
+    reinterpret_cast<uint2*>(outb)[row] = make_uint2((uint32_t)u, (uint32_t)v);
+}
 
 __device__ __forceinline__ uint64_t mad_wide_ref(uint32_t a, uint32_t b, uint32_t c) {
   uint64_t r;
@@ -160,13 +176,8 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
         }
       }
       const uint64_t row = b * g.B + emitted + e - g.first_block * g.B;
-      if (OUT64) {
-        reinterpret_cast<ulonglong2*>(g.out)[row] =
-            make_ulonglong2((ur & kmask) | g.rpre, (uc & kmask) | g.cpre);
-      } else {
-        reinterpret_cast<uint2*>(g.out)[row] =
-            make_uint2((uint32_t)(ur | g.rpre), (uint32_t)(uc | g.cpre));
-      }
+      ref_store<OUT64>(reinterpret_cast<char*>(g.out), row, (ur & kmask) | g.rpre,
+                       (uc & kmask) | g.cpre, g.post);
     }
     // 4. carry / nf (one thread), then advance
     if (tid == 0) {
@@ -412,13 +423,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
           // edge's last bit
           if (final_chunk && j + 1 == avail) s_nf = chunk_base + sidx - g.w0;
           const uint64_t row = emitted + j;
-          if (OUT64) {
-            reinterpret_cast<ulonglong2*>(outb)[row] =
-                make_ulonglong2((ur & kmask) | g.rpre, (uc & kmask) | g.cpre);
-          } else {
-            reinterpret_cast<uint2*>(outb)[row] =
-                make_uint2((uint32_t)(ur | g.rpre), (uint32_t)(uc | g.cpre));
-          }
+          ref_store<OUT64>(outb, row, (ur & kmask) | g.rpre, (uc & kmask) | g.cpre, g.post);
         }
       }
       emitted += avail;
@@ -566,14 +571,8 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
         s_er[e] = 0;
         s_ec[e] = 0;
         if (e < avail) {
-          const uint64_t row = emitted + e;
-          if (OUT64) {
-            reinterpret_cast<ulonglong2*>(outb)[row] =
-                make_ulonglong2((uint64_t)(er & kmask32) | g.rpre, (uint64_t)(ec & kmask32) | g.cpre);
-          } else {
-            reinterpret_cast<uint2*>(outb)[row] =
-                make_uint2((er & kmask32) | (uint32_t)g.rpre, (ec & kmask32) | (uint32_t)g.cpre);
-          }
+          ref_store<OUT64>(outb, emitted + e, (uint64_t)(er & kmask32) | g.rpre,
+                           (uint64_t)(ec & kmask32) | g.cpre, g.post);
         } else if (e == nfull && !final_chunk) {
           // partial edge: its bits sit at the top of the k-bit word
           s_carry_r = er;
@@ -642,6 +641,7 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
   g.rpre = a.row_prefix;
   g.cpre = a.col_prefix;
   g.w0 = a.word_offset;
+  g.post = a.post_flags;
   const uint64_t nb = a.n_blocks;
   if (packed && a.k <= 32 && dmax <= a.k) {
     // scatter variant: buckets + this chunk's edge words (carry < k bits)

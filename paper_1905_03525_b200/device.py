@@ -109,7 +109,7 @@ def _stream_ptr(dev) -> int:
 def launch_generate(dt: DeviceTable, k: int, seed: int, domain: int, edges_per_stream: int,
                     segments: list[tuple[int, int, int, int, int]], out, *,
                     samples_total=None, samples_per_stream=None,
-                    kernel: int = N.KERNEL_AUTO) -> int:
+                    kernel: int = N.KERNEL_AUTO, post_flags: int = 0) -> int:
     """rmat_generate on dt's device and torch's current stream; returns the kernel used."""
     import torch
 
@@ -124,7 +124,7 @@ def launch_generate(dt: DeviceTable, k: int, seed: int, domain: int, edges_per_s
         samples_total=samples_total.data_ptr() if samples_total is not None else None,
         samples_per_stream=(samples_per_stream.data_ptr()
                             if samples_per_stream is not None else None),
-        kernel=kernel, kernel_used=ctypes.pointer(used))
+        kernel=kernel, kernel_used=ctypes.pointer(used), post_flags=post_flags)
     with torch.cuda.device(dt.device):
         N.check(N.lib().rmat_generate(ctypes.byref(args), _stream_ptr(dt.device)),
                 "rmat_generate")
@@ -134,7 +134,7 @@ def launch_generate(dt: DeviceTable, k: int, seed: int, domain: int, edges_per_s
 def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size: int,
                      edge_count: int, first_block: int, n_blocks: int, out, *,
                      samples_per_block=None, samples_total=None, row_prefix: int = 0,
-                     col_prefix: int = 0, word_offset: int = 0) -> None:
+                     col_prefix: int = 0, word_offset: int = 0, post_flags: int = 0) -> None:
     import torch
 
     assert out.device == dt.device and out.is_contiguous()
@@ -145,7 +145,8 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
         samples_per_block=(samples_per_block.data_ptr()
                            if samples_per_block is not None else None),
         samples_total=samples_total.data_ptr() if samples_total is not None else None,
-        row_prefix=row_prefix, col_prefix=col_prefix, word_offset=word_offset)
+        row_prefix=row_prefix, col_prefix=col_prefix, word_offset=word_offset,
+        post_flags=post_flags)
     with torch.cuda.device(dt.device):
         N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), _stream_ptr(dt.device)),
                 "rmat_generate_refstream")

@@ -66,6 +66,9 @@ class GenConfig:
     (2^16 for "reference", 2^10 for "philox4x32").  threads: accepted for
     API compatibility; like the reference, it never changes the output.
     devices: CUDA device indices to spread the streams over (None = current).
+    undirected: emit every edge as (max(u, v), min(u, v)) -- the reference's
+    `to_undirected` (postprocess.py:26-35, applied by its CLI after
+    generation, cli.py:246-251) fused into the kernels' store.
     """
 
     params: RmatParams
@@ -76,6 +79,7 @@ class GenConfig:
     threads: int = 1
     rng: str = "philox4x32"
     devices: tuple[int, ...] | None = field(default=None)
+    undirected: bool = False
 
     def __post_init__(self) -> None:
         if not 0 <= self.edge_count < 1 << 63:
@@ -146,12 +150,14 @@ def generate_shard(config: GenConfig, rank: int = 0, world: int = 1, device=None
     samples = torch.zeros(1, dtype=torch.int64, device=dev) if count_samples else None
     if rows:
         dt = device_table(config.table, dev)
+        post = N.POST_UNDIRECTED if config.undirected else 0
         if config.rng == "reference":
             launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, config.edge_count, s_lo,
-                             s_hi - s_lo, out, samples_total=samples)
+                             s_hi - s_lo, out, samples_total=samples, post_flags=post)
         else:
             launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B,
-                            [(s_lo, rows, 0, 0, 0)], out, samples_total=samples, kernel=kernel)
+                            [(s_lo, rows, 0, 0, 0)], out, samples_total=samples, kernel=kernel,
+                            post_flags=post)
     return out, r_lo, samples
 
 

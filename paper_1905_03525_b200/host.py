@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _native as N
 from .device import DeviceTable, device_table, launch_generate, launch_refstream, require_cuda
 from .generator import DOMAIN_BLOCK, GenConfig, edge_dtype, shard_rows
 from .params import check_k
@@ -82,10 +83,13 @@ def generate_to_host(config: GenConfig, out=None, *, rank: int = 0, world: int =
         buf = bufs[b][:n]
         if done_copy[b] is not None:
             compute.wait_event(done_copy[b])
+        post = N.POST_UNDIRECTED if config.undirected else 0
         if config.rng == "reference":
-            launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, config.edge_count, s, ns, buf)
+            launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, config.edge_count, s, ns, buf,
+                             post_flags=post)
         else:
-            launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B, [(s, n, 0, 0, 0)], buf)
+            launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B, [(s, n, 0, 0, 0)], buf,
+                            post_flags=post)
         done_gen[b].record(compute)
         with torch.cuda.stream(copy):
             copy.wait_event(done_gen[b])
@@ -143,11 +147,13 @@ def write_edges(config: GenConfig, path: str, fmt: str = "binary", *, rank: int 
                 c_lo, c_hi = s * B, min((s + ns) * B, config.edge_count)
                 n = c_hi - c_lo
                 buf = gen[:n]
+                post = N.POST_UNDIRECTED if config.undirected else 0
                 if config.rng == "reference":
                     launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, config.edge_count, s, ns,
-                                     buf)
+                                     buf, post_flags=post)
                 else:
-                    launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B, [(s, n, 0, 0, 0)], buf)
+                    launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B, [(s, n, 0, 0, 0)], buf,
+                                    post_flags=post)
                 wide = (buf.view(torch.int32).to(torch.int64) & 0xFFFFFFFF) if k <= 32 else \
                     buf.view(torch.int64)
                 if writer is not None:

@@ -103,3 +103,73 @@ def test_device_pipeline_on_generated_edges(cuda):
     d0 = np.sort(np.bincount(u[:, 0].astype(np.int64), minlength=1 << k))
     d1 = np.sort(np.bincount(got[:, 0].astype(np.int64), minlength=1 << k))
     assert (d0 == d1).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rng,tag,k,block,kernel", [
+    ("philox4x32", "v16384", 28, 1024, 0),      # packed smem, aligned
+    ("philox4x32", "v16384", 28, 1021, 0),      # packed smem, PREFIX (unaligned) variant
+    ("philox4x32", "v1024", 33, 1024, 0),       # packed, u64 output
+    ("philox4x32", "v1024", 20, 1024, 2),       # packed global
+    ("philox4x32", "v253", 40, 500, 0),         # generic kernel
+    ("reference", "v16384", 28, 65536, 0),      # refstream scatter
+    ("reference", "v1024", 36, 65536, 0),       # refstream packed (k > 32)
+    ("reference", "v253", 20, 4096, 0),         # refstream generic
+])
+def test_fused_undirected_equals_separate_pass(cuda, rng, tag, k, block, kernel):
+    """GenConfig(undirected=True) == to_undirected(generate(...)) (reference cli.py:246-251)."""
+    import torch
+
+    from conftest import G500, params_for, table_for
+    from paper_1905_03525_b200 import GenConfig
+    from paper_1905_03525_b200.generator import generate_shard
+
+    m = 300_007
+    base = dict(params=params_for(G500, k), table=table_for(tag), edge_count=m, seed=5,
+                block_size=block, rng=rng)
+    plain, _, s0 = generate_shard(GenConfig(**base), kernel=kernel, count_samples=True)
+    fused, _, s1 = generate_shard(GenConfig(**base, undirected=True), kernel=kernel,
+                                  count_samples=True)
+    wide = torch.int32 if k <= 32 else torch.int64
+    a = plain.view(wide).cpu().numpy()
+    b = fused.view(wide).cpu().numpy()
+    if k <= 32:
+        a, b = a.view(np.uint32).astype(np.uint64), b.view(np.uint32).astype(np.uint64)
+    else:
+        a, b = a.view(np.uint64), b.view(np.uint64)
+    assert (b == OP.to_undirected(a)).all()
+    assert int(s0.item()) == int(s1.item())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [20, 32, 36])
+@pytest.mark.parametrize("rows,offset", [(4097, 0), (4096, 1), (1, 0), (3, 1)])
+def test_device_post_flag_combinations(cuda, k, rows, offset):
+    """Every undirected/scramble/mirror combination, odd row counts and 8-byte
+    misaligned slices (scalar path), both endpoint widths, against the oracle."""
+    import torch
+
+    from paper_1905_03525_b200.postprocess import make_scramble_key, postprocess_device
+
+    rng = np.random.default_rng(rows + k)
+    e = rng.integers(0, 1 << k, size=(rows + offset, 2), dtype=np.uint64)
+    width32 = k <= 32
+    host = e.astype(np.uint32) if width32 else e.view(np.int64)
+    key = make_scramble_key(11, k)
+    rounds = [tuple(r) for r in key.round_keys]
+    for und in (False, True):
+        for scr in (False, True):
+            for mir in (False, True):
+                t = torch.from_numpy(host.copy()).to(cuda)[offset:]
+                got = postprocess_device(t, k=k, undirected=und, key=key if scr else None,
+                                         mirror=mir, out=None if mir else t.clone())
+                got = got.cpu().numpy()
+                got = got.astype(np.uint64) if width32 else got.view(np.uint64)
+                want = e[offset:].copy()
+                if und:
+                    want = OP.to_undirected(want)
+                if scr:
+                    want = OP.scramble(want.reshape(-1), k, rounds).reshape(-1, 2)
+                if mir:
+                    want = OP.mirrored(want)
+                assert (got == want).all(), (und, scr, mir)

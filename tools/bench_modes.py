@@ -59,6 +59,26 @@ def main():
     del out
     torch.cuda.empty_cache()
 
+    # post-processing at full C3 (2^32 edges, 34 GB): fused undirected vs the separate pass
+    from paper_1905_03525_b200.postprocess import make_scramble_key, postprocess_device
+    m3 = 1 << 32
+    cfg = GenConfig(params=p, table=t, edge_count=m3, seed=1, block_size=1024)
+    out, _, _ = generate_shard(cfg, device=dev)
+    t_plain = timed(lambda: generate_shard(cfg, device=dev, out=out))
+    cfg_u = GenConfig(params=p, table=t, edge_count=m3, seed=1, block_size=1024, undirected=True)
+    t_fused = timed(lambda: generate_shard(cfg_u, device=dev, out=out))
+    t_und = timed(lambda: postprocess_device(out, k=28, undirected=True, out=out))
+    key = make_scramble_key(7, 28)
+    t_scr = timed(lambda: postprocess_device(out, k=28, key=key, out=out))
+    res["post_c3"] = {
+        "edges": m3, "generate_s": t_plain, "generate_fused_undirected_s": t_fused,
+        "separate_undirected_pass_s": t_und, "separate_scramble_pass_s": t_scr,
+        "separate_pass_gb_per_s": {"undirected": 2 * 8 * m3 / t_und / 1e9,
+                                   "scramble": 2 * 8 * m3 / t_scr / 1e9},
+        "note": "in-place passes read+write 16 B/edge; fused undirected adds two min/max per edge"}
+    del out
+    torch.cuda.empty_cache()
+
     pl = validate(0.45, 0.22, 0.22, 0.11, 36)
     tl = build_variable_table(pl, 1 << 14)
     plan = default_plan(36, 3, 1 << 33, 1, 8)
