@@ -235,3 +235,45 @@ def test_gpu_dedup_large_batch_incremental(cuda):
     want = opost.dedup_local(seen)
     got = np.concatenate(kept_all)
     assert (got == want).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rng", ["philox4x32", "reference"])
+def test_gpu_distinct_part_union_is_duplicate_free(cuda, rng):
+    """Reference test_partition.py:297-305 (per-tile dedup is global dedup), also over parts."""
+    from paper_1905_03525_b200.partition import default_plan, generate_part
+
+    k, t, m, seed = 8, 2, 3000, 12
+    p = params_for(G500, k)
+    for parts in (1, 3):
+        plan = default_plan(k, t, m, seed, parts)
+        alle = np.concatenate([generate_part(plan, p, table_for("v253"), part, distinct=True,
+                                             rng=rng)[0] for part in range(parts)])
+        assert len(alle) == m
+        assert len(np.unique(alle, axis=0)) == m
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rng", ["philox4x32", "reference"])
+def test_gpu_distinct_tile_fills_every_cell(cuda, rng):
+    """Reference test_partition.py:232-238: 16 distinct edges of a 16-cell tile."""
+    k, t, tile = 4, 2, (1, 3)
+    e = generate_tile(tile, 16, params_for(G500, k), table_for("v253"), k, t, 7, distinct=True,
+                      rng=rng)
+    cells = set(map(tuple, e.tolist()))
+    assert len(cells) == 16
+    assert all(u >> 2 == tile[0] and v >> 2 == tile[1] for u, v in cells)
+    e = generate_tile((5, 5), 200, params_for(G500, 8), table_for("v253"), 8, 4, 2,
+                      distinct=True, rng=rng)
+    assert len(np.unique(e, axis=0)) == 200
+
+
+@pytest.mark.gpu
+def test_gpu_dedup_local_semantics(cuda):
+    """Reference test_postprocess.py:166-214 on the device path."""
+    from paper_1905_03525_b200 import dedup_local
+
+    e = np.array([[5, 1], [2, 2], [5, 1], [0, 9], [2, 2], [7, 7]], dtype=np.uint64)
+    assert dedup_local(e).tolist() == [[5, 1], [2, 2], [0, 9], [7, 7]]  # first occurrences, in order
+    assert dedup_local(e, (0, 8), (0, 10)).shape == (4, 2)
+    assert dedup_local(np.empty((0, 2), dtype=np.uint64), (0, 1), (0, 1)).shape == (0, 2)
