@@ -107,3 +107,11 @@ def test_product_never_imports_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "liboracle" not in text, f
+
+
+def test_graft_build_entry_point():
+    """__graft_entry__.build(): nvcc for sm_100a + the oracle, then the ABI check."""
+    import __graft_entry__
+
+    __graft_entry__.build()
+    assert N.lib().rmat_abi_version() == N.ABI_VERSION
