@@ -23,7 +23,7 @@ __all__ = ["generate_to_host", "write_edges", "DEFAULT_CHUNK_EDGES", "TABLESIZE_
 #: reference cli.py:45 -- the `rmat bench-tablesize` CSV header
 TABLESIZE_HEADER = "size,kind,edges_per_sec,samples_per_edge,expected_depth"
 
-DEFAULT_CHUNK_EDGES = 1 << 28
+DEFAULT_CHUNK_EDGES = 1 << 26  # 512 MiB of u32 pairs: shortest pipeline fill (tools/e2e_probe.py)
 
 
 def generate_to_host(config: GenConfig, out=None, *, rank: int = 0, world: int = 1, device=None,
