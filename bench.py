@@ -136,7 +136,7 @@ def run_reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    res = cpu_reference(args.steps, min(args.warmup, 1), args.cpu_sample)
+    res = cpu_reference(args.steps, min(args.warmup, 1), args.ref_sample)
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": res["seconds_per_step"] * 1e3, "higher_is_better": True,
@@ -166,7 +166,10 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 25)
+    # cpu_baseline leg (our arm, rank 0, once): ~11 s of CPU work on 16 cores;
+    # --impl reference: per step, so the whole K-step run stays within minutes
+    ap.add_argument("--cpu-sample", type=int, default=1 << 28)
+    ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
