@@ -160,7 +160,8 @@ rmat_status rmat_refstream_depth_sum(const rmat_table* table, uint64_t key0, uin
  * on concatenate([edges, more])).  Rows of `in` whose (u, v) has not been seen
  * -- and is not repeated earlier in `in` -- are written to `out` in input
  * order; *kept (device) receives their number.  `in` and `out` must not
- * overlap.  Workspace: `set` of rmat_dedup_set_bytes(capacity) bytes (capacity
+ * overlap.  Workspace: `set` of rmat_dedup_set_bytes(capacity) bytes, 32-byte
+ * aligned (capacity
  * a power of two above the number of distinct keys the set will hold; half
  * full or less keeps probing short), `scratch` of rmat_dedup_scratch_bytes(rows).
  * *status (device, optional) gets RMAT_DEDUP_STATUS_* bits OR'd in. */

@@ -499,18 +499,18 @@ rmat_status rmat_refstream_depth_sum(const rmat_table* t, uint64_t key0, uint64_
   return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
 }
 
-uint64_t rmat_dedup_set_bytes(uint64_t capacity) { return capacity * 24; }
+uint64_t rmat_dedup_set_bytes(uint64_t capacity) { return capacity * 32; }
 
 uint64_t rmat_dedup_scratch_bytes(uint64_t rows) {
   const uint64_t tiles = (rows + rmat::kDedupTile - 1) / rmat::kDedupTile;
-  return rows * 8 + tiles * 8;
+  return rows * 8 + tiles * 8 + ((rows + 7) & ~7ull);  // slot, tile offsets, keep flags
 }
 
 rmat_status rmat_dedup(const rmat_dedup_args* a, int device, void* cuda_stream) {
   if (!a || (a->width != 4 && a->width != 8) || (a->flags & ~3u)) return RMAT_ERR_INVALID;
   if (!a->set || a->capacity < 2 || (a->capacity & (a->capacity - 1)) || !a->kept)
     return RMAT_ERR_INVALID;
-  if ((reinterpret_cast<uintptr_t>(a->set) & 15) != 0) return RMAT_ERR_INVALID;
+  if ((reinterpret_cast<uintptr_t>(a->set) & 31) != 0) return RMAT_ERR_INVALID;
   if (a->rows && (!a->in || !a->out || !a->scratch)) return RMAT_ERR_INVALID;
   if ((a->flags & RMAT_DEDUP_CHECK_RANGE) && !a->status) return RMAT_ERR_INVALID;
   if (a->index_base + a->rows < a->index_base || a->index_base + a->rows == ~0ull)
@@ -528,13 +528,12 @@ rmat_status rmat_dedup(const rmat_dedup_args* a, int device, void* cuda_stream) 
   g.in = a->in;
   g.out = a->out;
   g.base = a->index_base;
-  g.keys = reinterpret_cast<ulonglong2*>(a->set);
-  g.first = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a->set) +
-                                                  a->capacity * 16);
+  g.slots = reinterpret_cast<ulonglong4*>(a->set);
   g.mask = a->capacity - 1;
   g.slot_of = reinterpret_cast<uint64_t*>(a->scratch);
   g.ntiles = (a->rows + rmat::kDedupTile - 1) / rmat::kDedupTile;
   g.tile_off = g.slot_of + a->rows;
+  g.keep = reinterpret_cast<uint8_t*>(g.tile_off + g.ntiles);
   g.kept = a->kept;
   g.status = a->status;
   g.row_lo = a->row_lo; g.row_hi = a->row_hi; g.col_lo = a->col_lo; g.col_hi = a->col_hi;
@@ -554,6 +553,7 @@ rmat_status rmat_dedup(const rmat_dedup_args* a, int device, void* cuda_stream) 
     // tiles [done, done+n): shift the row window, keep priorities global
     gg.in = reinterpret_cast<const char*>(g.in) + done * rmat::kDedupTile * 2 * g.width;
     gg.slot_of = g.slot_of + done * rmat::kDedupTile;
+    gg.keep = g.keep + done * rmat::kDedupTile;
     gg.base = g.base + done * rmat::kDedupTile;
     gg.rows = std::min<uint64_t>(g.rows - done * rmat::kDedupTile, n * rmat::kDedupTile);
     gg.tile_off = g.tile_off + done;
@@ -566,6 +566,7 @@ rmat_status rmat_dedup(const rmat_dedup_args* a, int device, void* cuda_stream) 
     rmat::DedupLaunch gg = g;
     gg.in = reinterpret_cast<const char*>(g.in) + done * rmat::kDedupTile * 2 * g.width;
     gg.slot_of = g.slot_of + done * rmat::kDedupTile;
+    gg.keep = g.keep + done * rmat::kDedupTile;
     gg.base = g.base + done * rmat::kDedupTile;
     gg.rows = std::min<uint64_t>(g.rows - done * rmat::kDedupTile, n * rmat::kDedupTile);
     gg.tile_off = g.tile_off + done;

@@ -11,17 +11,20 @@
 // lower priorities, a call keeps exactly the rows of `in` that are new --
 // which is what dedup(concatenate([kept, more])) appends after `kept`.
 //
-// Layout (caller-allocated workspace, rmat_dedup_set_bytes(capacity)):
-//   keys : capacity x 16 B  (u, v) as two u64, empty = all ones
-//   first: capacity x 8 B   lowest priority seen for the slot's key
+// Layout (caller-allocated workspace, rmat_dedup_set_bytes(capacity)): one
+// 32-byte slot (= one DRAM sector) per key, so the claim, the priority update
+// and the later reads of a key touch a single sector:
+//   slot.key   16 B  (u, v) as two u64, empty = all ones
+//   slot.first  8 B  lowest priority seen for the key
+//   (8 B pad)
 // Linear probing from splitmix64(u ^ splitmix64(v)); slots are claimed with a
 // single 128-bit CAS (sm_90+ atom.cas.b128), so an edge of any width is one key.
 //
 // Kernels (all HBM/L2-latency bound, one pass each over the rows):
 //   k_dedup_insert   claim/find the slot, atomicMin the priority, remember the slot
-//   k_dedup_count    per 4096-row tile: how many rows are first occurrences
+//   k_dedup_count    per 4096-row tile: flag first occurrences (1 byte/row), count them
 //   k_dedup_scan     one CTA: exclusive tile offsets + total kept
-//   k_dedup_scatter  per tile: CTA scan of the keep flags, write kept rows in order
+//   k_dedup_scatter  per tile: CTA scan of the flags, write kept rows in order
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -40,10 +43,10 @@ struct DedupLaunch {
   const void* in;
   void* out;
   uint64_t base;
-  ulonglong2* keys;
-  unsigned long long* first;
+  ulonglong4* slots;
   uint64_t mask;  // capacity - 1
   uint64_t* slot_of;
+  uint8_t* keep;
   uint64_t* tile_off;
   uint64_t ntiles;
   uint64_t* kept;
@@ -90,7 +93,8 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const DedupLaunch g) {
     uint64_t h = splitmix_fin(e.x ^ splitmix_fin(e.y)) & g.mask;
     uint64_t probes = 0;
     for (;;) {
-      const ulonglong2 prev = cas128(g.keys + h, make_ulonglong2(~0ull, ~0ull), e);
+      const ulonglong2 prev =
+          cas128(reinterpret_cast<ulonglong2*>(g.slots + h), make_ulonglong2(~0ull, ~0ull), e);
       if ((prev.x == ~0ull && prev.y == ~0ull) || (prev.x == e.x && prev.y == e.y)) break;
       h = (h + 1) & g.mask;
       if (++probes > g.mask) {  // every slot holds another key: caller under-sized the set
@@ -99,14 +103,14 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const DedupLaunch g) {
         break;
       }
     }
-    if (h != ~0ull) atomicMin(g.first + h, (unsigned long long)(g.base + i));
+    if (h != ~0ull) atomicMin(&g.slots[h].z, (unsigned long long)(g.base + i));
     g.slot_of[i] = h;
   }
 }
 
 __device__ __forceinline__ bool dedup_keep(const DedupLaunch& g, uint64_t i) {
   const uint64_t h = g.slot_of[i];
-  return h != ~0ull && g.first[h] == g.base + i;
+  return h != ~0ull && g.slots[h].z == g.base + i;
 }
 
 __global__ void __launch_bounds__(kDedupThreads) k_dedup_count(const DedupLaunch g) {
@@ -115,7 +119,11 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup_count(const DedupLaunch
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const uint64_t i = t0 + q * kDedupThreads + threadIdx.x;
-    if (i < g.rows && dedup_keep(g, i)) ++c;
+    if (i < g.rows) {
+      const bool kp = dedup_keep(g, i);
+      g.keep[i] = kp;
+      c += kp;
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -175,7 +183,7 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup_scatter(const DedupLaun
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const uint64_t i = t0 + 4 * threadIdx.x + q;
-    keep[q] = i < g.rows && dedup_keep(g, i);
+    keep[q] = i < g.rows && g.keep[i];
     c += keep[q];
   }
   uint32_t incl = c;

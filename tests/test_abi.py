@@ -38,8 +38,8 @@ def test_pure_host_entry_points():
     L = N.lib()
     assert L.rmat_abi_version() == N.ABI_VERSION == 2
     # workspace sizing of the dedup set / scratch (pure host arithmetic)
-    assert L.rmat_dedup_set_bytes(1 << 20) == 24 << 20
-    assert L.rmat_dedup_scratch_bytes(4096) == 4096 * 8 + 8
+    assert L.rmat_dedup_set_bytes(1 << 20) == 32 << 20
+    assert L.rmat_dedup_scratch_bytes(4096) == 4096 * 8 + 8 + 4096
     assert L.rmat_dedup_scratch_bytes(0) == 0
     assert L.rmat_strerror(0) == b"ok"
     assert L.rmat_strerror(2) == b"inconsistent fragment table"

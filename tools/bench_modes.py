@@ -79,6 +79,26 @@ def main():
     del out
     torch.cuda.empty_cache()
 
+    # first-occurrence dedup (distinct tiles, dedup_local) on 2^28 C3 edges
+    from paper_1905_03525_b200.device import DedupSet
+    m4 = 1 << 28
+    cfg = GenConfig(params=p, table=t, edge_count=m4, seed=1, block_size=1024)
+    e4, _, _ = generate_shard(cfg, device=dev)
+    ds = DedupSet(m4, dev)
+    o4 = torch.empty_like(e4)
+    kept = [0]
+
+    def run_dedup():
+        ds.reset()
+        kept[0] = ds.append(e4, o4)
+    dt = timed(run_dedup, reps=3, warm=1)
+    res["dedup_c3_2pow28"] = {"edges": m4, "kept": kept[0], "seconds": dt,
+                              "edges_per_s": m4 / dt, "set_capacity": ds.capacity,
+                              "note": "rmat_dedup: 128-bit CAS hash set (reset + insert + "
+                                      "count + scan + ordered scatter), uint32 pairs"}
+    del e4, o4, ds
+    torch.cuda.empty_cache()
+
     pl = validate(0.45, 0.22, 0.22, 0.11, 36)
     tl = build_variable_table(pl, 1 << 14)
     plan = default_plan(36, 3, 1 << 33, 1, 8)
