@@ -236,3 +236,66 @@ def test_part_segments_layout():
             assert tweak == tile_key((tc.tile_row << 3) | tc.tile_col)
         r += tc.count
     assert len({s[5] for s in segs}) == len(segs)  # distinct keys per tile
+
+
+# ------------------------------------------------------------------ property tests (hypothesis)
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=50, deadline=None)
+@given(st.lists(st.floats(0.0, 100.0), min_size=1, max_size=64).filter(lambda w: sum(w) > 0))
+def test_alias_reconstruction_property(w):
+    """Reference tests/test_alias.py:105-110."""
+    t = build_alias(w)
+    np.testing.assert_allclose(t.reconstructed_probs(), np.asarray(w) / sum(w), atol=1e-12)
+
+
+@settings(max_examples=100, deadline=None)
+@given(st.tuples(st.floats(0.01, 1.0), st.floats(0.01, 1.0), st.floats(0.01, 1.0),
+                 st.floats(0.01, 1.0)), st.integers(1, 62))
+def test_validate_properties(raw, k):
+    """Reference tests/test_params.py:89-103."""
+    s = sum(raw)
+    p = validate(*(x / s for x in raw), k)
+    assert p.a + p.b + p.c + p.d == 1.0
+    assert min(p.quadrants) > 0
+    assert 0.0 < entropy(p) <= 2.0 + 1e-12
+    assert speedup_bound(p) >= 1.0 - 1e-12
+
+
+@settings(max_examples=40, deadline=None)
+@given(st.integers(1, 62), st.integers(0, 300), st.integers(0, 2**64 - 1),
+       st.sampled_from(["f1", "f5", "v253", "v1024"]))
+def test_oracle_emission_property(k, count, seed, tag):
+    """The C oracle's emission loop against a pure-Python restatement of the
+    reference's normative scalar loop (generator.py:324-356) on random words."""
+    import oracle
+    from conftest import oracle_table
+
+    ot = oracle_table(tag)
+    rng = np.random.default_rng(seed % (2**63))
+    words = rng.integers(0, 2**63, size=count * 64 + 64, dtype=np.uint64) * np.uint64(2)
+    got, nf = oracle.emit(ot, k, count, words)
+    acc_r = acc_c = 0
+    ln = 0
+    out = []
+    used = 0
+    n = ot.n
+    while len(out) < count:
+        w = int(words[used])
+        used += 1
+        idx = (w >> 32) & (n - 1) if n & (n - 1) == 0 else (w >> 32) % n
+        e = idx if (w & 0xFFFFFFFF) < int(ot.thr32[idx]) else int(ot.alias[idx])
+        d = int(ot.depth[e])
+        acc_r = (acc_r << d) | int(ot.row[e])
+        acc_c = (acc_c << d) | int(ot.col[e])
+        ln += d
+        while ln >= k and len(out) < count:
+            over = ln - k
+            out.append((acc_r >> over, acc_c >> over))
+            acc_r &= (1 << over) - 1
+            acc_c &= (1 << over) - 1
+            ln = over
+    assert got.tolist() == [list(x) for x in out]
+    assert nf == (used if count else 0)
