@@ -141,6 +141,9 @@ typedef struct {
                                  a later `_emit` on the same numpy Generator continues there
                                  (partition.py:156-159) */
   uint32_t post_flags;        /* 0 or RMAT_POST_UNDIRECTED (as rmat_gen_args) */
+  int kernel;                 /* RMAT_KERNEL_AUTO; PACKED_SMEM = one thread per block (the
+                                 fast path's kernel on numpy words), PACKED_GLOBAL = one CTA
+                                 per block (packed buckets), GENERIC = one CTA per block */
 } rmat_refstream_args;
 
 rmat_status rmat_generate_refstream(const rmat_refstream_args* args, void* cuda_stream);

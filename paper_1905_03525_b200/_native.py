@@ -100,7 +100,8 @@ class RefArgs(ctypes.Structure):
                 ("n_blocks", ctypes.c_uint64), ("out", ctypes.c_void_p),
                 ("samples_per_block", ctypes.c_void_p), ("samples_total", ctypes.c_void_p),
                 ("row_prefix", ctypes.c_uint64), ("col_prefix", ctypes.c_uint64),
-                ("word_offset", ctypes.c_uint64), ("post_flags", ctypes.c_uint32)]
+                ("word_offset", ctypes.c_uint64), ("post_flags", ctypes.c_uint32),
+                ("kernel", ctypes.c_int)]
 
 
 class DedupArgs(ctypes.Structure):

@@ -42,6 +42,19 @@ struct rmat_table {
 
 namespace {
 
+// rmat_generate_refstream AUTO policy.  One thread per block costs one
+// block-time per wave of (SMs x 512) blocks; one CTA per block costs a fixed
+// time per block.  Measured at C3 (2^16-edge blocks, 65536 of them): 70 ms
+// per wave vs 105 ms per 65536 blocks, i.e. a wave is worth 0.58 of a full
+// wave's blocks on the CTA kernel (tools/bench_modes.py).
+constexpr double kRefThreadWaveFrac = 0.58;
+
+bool ref_thread_per_block_wins(uint64_t n_blocks, int sms) {
+  const uint64_t wave = (uint64_t)sms * rmat::kSmemThreads;
+  const uint64_t waves = (n_blocks + wave - 1) / wave;
+  return (double)n_blocks >= kRefThreadWaveFrac * (double)(waves * wave);
+}
+
 struct DeviceGuard {
   int prev = -1;
   bool ok = false;
@@ -116,9 +129,9 @@ rmat::GenericTab generic_view(const rmat_table* t) {
   return g;
 }
 
-template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND>
+template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false>
 rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND>;
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF>;
   const int sms = num_sms(t->device);
   int threads, blocks;
   size_t smem = 0;
@@ -168,6 +181,31 @@ rmat_status launch_packed_fb(const rmat_table* t, const rmat::GenLaunch& g, bool
   return (g.post & RMAT_POST_UNDIRECTED)
              ? launch_packed_fu<FB, SMEM, true>(t, g, out64, prefix, count, st)
              : launch_packed_fu<FB, SMEM, false>(t, g, out64, prefix, count, st);
+}
+
+// Reference blocks through the per-thread fast-path machinery (k_packed<..., REF>):
+// one thread per reference block; packed 16-bit buckets in shared memory.
+template <bool OUT64, bool PREFIX, bool COUNT>
+rmat_status launch_ref_thread_c(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
+  return (g.post & RMAT_POST_UNDIRECTED)
+             ? launch_packed_t<16, true, OUT64, PREFIX, COUNT, true, true>(t, g, st)
+             : launch_packed_t<16, true, OUT64, PREFIX, COUNT, false, true>(t, g, st);
+}
+
+rmat_status launch_ref_thread(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
+                              bool prefix, bool count, cudaStream_t st) {
+  if (out64) {
+    if (prefix)
+      return count ? launch_ref_thread_c<true, true, true>(t, g, st)
+                   : launch_ref_thread_c<true, true, false>(t, g, st);
+    return count ? launch_ref_thread_c<true, false, true>(t, g, st)
+                 : launch_ref_thread_c<true, false, false>(t, g, st);
+  }
+  if (prefix)
+    return count ? launch_ref_thread_c<false, true, true>(t, g, st)
+                 : launch_ref_thread_c<false, true, false>(t, g, st);
+  return count ? launch_ref_thread_c<false, false, true>(t, g, st)
+               : launch_ref_thread_c<false, false, false>(t, g, st);
 }
 
 rmat_status launch_generic(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
@@ -470,8 +508,57 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
   const rmat_table* t = a->table;
   DeviceGuard guard(t->device);
   if (!guard.ok) return RMAT_ERR_DEVICE;
+  // Enough blocks to give every thread of the GPU its own: one thread per
+  // block (k_packed<..., REF>), the fast path's per-sample cost plus numpy's
+  // 64-bit Philox.  Fewer blocks: the CTA-cooperative kernels below.
+  const uint64_t E = a->block_size;
+  if (a->kernel < RMAT_KERNEL_AUTO || a->kernel > RMAT_KERNEL_GENERIC) return RMAT_ERR_INVALID;
+  const bool thread_ok = t->fb == 16 && t->scheme_p && t->packed_smem && t->dmax <= a->k &&
+                         a->k <= 33 && a->word_offset == 0 &&
+                         (double)E * a->k / t->dmin < 17179869184.0;
+  const bool cta_packed_ok = t->fb == 16 && t->scheme_p;
+  if ((a->kernel == RMAT_KERNEL_PACKED_SMEM && !thread_ok) ||
+      (a->kernel == RMAT_KERNEL_PACKED_GLOBAL && !cta_packed_ok))
+    return RMAT_ERR_UNSUPPORTED;
+  if (a->kernel == RMAT_KERNEL_PACKED_SMEM ||
+      (a->kernel == RMAT_KERNEL_AUTO && thread_ok &&
+       ref_thread_per_block_wins(a->n_blocks, num_sms(t->device)))) {
+    const uint64_t rows = std::min<uint64_t>(a->n_blocks * E, a->edge_count - a->first_block * E);
+    const uint64_t G = a->out_width == 8 ? 2 : 4;
+    const bool prefix = a->row_prefix || a->col_prefix || (E % G) != 0;
+    const bool count = a->samples_total || a->samples_per_block;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+    const uint64_t key = a->seed ^ a->domain;
+    for (uint64_t done = 0; done < a->n_blocks;) {  // one segment per launch slice
+      const uint64_t nb = std::min<uint64_t>(a->n_blocks - done, 1ull << 40);
+      rmat::GenLaunch g;
+      std::memset(&g, 0, sizeof g);
+      g.k = a->k;
+      g.k0 = (uint32_t)key;
+      g.k1 = (uint32_t)(key >> 32);
+      g.E = E;
+      g.out = a->out;
+      g.samples_total = a->samples_total;
+      g.samples_per_stream = a->samples_per_block ? a->samples_per_block + done : nullptr;
+      g.post = a->post_flags;
+      g.nseg = 1;
+      rmat::SegDev& dv = g.segs[0];
+      dv.sid_base = a->first_block + done;
+      dv.edge_count = std::min<uint64_t>(nb * E, rows - done * E);
+      dv.out_row = done * E;
+      dv.row_prefix = a->row_prefix;
+      dv.col_prefix = a->col_prefix;
+      dv.stream_begin = 0;
+      dv.key = key;
+      g.total_streams = nb;
+      const rmat_status rs = launch_ref_thread(t, g, a->out_width == 8, prefix, count, st);
+      if (rs != RMAT_OK) return rs;
+      done += nb;
+    }
+    return RMAT_OK;
+  }
   // packed shared-memory variant for power-of-two tables with 16-bit fragments
-  if (t->fb == 16 && t->scheme_p) {
+  if (cta_packed_ok && a->kernel != RMAT_KERNEL_GENERIC) {
     const rmat::PackedTab pv = packed_view(t);
     // static smem of the kernel (~300 B) stays well inside the 1 KiB margin
     return rmat::launch_refstream(generic_view(t), t->dmax, *a,

@@ -225,7 +225,14 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 
 // UND: fused to_undirected (reference postprocess.py:26-35): every edge leaves
 // as (max(u, v), min(u, v)), two integer min/max per edge before staging.
-template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND>
+// REF: the stream is a reference block instead of a fast-mode stream -- numpy's
+// Philox4x64-10 keyed [seed ^ domain, sid], word i = call(i / 4 + 1)[i % 4],
+// bucket = high 32 bits, fraction = low 32 bits (generator.py:133-142); ties
+// of the top fraction bits are settled with the word's own low bits against
+// TLO.  One thread walks one whole block, so the output equals
+// rmatgen.generate() byte for byte with the fast path's emission machinery
+// (used when there are enough blocks to fill the GPU).
+template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, 1)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
@@ -275,7 +282,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #define RMAT_RK_REGS 1
 #endif
   uint32_t rk[20];
-  if (!RMAT_RK_REGS) {
+  if (REF) {
+  } else if (!RMAT_RK_REGS) {
 #pragma unroll
     for (int i = 0; i < 20; ++i) rk[i] = g.rk[i];
   } else {
@@ -295,7 +303,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   if (!p.valid) return;
   // Tile segments carry their own key: rebuild the round keys per stream.
   auto stream_keys = [&]() {
-    if (PREFIX) {
+    if (PREFIX && !REF) {
       uint32_t k0 = p.k0, k1 = p.k1;
 #pragma unroll
       for (int i = 0; i < 10; ++i) {
@@ -307,7 +315,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
   };
   stream_keys();
-  PhiloxPre pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
+  PhiloxPre pre{};
+  if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
   uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
   uint32_t cur_r = 0, cur_c = 0, f = 0;
   uint64_t total_nf = 0;
@@ -328,7 +337,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 
   // One call's worth of samples: words, bucket entries, byte selectors.
   struct Batch {
-    uint32_t w[4], b[4], sel[4], seld[4];
+    uint32_t w[4], b[4], sel[4], seld[4], x[4];  // x: REF bucket byte offsets
     AE a[4];
     bool tie;
   };
@@ -336,12 +345,24 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // depend on the bit accumulator (software-pipelined one call ahead).
   auto fetch = [&](uint32_t jj) {
     Batch q;
-    // primary call: rounds 1-2 partly precomputed per stream (philox.cuh)
-    const u32x4 w4 = philox4x32_10_pre(jj, pre, rk);
-    q.w[0] = w4.x; q.w[1] = w4.y; q.w[2] = w4.z; q.w[3] = w4.w;
+    if constexpr (REF) {
+      // numpy counter = call + 1; key = [segment key, block]
+      const u64x4 w4 = philox4x64_10((uint64_t)jj + 1, 0, 0, 0,
+                                     ((uint64_t)p.k1 << 32) | p.k0, p.sid);
+      const uint64_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        q.w[t] = (uint32_t)ww[t];
+        q.x[t] = ((uint32_t)(ww[t] >> 32) << 2) & idxmask4;
+      }
+    } else {
+      // primary call: rounds 1-2 partly precomputed per stream (philox.cuh)
+      const u32x4 w4 = philox4x32_10_pre(jj, pre, rk);
+      q.w[0] = w4.x; q.w[1] = w4.y; q.w[2] = w4.z; q.w[3] = w4.w;
+    }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const uint32_t a4 = q.w[t] & idxmask4;
+      const uint32_t a4 = REF ? q.x[t] : (q.w[t] & idxmask4);
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
       q.a[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
     }
@@ -364,6 +385,16 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // Rare (2^-(32-F) per sample): decide fraction ties with the lazy word.
   auto resolve_ties = [&](Batch& cb, uint32_t jj) {
     if (!cb.tie) return;
+    if constexpr (REF) {  // the reference word carries its full fraction
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if ((uint32_t)mad_wide(cb.w[t] | fm, one, cb.b[t]) <= fm) {
+          const bool lt = (cb.w[t] & fm) < __ldg(tab.tlo + (cb.x[t] >> 2));
+          cb.sel[t] = lt ? 0x4410u : 0x4432u;
+          cb.seld[t] = lt ? 0x4440u : 0x4441u;
+        }
+      return;
+    }
     const u32x4 z4 = philox4x32_10_rk(jj, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
     const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
@@ -461,7 +492,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #endif
     // Philox calls drawn back to back (ILP).  Two calls fit the 128-register
     // budget of the 512-thread shared-memory CTA only for the plain variant.
-    constexpr int CPI = (SMEM && (PREFIX || OUT64 || FB == 32)) ? 1 : RMAT_CALLS_PER_ITER;
+    constexpr int CPI = (REF || (SMEM && (PREFIX || OUT64 || FB == 32))) ? 1 : RMAT_CALLS_PER_ITER;
     if (__all_sync(0xFFFFFFFFu, L >= 4 * CPI + R - 1)) {
       Batch cb[CPI];
 #pragma unroll
@@ -495,7 +526,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       p = open_stream(g, s);
       if (!p.valid) break;
       stream_keys();
-      pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
+      if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
       j = 0; cur_r = cur_c = f = 0;
       L = (uint32_t)p.left;
       roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;

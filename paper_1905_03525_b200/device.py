@@ -134,7 +134,8 @@ def launch_generate(dt: DeviceTable, k: int, seed: int, domain: int, edges_per_s
 def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size: int,
                      edge_count: int, first_block: int, n_blocks: int, out, *,
                      samples_per_block=None, samples_total=None, row_prefix: int = 0,
-                     col_prefix: int = 0, word_offset: int = 0, post_flags: int = 0) -> None:
+                     col_prefix: int = 0, word_offset: int = 0, post_flags: int = 0,
+                     kernel: int = N.KERNEL_AUTO) -> None:
     import torch
 
     assert out.device == dt.device and out.is_contiguous()
@@ -146,7 +147,7 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
                            if samples_per_block is not None else None),
         samples_total=samples_total.data_ptr() if samples_total is not None else None,
         row_prefix=row_prefix, col_prefix=col_prefix, word_offset=word_offset,
-        post_flags=post_flags)
+        post_flags=post_flags, kernel=kernel)
     with torch.cuda.device(dt.device):
         N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), _stream_ptr(dt.device)),
                 "rmat_generate_refstream")

@@ -153,7 +153,8 @@ def generate_shard(config: GenConfig, rank: int = 0, world: int = 1, device=None
         post = N.POST_UNDIRECTED if config.undirected else 0
         if config.rng == "reference":
             launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, config.edge_count, s_lo,
-                             s_hi - s_lo, out, samples_total=samples, post_flags=post)
+                             s_hi - s_lo, out, samples_total=samples, post_flags=post,
+                             kernel=kernel)
         else:
             launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B,
                             [(s_lo, rows, 0, 0, 0)], out, samples_total=samples, kernel=kernel,

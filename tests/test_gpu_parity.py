@@ -182,3 +182,52 @@ def test_reference_mode_generate_less_skewed_k36(cuda):
     want, samples = oracle.ref_generate(oracle_table("v16384", quads), 36, m, 4, 65536)
     assert (got.edges == want).all()
     assert got.samples_consumed == samples
+
+
+@pytest.mark.parametrize("tag,k,B,m", [
+    ("v16384", 28, 1 << 16, 3 * (1 << 16) + 12345),   # C3 table, reference blocks
+    ("v1024", 16, 4096, 1 << 20),                      # C1 table
+    ("v1024", 20, 1021, 300_000),                      # unaligned blocks (PREFIX variant)
+    ("v1024", 33, 2048, 200_000),                      # uint64 endpoints
+    ("f5", 13, 999, 100_000),                          # fixed-depth table
+])
+def test_reference_mode_thread_per_block_kernel(cuda, tag, k, B, m):
+    """k_packed<..., REF> (one thread per reference block) == CTA kernels == oracle,
+    including per-block sample counts."""
+    from paper_1905_03525_b200 import _native as N
+    from paper_1905_03525_b200.device import device_table, launch_refstream
+    from paper_1905_03525_b200.generator import DOMAIN_BLOCK, edge_dtype
+
+    table = table_for(tag)
+    dt = device_table(table, cuda)
+    nb = (m + B - 1) // B
+    outs, spbs = [], []
+    for kern in (N.KERNEL_PACKED_SMEM, N.KERNEL_PACKED_GLOBAL):
+        out = torch.empty((m, 2), dtype=edge_dtype(k), device=cuda)
+        spb = torch.zeros(nb, dtype=torch.int64, device=cuda)
+        tot = torch.zeros(1, dtype=torch.int64, device=cuda)
+        launch_refstream(dt, k, 5, DOMAIN_BLOCK, B, m, 0, nb, out, samples_per_block=spb,
+                         samples_total=tot, kernel=kern)
+        assert int(tot.item()) == int(spb.sum().item())
+        outs.append(out.view(torch.int32 if k <= 32 else torch.int64).cpu().numpy())
+        spbs.append(spb.cpu().numpy())
+    assert (outs[0] == outs[1]).all()
+    assert (spbs[0] == spbs[1]).all()
+    got = outs[0].view(np.uint32).astype(np.uint64) if k <= 32 else outs[0].view(np.uint64)
+    for b in sorted({0, nb // 2, nb - 1}):
+        cnt = min(B, m - b * B)
+        want, nf = oracle.ref_block(oracle_table(tag), k, cnt, 5, b)
+        assert (got[b * B:b * B + cnt] == want).all(), b
+        assert nf == spbs[0][b]
+
+
+def test_reference_mode_thread_kernel_undirected(cuda):
+    from paper_1905_03525_b200 import _native as N
+    from paper_1905_03525_b200.generator import generate_shard
+
+    p = params_for(G500, 28)
+    base = dict(params=p, table=table_for("v16384"), edge_count=1 << 20, seed=2,
+                block_size=1 << 12, rng="reference")
+    a, _, _ = generate_shard(GenConfig(**base, undirected=True), kernel=N.KERNEL_PACKED_SMEM)
+    b, _, _ = generate_shard(GenConfig(**base, undirected=True), kernel=N.KERNEL_PACKED_GLOBAL)
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))

@@ -53,6 +53,24 @@ def main():
     dt = timed(lambda: generate_shard(cfg, device=dev, out=out))
     res["reference_stream_c3_shape"] = {"edges": m, "seconds": dt, "edges_per_s": m / dt,
                                         "note": "numpy Philox4x64 blocks of 2^16, CTA per block"}
+    del out
+    torch.cuda.empty_cache()
+    # full C3 (2^32 edges = 65536 reference blocks): one thread per block vs one CTA per block
+    m3 = 1 << 32
+    cfg = GenConfig(params=p, table=t, edge_count=m3, seed=1, rng="reference")
+    out, _, _ = generate_shard(cfg, device=dev)
+    t_thr = timed(lambda: generate_shard(cfg, device=dev, out=out,
+                                         kernel=N.KERNEL_PACKED_SMEM), reps=2, warm=1)
+    t_cta = timed(lambda: generate_shard(cfg, device=dev, out=out,
+                                         kernel=N.KERNEL_PACKED_GLOBAL), reps=2, warm=1)
+    res["reference_stream_c3_full"] = {
+        "edges": m3, "thread_per_block_s": t_thr, "cta_per_block_s": t_cta,
+        "edges_per_s": m3 / min(t_thr, t_cta),
+        "thread_per_block_edges_per_s": m3 / t_thr, "cta_per_block_edges_per_s": m3 / t_cta,
+        "note": "65536 numpy-Philox blocks of 2^16; AUTO: thread-per-block when the blocks fill >= 58 % of its last wave"}
+    del out
+    torch.cuda.empty_cache()
+    out = torch.empty((m, 2), dtype=torch.uint32, device=dev)
     cfg = GenConfig(params=p, table=t, edge_count=m, seed=1, block_size=1024)
     dt = timed(lambda: generate_shard(cfg, device=dev, out=out, kernel=N.KERNEL_GENERIC))
     res["generic_kernel_c3_shape"] = {"edges": m, "seconds": dt, "edges_per_s": m / dt}
