@@ -44,10 +44,10 @@ namespace {
 
 // rmat_generate_refstream AUTO policy.  One thread per block costs one
 // block-time per wave of (SMs x 512) blocks; one CTA per block costs a fixed
-// time per block.  Measured at C3 (2^16-edge blocks, 65536 of them): 70 ms
-// per wave vs 105 ms per 65536 blocks, i.e. a wave is worth 0.58 of a full
-// wave's blocks on the CTA kernel (tools/bench_modes.py).
-constexpr double kRefThreadWaveFrac = 0.58;
+// time per block.  Measured at C3 (2^16-edge blocks, 65536 of them): 65 ms
+// per wave vs 105 ms per 65536 blocks, i.e. a wave is worth 0.54 of a full
+// wave's blocks on the CTA kernel (tools/ref_c3_time.py, bench_modes.py).
+constexpr double kRefThreadWaveFrac = 0.54;
 
 bool ref_thread_per_block_wins(uint64_t n_blocks, int sms) {
   const uint64_t wave = (uint64_t)sms * rmat::kSmemThreads;

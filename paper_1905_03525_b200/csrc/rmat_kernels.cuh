@@ -492,7 +492,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #endif
     // Philox calls drawn back to back (ILP).  Two calls fit the 128-register
     // budget of the 512-thread shared-memory CTA only for the plain variant.
-    constexpr int CPI = (REF || (SMEM && (PREFIX || OUT64 || FB == 32))) ? 1 : RMAT_CALLS_PER_ITER;
+#ifndef RMAT_REF_CPI
+#define RMAT_REF_CPI 2
+#endif
+    constexpr int CPI = (SMEM && (PREFIX || OUT64 || FB == 32)) ? 1
+                        : REF ? RMAT_REF_CPI : RMAT_CALLS_PER_ITER;
     if (__all_sync(0xFFFFFFFFu, L >= 4 * CPI + R - 1)) {
       Batch cb[CPI];
 #pragma unroll

@@ -67,7 +67,7 @@ def main():
         "edges": m3, "thread_per_block_s": t_thr, "cta_per_block_s": t_cta,
         "edges_per_s": m3 / min(t_thr, t_cta),
         "thread_per_block_edges_per_s": m3 / t_thr, "cta_per_block_edges_per_s": m3 / t_cta,
-        "note": "65536 numpy-Philox blocks of 2^16; AUTO: thread-per-block when the blocks fill >= 58 % of its last wave"}
+        "note": "65536 numpy-Philox blocks of 2^16; AUTO: thread-per-block when the blocks fill >= 54 % of its last wave"}
     del out
     torch.cuda.empty_cache()
     out = torch.empty((m, 2), dtype=torch.uint32, device=dev)
