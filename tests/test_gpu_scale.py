@@ -251,3 +251,23 @@ def test_c3_reference_mode_sampled_blocks(cuda):
         return bool((res.edges[b * B:(b + 1) * B] == want).all())
     assert all(POOL.map(one, picks))
     assert abs(res.samples_consumed / m - k / table.mean_depth) < 0.005
+
+
+def test_refstream_abi_kernel_selection_errors(cuda):
+    from paper_1905_03525_b200.device import launch_refstream
+
+    dt = device_table(table_for("v1024"), cuda)
+    out = torch.empty((100, 2), dtype=torch.uint32, device=cuda)
+    with pytest.raises(NativeError):  # kernel id out of range
+        launch_refstream(dt, 16, 1, DOMAIN_BLOCK, 10, 100, 0, 10, out, kernel=7)
+    with pytest.raises(NativeError):  # thread-per-block kernel cannot continue mid-stream
+        launch_refstream(dt, 16, 1, DOMAIN_BLOCK, 10, 100, 0, 10, out, word_offset=3,
+                         kernel=N.KERNEL_PACKED_SMEM)
+    with pytest.raises(NativeError):  # ... nor cut edges shorter than a fragment
+        launch_refstream(dt, 4, 1, DOMAIN_BLOCK, 10, 100, 0, 10, out,
+                         kernel=N.KERNEL_PACKED_SMEM)
+    dt2 = device_table(table_for("v253"), cuda)  # not a power of two: no packed layout
+    with pytest.raises(NativeError):
+        launch_refstream(dt2, 16, 1, DOMAIN_BLOCK, 10, 100, 0, 10, out,
+                         kernel=N.KERNEL_PACKED_GLOBAL)
+    launch_refstream(dt2, 16, 1, DOMAIN_BLOCK, 10, 100, 0, 10, out, kernel=N.KERNEL_GENERIC)
