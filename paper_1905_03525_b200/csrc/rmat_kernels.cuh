@@ -103,6 +103,13 @@ __device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint32_t c)
   return r;
 }
 
+// (a & b) | c as one LOP3
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t mul_hi(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -273,6 +280,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 
   const uint32_t k = g.k;
   const uint32_t kmask = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
+  const uint32_t hmask = k > 32 ? 1u : 0u;  // OUT64: bit 32 of a 33-bit edge
   const uint32_t idxmask4 = tab.idxmask4, fm = tab.fm;
   const uint32_t one = tab.one;
   // Round keys as per-thread registers (tab.zero is 0 at run time but opaque
@@ -434,13 +442,21 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       cur_c = vc;
       f = over;
       const bool st = CAREFUL ? (emit && left != 0) : emit;
-      uint64_t u = __funnelshift_r(vr, vrh, over) & kmask;
-      uint64_t v = __funnelshift_r(vc, vch, over) & kmask;
+      uint64_t u, v;
       if constexpr (OUT64) {
-        u |= (uint64_t)((vrh >> over) & (k > 32 ? 1u : 0u)) << 32;  // k <= 33
-        v |= (uint64_t)((vch >> over) & (k > 32 ? 1u : 0u)) << 32;
+        // (hi:lo) halves, each one LOP3 (a & b) | prefix: bit 32 of a 33-bit
+        // edge comes from the high accumulator word (hmask = 1 iff k = 33)
+        const uint32_t rlo = PREFIX ? (uint32_t)p.rpre : 0u, rhi = PREFIX ? (uint32_t)(p.rpre >> 32) : 0u;
+        const uint32_t clo = PREFIX ? (uint32_t)p.cpre : 0u, chi = PREFIX ? (uint32_t)(p.cpre >> 32) : 0u;
+        u = ((uint64_t)and_or(vrh >> over, hmask, rhi) << 32) |
+            and_or(__funnelshift_r(vr, vrh, over), kmask, rlo);
+        v = ((uint64_t)and_or(vch >> over, hmask, chi) << 32) |
+            and_or(__funnelshift_r(vc, vch, over), kmask, clo);
+      } else {
+        u = __funnelshift_r(vr, vrh, over) & kmask;
+        v = __funnelshift_r(vc, vch, over) & kmask;
+        if (PREFIX) { u |= p.rpre; v |= p.cpre; }
       }
-      if (PREFIX) { u |= p.rpre; v |= p.cpre; }
       if constexpr (UND) {
         if constexpr (OUT64) {
           const uint64_t hi = u > v ? u : v;
@@ -495,7 +511,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #ifndef RMAT_REF_CPI
 #define RMAT_REF_CPI 2
 #endif
-    constexpr int CPI = (SMEM && (PREFIX || OUT64 || FB == 32)) ? 1
+#ifndef RMAT_WIDE_CPI
+#define RMAT_WIDE_CPI 1
+#endif
+    constexpr int CPI = (SMEM && FB == 32) ? 1
+                        : (SMEM && (PREFIX || OUT64)) ? RMAT_WIDE_CPI
                         : REF ? RMAT_REF_CPI : RMAT_CALLS_PER_ITER;
     if (__all_sync(0xFFFFFFFFu, L >= 4 * CPI + R - 1)) {
       Batch cb[CPI];
