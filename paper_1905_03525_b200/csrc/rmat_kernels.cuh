@@ -452,10 +452,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
             and_or(__funnelshift_r(vr, vrh, over), kmask, rlo);
         v = ((uint64_t)and_or(vch >> over, hmask, chi) << 32) |
             and_or(__funnelshift_r(vc, vch, over), kmask, clo);
+      } else if constexpr (PREFIX) {
+        u = and_or(__funnelshift_r(vr, vrh, over), kmask, (uint32_t)p.rpre);
+        v = and_or(__funnelshift_r(vc, vch, over), kmask, (uint32_t)p.cpre);
       } else {
         u = __funnelshift_r(vr, vrh, over) & kmask;
         v = __funnelshift_r(vc, vch, over) & kmask;
-        if (PREFIX) { u |= p.rpre; v |= p.cpre; }
       }
       if constexpr (UND) {
         if constexpr (OUT64) {
