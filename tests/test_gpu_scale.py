@@ -271,3 +271,30 @@ def test_refstream_abi_kernel_selection_errors(cuda):
         launch_refstream(dt2, 16, 1, DOMAIN_BLOCK, 10, 100, 0, 10, out,
                          kernel=N.KERNEL_PACKED_GLOBAL)
     launch_refstream(dt2, 16, 1, DOMAIN_BLOCK, 10, 100, 0, 10, out, kernel=N.KERNEL_GENERIC)
+
+
+def test_c3_reference_mode_full_size_thread_per_block(cuda):
+    """Full C3 in reference mode (2^32 edges, 65536 numpy-Philox blocks): AUTO runs one
+    thread per block; sampled blocks bit-exact vs the oracle, and the sample total
+    equals the CTA kernel's on the same run."""
+    from paper_1905_03525_b200.generator import generate_shard
+
+    k, m, B = 28, 1 << 32, 1 << 16
+    table = table_for("v16384")
+    cfg = GenConfig(params=params_for(G500, k), table=table, edge_count=m, seed=1,
+                    rng="reference")
+    out, _, s_auto = generate_shard(cfg, count_samples=True)
+    v = out.view(torch.int32)
+    ot = oracle_table_v("v16384")
+    picks = sorted(set(np.linspace(0, m // B - 1, 8).astype(int).tolist()))
+
+    def one(b):
+        got = v[b * B:(b + 1) * B].cpu().numpy().view(np.uint32).astype(np.uint64)
+        want, _ = oracle.ref_block(ot, k, B, 1, b)
+        return bool((got == want).all())
+    assert all(POOL.map(one, picks))
+    _, _, s_cta = generate_shard(cfg, out=out, count_samples=True,
+                                 kernel=N.KERNEL_PACKED_GLOBAL)
+    assert int(s_auto.item()) == int(s_cta.item())
+    del out, v
+    torch.cuda.empty_cache()
