@@ -97,6 +97,17 @@ def main():
     del out
     torch.cuda.empty_cache()
 
+    # C2 (k=24, S=2^12, m=2^28, uint32): the fast path on BASELINE configs[1]
+    p2 = validate(0.57, 0.19, 0.19, 0.05, 24)
+    t2 = build_variable_table(p2, 1 << 12)
+    cfg2 = GenConfig(params=p2, table=t2, edge_count=1 << 28, seed=1, block_size=1024)
+    o2, _, _ = generate_shard(cfg2, device=dev)
+    dt = timed(lambda: generate_shard(cfg2, device=dev, out=o2))
+    res["c2_fast"] = {"edges": 1 << 28, "seconds": dt, "edges_per_s": (1 << 28) / dt,
+                      "gb_per_s": 8 * (1 << 28) / dt / 1e9}
+    del o2
+    torch.cuda.empty_cache()
+
     # first-occurrence dedup (distinct tiles, dedup_local) on 2^28 C3 edges
     from paper_1905_03525_b200.device import DedupSet
     m4 = 1 << 28
