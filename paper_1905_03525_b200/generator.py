@@ -182,12 +182,9 @@ def generate_device(config: GenConfig, count_samples: bool = False):
 
 
 def _to_host_u64(t) -> np.ndarray:
-    import torch
+    from .gather import copy_to_host_u64
 
-    host = t.to("cpu")
-    if host.dtype == torch.uint32:
-        return host.numpy().astype(np.uint64)
-    return host.numpy()
+    return copy_to_host_u64(t, np.empty((t.shape[0], 2), dtype=np.uint64))
 
 
 def generate_result(config: GenConfig) -> GenResult:
@@ -201,9 +198,11 @@ def generate_result(config: GenConfig) -> GenResult:
     if m == 0:
         return GenResult(np.empty((0, 2), dtype=np.uint64), 0)
     shards, samples = generate_device(config, count_samples=True)
+    from .gather import copy_to_host_u64
+
     edges = np.empty((m, 2), dtype=np.uint64)
     for t, r_lo in shards:
-        edges[r_lo:r_lo + t.shape[0]] = _to_host_u64(t)
+        copy_to_host_u64(t, edges[r_lo:r_lo + t.shape[0]])
     return GenResult(edges, samples)
 
 
@@ -213,9 +212,11 @@ def generate(config: GenConfig) -> np.ndarray:
     m = config.edge_count
     if m == 0:
         return np.empty((0, 2), dtype=np.uint64)
+    from .gather import copy_to_host_u64
+
     edges = np.empty((m, 2), dtype=np.uint64)
     for t, r_lo in generate_device(config):
-        edges[r_lo:r_lo + t.shape[0]] = _to_host_u64(t)
+        copy_to_host_u64(t, edges[r_lo:r_lo + t.shape[0]])
     return edges
 
 

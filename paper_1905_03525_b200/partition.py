@@ -337,10 +337,9 @@ def generate_part_device(plan: PartitionPlan, params: RmatParams, table: Fragmen
 
 
 def _host_u64(tensor) -> np.ndarray:
-    import torch
+    from .gather import copy_to_host_u64
 
-    h = tensor.cpu()
-    return h.numpy().astype(np.uint64) if h.dtype == torch.uint32 else h.numpy()
+    return copy_to_host_u64(tensor, np.empty((tensor.shape[0], 2), dtype=np.uint64))
 
 
 def generate_part(plan: PartitionPlan, params: RmatParams, table: FragmentTable, part: int = 0,

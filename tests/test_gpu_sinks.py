@@ -61,3 +61,20 @@ def test_bench_tablesize_csv_format(cuda, tmp_path):
     assert [r.split(",")[3] for r in fixed[1:]] == [f"{26 / 4:.6f}", f"{26 / 6:.6f}"]
     with pytest.raises(ValueError):
         bench_tablesize(p, [1000], kind="fixed", m=1 << 10)
+
+
+@pytest.mark.parametrize("rows,k", [(0, 20), (1, 20), (123457, 20), (123457, 40), (4096 * 33 + 7, 28)])
+def test_copy_to_host_u64_chunks(cuda, monkeypatch, rows, k):
+    """Pinned staging pipeline of the host gather: several chunks, odd tails, both widths."""
+    from paper_1905_03525_b200 import gather
+
+    monkeypatch.setattr(gather, "STAGING_BYTES", 64 << 10)  # force many chunks
+    monkeypatch.setattr(gather, "_STAGING", {})
+    rng = np.random.default_rng(rows)
+    want = rng.integers(0, 1 << k, size=(rows, 2), dtype=np.uint64)
+    t = torch.from_numpy(want.astype(np.uint32) if k <= 32 else want.view(np.int64)).to(cuda)
+    if k <= 32:
+        t = t.view(torch.uint32)
+    got = gather.copy_to_host_u64(t, np.empty((rows, 2), dtype=np.uint64))
+    assert got.dtype == np.uint64 and (got == want).all()
+    gather._STAGING.clear()
