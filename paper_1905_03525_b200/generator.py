@@ -187,37 +187,71 @@ def _to_host_u64(t) -> np.ndarray:
     return copy_to_host_u64(t, np.empty((t.shape[0], 2), dtype=np.uint64))
 
 
+#: generate()/generate_result() stream through HBM in slices of at most this
+#: many bytes of edges per device (whole streams), so m is bounded by host RAM only
+HOST_SLICE_BYTES = 16 << 30
+
+
+def _generate_host(config: GenConfig, count_samples: bool):
+    """(m, 2) uint64 host edges (+ samples): per device, slices of whole streams are
+    generated in HBM and gathered into the host array (gather.copy_to_host_u64)."""
+    import torch
+
+    from .gather import copy_to_host_u64
+
+    m = config.edge_count
+    edges = np.empty((m, 2), dtype=np.uint64)
+    B = config.stream_edges
+    k = config.params.k
+    width = 4 if k <= 32 else 8
+    devices = config.devices or (None,)
+    world = len(devices)
+    post = N.POST_UNDIRECTED if config.undirected else 0
+    total = 0
+    for rank, d in enumerate(devices):
+        dev = require_cuda(d)
+        s_lo, s_hi, r_lo, r_hi = shard_rows(m, B, rank, world)
+        if r_hi == r_lo:
+            continue
+        dt = device_table(config.table, dev)
+        per = max(1, HOST_SLICE_BYTES // (2 * width * B))  # streams per slice
+        buf = torch.empty((min(per * B, r_hi - r_lo), 2), dtype=edge_dtype(k), device=dev)
+        samples = torch.zeros(1, dtype=torch.int64, device=dev) if count_samples else None
+        for s in range(s_lo, s_hi, per):
+            ns = min(per, s_hi - s)
+            a, b = s * B, min((s + ns) * B, m)
+            out = buf[:b - a]
+            if config.rng == "reference":
+                launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, m, s, ns, out,
+                                 samples_total=samples, post_flags=post)
+            else:
+                launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B, [(s, b - a, 0, 0, 0)], out,
+                                samples_total=samples, post_flags=post)
+            copy_to_host_u64(out, edges[a:b])
+        if count_samples:
+            total += int(samples.item())
+    return edges, total
+
+
 def generate_result(config: GenConfig) -> GenResult:
     """Generate `edge_count` edges; host (m, 2) uint64 plus samples consumed.
 
-    Reference generator.py:435-469.  Edges are produced in HBM and copied
-    back once (the reference's return type is a host numpy array).
+    Reference generator.py:435-469.  Edges are produced in HBM and streamed
+    into the host array (the reference's return type).
     """
     check_k(config.params.k)
-    m = config.edge_count
-    if m == 0:
+    if config.edge_count == 0:
         return GenResult(np.empty((0, 2), dtype=np.uint64), 0)
-    shards, samples = generate_device(config, count_samples=True)
-    from .gather import copy_to_host_u64
-
-    edges = np.empty((m, 2), dtype=np.uint64)
-    for t, r_lo in shards:
-        copy_to_host_u64(t, edges[r_lo:r_lo + t.shape[0]])
+    edges, samples = _generate_host(config, True)
     return GenResult(edges, samples)
 
 
 def generate(config: GenConfig) -> np.ndarray:
     """Generate `edge_count` edges as a (m, 2) uint64 host array (reference generator.py:472)."""
     check_k(config.params.k)
-    m = config.edge_count
-    if m == 0:
+    if config.edge_count == 0:
         return np.empty((0, 2), dtype=np.uint64)
-    from .gather import copy_to_host_u64
-
-    edges = np.empty((m, 2), dtype=np.uint64)
-    for t, r_lo in generate_device(config):
-        copy_to_host_u64(t, edges[r_lo:r_lo + t.shape[0]])
-    return edges
+    return _generate_host(config, False)[0]
 
 
 def emit_block(table: FragmentTable, k: int, count: int, stream_key: tuple[int, int],

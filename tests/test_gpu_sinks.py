@@ -78,3 +78,19 @@ def test_copy_to_host_u64_chunks(cuda, monkeypatch, rows, k):
     got = gather.copy_to_host_u64(t, np.empty((rows, 2), dtype=np.uint64))
     assert got.dtype == np.uint64 and (got == want).all()
     gather._STAGING.clear()
+
+
+@pytest.mark.parametrize("rng,block", [("philox4x32", 1000), ("reference", 4096)])
+def test_generate_streams_through_hbm_slices(cuda, monkeypatch, rng, block):
+    """generate()/generate_result() in many HBM slices == one device-resident run."""
+    from paper_1905_03525_b200 import generate_result
+    from paper_1905_03525_b200 import generator as G
+
+    cfg = GenConfig(params=params_for(G500, 20), table=table_for("v1024"), edge_count=777_777,
+                    seed=3, block_size=block, rng=rng)
+    whole, _, s = G.generate_shard(cfg, count_samples=True)
+    want = whole.view(torch.int32).cpu().numpy().view(np.uint32).astype(np.uint64)
+    monkeypatch.setattr(G, "HOST_SLICE_BYTES", 5 * 8 * block)  # 5 streams per slice
+    res = generate_result(cfg)
+    assert (res.edges == want).all() and res.samples_consumed == int(s.item())
+    assert (generate(cfg) == want).all()
