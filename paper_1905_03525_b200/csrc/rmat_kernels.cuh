@@ -240,7 +240,13 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 // rmatgen.generate() byte for byte with the fast path's emission machinery
 // (used when there are enough blocks to fill the GPU).
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF>
-__global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, 1)
+#ifndef RMAT_GLOBAL_MINB
+#define RMAT_GLOBAL_MINB 1
+#endif
+#ifndef RMAT_GLOBAL_CPI
+#define RMAT_GLOBAL_CPI RMAT_CALLS_PER_ITER
+#endif
+__global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
   constexpr int THREADS = SMEM ? kSmemThreads : kGlobalThreads;
@@ -518,7 +524,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #endif
     constexpr int CPI = (SMEM && FB == 32) ? 1
                         : (SMEM && (PREFIX || OUT64)) ? RMAT_WIDE_CPI
-                        : REF ? RMAT_REF_CPI : RMAT_CALLS_PER_ITER;
+                        : REF ? RMAT_REF_CPI
+                        : !SMEM ? RMAT_GLOBAL_CPI : RMAT_CALLS_PER_ITER;
     if (__all_sync(0xFFFFFFFFu, L >= 4 * CPI + R - 1)) {
       Batch cb[CPI];
 #pragma unroll
