@@ -21,6 +21,7 @@ __all__ = ["copy_to_host_u64", "STAGING_BYTES"]
 #: bytes per pinned staging buffer (two per device)
 STAGING_BYTES = 256 << 20
 
+_THREADS = max(2, min(32, os.cpu_count() or 4))
 _POOL: ThreadPoolExecutor | None = None
 _STAGING: dict = {}
 
@@ -28,7 +29,7 @@ _STAGING: dict = {}
 def _pool() -> ThreadPoolExecutor:
     global _POOL
     if _POOL is None:
-        _POOL = ThreadPoolExecutor(max_workers=max(2, min(32, os.cpu_count() or 4)))
+        _POOL = ThreadPoolExecutor(max_workers=_THREADS)
     return _POOL
 
 
@@ -56,7 +57,7 @@ def copy_to_host_u64(t, dst: np.ndarray) -> np.ndarray:
     bufs, cs, evs = _staging(t.device)
     chunk = STAGING_BYTES // (2 * width)
     pool = _pool()
-    nthreads = pool._max_workers
+    nthreads = _THREADS
     pending: list[list] = [[], []]
     cs.wait_stream(torch.cuda.current_stream(t.device))  # edges produced on the compute stream
     for i, a in enumerate(range(0, rows, chunk)):
