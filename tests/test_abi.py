@@ -115,3 +115,35 @@ def test_graft_build_entry_point():
 
     __graft_entry__.build()
     assert N.lib().rmat_abi_version() == N.ABI_VERSION
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """Every ctypes mirror in _native.py has the C header's size and field offsets (gcc)."""
+    import json
+
+    specs = {
+        "rmat_table_desc": N.TableDesc, "rmat_table_info": N.TableInfo,
+        "rmat_segment": N.Segment, "rmat_gen_args": N.GenArgs,
+        "rmat_refstream_args": N.RefArgs, "rmat_post_args": N.PostArgs,
+        "rmat_dedup_args": N.DedupArgs,
+    }
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"',
+             "int main(void) {", 'printf("{");']
+    first = True
+    for cname, cls in specs.items():
+        for fname, _ in cls._fields_:
+            cf = fname.rstrip("_")  # in_ -> in
+            sep = "" if first else ","
+            first = False
+            lines.append(f'printf("{sep}\\"{cname}.{cf}\\": %zu", offsetof({cname}, {cf}));')
+        lines.append(f'printf(",\\"{cname}\\": %zu", sizeof({cname}));')
+    lines += ['printf("}");', "return 0; }"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    got = json.loads(subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout)
+    for cname, cls in specs.items():
+        assert got[cname] == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[f"{cname}.{fname.rstrip('_')}"] == getattr(cls, fname).offset, (cname, fname)
