@@ -211,6 +211,23 @@ typedef struct {
 
 rmat_status rmat_postprocess(const rmat_post_args* args, int device, void* cuda_stream);
 
+/* The reference's naive per-level sampler (naive_edges, generator.py:372-395):
+ * edge e, level l takes word word_offset + e*k + l of the numpy Philox4x64-10
+ * stream keyed [key0, key1], r = (word >> 11) * 2^-53, quadrant digit =
+ * [r >= a] + [r >= a+b] + [r >= a+b+c].  thresholds[i] = ceil(t_i * 2^53) so
+ * the comparisons are exact integer ones.  Baseline and statistical oracle. */
+typedef struct {
+  uint32_t k;              /* 1..62 */
+  uint32_t out_width;      /* 4 (k <= 32) or 8 */
+  uint64_t count;
+  uint64_t key0, key1;
+  uint64_t word_offset;
+  uint64_t thresholds[3];  /* a, a+b, a+b+c scaled by 2^53, rounded up */
+  void* out;               /* device, count x 2 */
+} rmat_naive_args;
+
+rmat_status rmat_naive_edges(const rmat_naive_args* args, int device, void* cuda_stream);
+
 const char* rmat_strerror(rmat_status status);
 int rmat_abi_version(void);
 

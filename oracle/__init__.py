@@ -283,3 +283,22 @@ def ref_tile(table: OracleTable, k: int, t: int, row: int, col: int, count: int,
     edges[:, 0] |= np.uint64(row << inner)
     edges[:, 1] |= np.uint64(col << inner)
     return edges, samples
+
+
+# ---------------------------------------------------------------- a17: naive sampler
+DOMAIN_ORACLE = 0xFF51AFD7ED558CCD  # reference _rng.py:22
+
+
+def naive_edges(quads, k: int, count: int, key0: int, key1: int = 0, start: int = 0):
+    """The reference's naive_edges (generator.py:372-395) on raw words [start, start+count*k):
+    r = (w >> 11) * 2^-53, digit = [r >= a] + [r >= a+b] + [r >= a+b+c]."""
+    a, b, c = quads[0], quads[1], quads[2]
+    words = ref_words(key0, key1, count * k, start=start).reshape(count, k)
+    r = (words >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    digit = ((r >= a).astype(np.uint64) + (r >= a + b).astype(np.uint64)
+             + (r >= a + b + c).astype(np.uint64))
+    w = np.uint64(1) << np.arange(k - 1, -1, -1, dtype=np.uint64)
+    out = np.empty((count, 2), dtype=np.uint64)
+    out[:, 0] = ((digit >> np.uint64(1)) * w).sum(axis=1, dtype=np.uint64)
+    out[:, 1] = ((digit & np.uint64(1)) * w).sum(axis=1, dtype=np.uint64)
+    return out

@@ -18,6 +18,8 @@ from .generator import (
     GenConfig,
     GenResult,
     emit_block,
+    naive_edge,
+    naive_edges,
     generate,
     generate_device,
     generate_result,
@@ -78,6 +80,7 @@ __all__ = [
     "AliasTable", "alias_sample", "build_alias",
     "DEFAULT_BLOCK_SIZE", "FAST_STREAM_EDGES", "DOMAIN_BLOCK", "DOMAIN_TILE", "RNG_MODES",
     "Edge", "GenConfig", "GenResult", "emit_block", "generate", "generate_device",
+    "naive_edge", "naive_edges",
     "generate_result", "generate_shard", "shard_rows", "stream_replay_words",
     "GRAPH500", "MAX_K", "BadExponent", "NegativeOrZeroWeight", "RmatParams",
     "SumOutOfTolerance", "entropy", "speedup_bound", "validate",

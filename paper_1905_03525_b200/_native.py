@@ -114,6 +114,13 @@ class DedupArgs(ctypes.Structure):
                 ("col_lo", ctypes.c_uint64), ("col_hi", ctypes.c_uint64)]
 
 
+class NaiveArgs(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_uint32), ("out_width", ctypes.c_uint32), ("count", ctypes.c_uint64),
+                ("key0", ctypes.c_uint64), ("key1", ctypes.c_uint64),
+                ("word_offset", ctypes.c_uint64), ("thresholds", ctypes.c_uint64 * 3),
+                ("out", ctypes.c_void_p)]
+
+
 DEDUP_RESET, DEDUP_CHECK_RANGE = 1, 2
 DEDUP_STATUS_RANGE, DEDUP_STATUS_FULL = 1, 2
 
@@ -134,7 +141,7 @@ KERNEL_NAMES = {1: "packed_smem", 2: "packed_global", 3: "generic"}
 EXPORTS = ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
            "rmat_replay_words", "rmat_generate_refstream", "rmat_refstream_depth_sum",
            "rmat_dedup_set_bytes", "rmat_dedup_scratch_bytes", "rmat_dedup", "rmat_postprocess",
-           "rmat_strerror", "rmat_abi_version")
+           "rmat_naive_edges", "rmat_strerror", "rmat_abi_version")
 
 ABI_VERSION = 2
 
@@ -169,12 +176,13 @@ def lib() -> ctypes.CDLL:
     L.rmat_dedup_scratch_bytes.argtypes = [ctypes.c_uint64]
     L.rmat_dedup_scratch_bytes.restype = ctypes.c_uint64
     L.rmat_dedup.argtypes = [ctypes.POINTER(DedupArgs), ctypes.c_int, vp]
+    L.rmat_naive_edges.argtypes = [ctypes.POINTER(NaiveArgs), ctypes.c_int, vp]
     L.rmat_strerror.argtypes = [ctypes.c_int]
     L.rmat_strerror.restype = ctypes.c_char_p
     L.rmat_abi_version.restype = ctypes.c_int
     for f in ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
               "rmat_replay_words", "rmat_generate_refstream", "rmat_postprocess",
-              "rmat_refstream_depth_sum", "rmat_dedup"):
+              "rmat_refstream_depth_sum", "rmat_dedup", "rmat_naive_edges"):
         getattr(L, f).restype = ctypes.c_int
     return L
 

@@ -18,6 +18,7 @@
 #include "rmat_post.cuh"
 #include "rmat_refstream.cuh"
 #include "rmat_dedup.cuh"
+#include "rmat_naive.cuh"
 
 struct rmat_table {
   int device;
@@ -660,6 +661,36 @@ rmat_status rmat_dedup(const rmat_dedup_args* a, int device, void* cuda_stream) 
     rmat::k_dedup_scatter<<<(unsigned)n, rmat::kDedupThreads, 0, st>>>(gg);
     done += n;
   }
+  return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+}
+
+rmat_status rmat_naive_edges(const rmat_naive_args* a, int device, void* cuda_stream) {
+  if (!a || a->k < 1 || a->k > 62 || (a->out_width != 4 && a->out_width != 8) ||
+      (a->out_width == 4 && a->k > 32))
+    return RMAT_ERR_INVALID;
+  if (a->count == 0) return RMAT_OK;
+  if (!a->out) return RMAT_ERR_INVALID;
+  for (int i = 0; i < 3; ++i)
+    if (a->thresholds[i] > (1ull << 53)) return RMAT_ERR_INVALID;
+  DeviceGuard guard(device);
+  if (!guard.ok) return RMAT_ERR_DEVICE;
+  rmat::NaiveLaunch g;
+  g.k = a->k;
+  g.count = a->count;
+  g.key0 = a->key0;
+  g.key1 = a->key1;
+  g.w0 = a->word_offset;
+  g.t1 = a->thresholds[0];
+  g.t2 = a->thresholds[1];
+  g.t3 = a->thresholds[2];
+  g.out = a->out;
+  const unsigned blocks =
+      (unsigned)std::min<uint64_t>((a->count + 255) / 256, (uint64_t)num_sms(device) * 16);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  if (a->out_width == 8)
+    rmat::k_naive<true><<<blocks, 256, 0, st>>>(g);
+  else
+    rmat::k_naive<false><<<blocks, 256, 0, st>>>(g);
   return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
 }
 

@@ -23,6 +23,7 @@ function of (table, k, m, seed, block_size, rng) and never of the GPU count.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 from typing import NamedTuple
 
@@ -37,6 +38,7 @@ __all__ = [
     "DEFAULT_BLOCK_SIZE", "FAST_STREAM_EDGES", "DOMAIN_BLOCK", "DOMAIN_TILE", "RNG_MODES",
     "Edge", "GenConfig", "GenResult", "generate", "generate_result", "generate_device",
     "generate_shard", "emit_block", "shard_rows", "stream_replay_words", "edge_dtype",
+    "naive_edge", "naive_edges", "DOMAIN_ORACLE",
 ]
 
 #: Reference block size (reference generator.py:31) -- the default in "reference" mode.
@@ -48,6 +50,7 @@ FAST_STREAM_EDGES = 1 << 10
 DOMAIN_BLOCK = 0x9E3779B97F4A7C15
 DOMAIN_NODE = 0xBF58476D1CE4E5B9
 DOMAIN_TILE = 0x94D049BB133111EB
+DOMAIN_ORACLE = 0xFF51AFD7ED558CCD
 
 RNG_MODES = ("philox4x32", "reference")
 _M64 = (1 << 64) - 1
@@ -290,3 +293,80 @@ def stream_replay_words(table: FragmentTable, seed: int, stream: int, count: int
     """
     dev = require_cuda(device)
     return replay_words(device_table(table, dev), seed, domain, stream, count).cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# The naive per-level sampler (reference generator.py:359-395): baseline and
+# statistical oracle, on the device (k_naive), same numpy Philox words.
+# ---------------------------------------------------------------------------
+def _philox_word_position(gen) -> tuple[int, int, int]:
+    """(key0, key1, index of the next raw word) of a numpy Philox Generator."""
+    st = gen.bit_generator.state
+    if st.get("bit_generator") != "Philox":
+        raise TypeError("naive_edge(s) needs a numpy Philox Generator (e.g. keyed_stream) or a seed")
+    ctr = [int(x) for x in st["state"]["counter"]]
+    key = [int(x) for x in st["state"]["key"]]
+    if any(ctr[1:]):
+        raise ValueError("Philox counter beyond 2^64 blocks is not supported")
+    pos = int(st["buffer_pos"])
+    w = 0 if ctr[0] == 0 else 4 * (ctr[0] - 1) + pos
+    return key[0], key[1], w
+
+
+def _philox_seek(gen, w: int) -> None:
+    """Leave `gen` exactly as if it had drawn raw words up to index w - 1."""
+    st = gen.bit_generator.state
+    st["state"]["counter"] = np.array([0 if w == 0 else (w - 1) // 4, 0, 0, 0], dtype=np.uint64)
+    st["buffer_pos"] = 4
+    gen.bit_generator.state = st
+    if w:
+        gen.bit_generator.random_raw((w - 1) % 4 + 1)  # numpy refills its own buffer
+
+
+def naive_edges(params: RmatParams, k: int, count: int, rng, chunk: int = 1 << 16,
+                device=None) -> np.ndarray:
+    """Bulk naive sampler (reference generator.py:372-395): k uniforms per edge.
+
+    rng: an int seed (stream keyed (seed, DOMAIN_ORACLE, 0) as the reference)
+    or a numpy Philox Generator, which is advanced by count*k words exactly as
+    `rng.random((count, k))` would.  `chunk` is accepted for API compatibility;
+    it never changes the output (the reference draws consecutive words).
+    """
+    import math
+
+    import torch
+
+    from .gather import copy_to_host_u64
+
+    check_k(k)
+    if count < 0:
+        raise ValueError(f"count must be >= 0, got {count}")
+    if isinstance(rng, (int, np.integer)):
+        key0, key1, w0, gen = (int(rng) ^ DOMAIN_ORACLE) & _M64, 0, 0, None
+    else:
+        key0, key1, w0 = _philox_word_position(rng)
+        gen = rng
+    if count == 0:
+        return np.empty((0, 2), dtype=np.uint64)
+    a, b, c, _ = params.quadrants
+    thr = [math.ceil(t * 2.0 ** 53) for t in (a, a + b, a + b + c)]
+    dev = require_cuda(device)
+    out = torch.empty((count, 2), dtype=edge_dtype(k), device=dev)
+    args = N.NaiveArgs(k=k, out_width=out.element_size(), count=count, key0=key0, key1=key1,
+                       word_offset=w0, out=out.data_ptr())
+    for i, t in enumerate(thr):
+        args.thresholds[i] = t
+    with torch.cuda.device(dev):
+        N.check(N.lib().rmat_naive_edges(ctypes.byref(args), dev.index,
+                                         torch.cuda.current_stream(dev).cuda_stream),
+                "rmat_naive_edges")
+    edges = copy_to_host_u64(out, np.empty((count, 2), dtype=np.uint64))
+    if gen is not None:
+        _philox_seek(gen, w0 + count * k)
+    return edges
+
+
+def naive_edge(params: RmatParams, k: int, rng) -> Edge:
+    """One edge of the plain recursive process (reference generator.py:359-369)."""
+    e = naive_edges(params, k, 1, rng)
+    return Edge(int(e[0, 0]), int(e[0, 1]))

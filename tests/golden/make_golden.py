@@ -236,6 +236,25 @@ def main() -> None:
                    "out": sha(d)})
     out["dedup_local"] = dd
 
+    # ---- a17: the naive per-level sampler (generator.py:359-395)
+    from rmatgen._rng import DOMAIN_ORACLE
+    from rmatgen.generator import naive_edge, naive_edges
+    nv = {"bulk": [], "sequence": None}
+    for quads, k, count, seed in ((G500, 16, 5000, 3), (LESS, 36, 1000, 9), (G500, 62, 10, 1),
+                                  (SKEW, 1, 333, 4), (G500, 28, 70000, 11)):
+        pp = rmatgen.validate(*quads, k)
+        e = naive_edges(pp, k, count, seed)
+        nv["bulk"].append({"quads": list(quads), "k": k, "count": count, "seed": seed,
+                           "edges": sha(e)})
+    pp = rmatgen.validate(*G500, 10)
+    gen = keyed_stream(5, DOMAIN_ORACLE, 2)
+    singles = [list(naive_edge(pp, 10, gen)) for _ in range(5)]
+    bulk = naive_edges(pp, 10, 7, gen, chunk=3)
+    nxt = int(gen.bit_generator.random_raw(1)[0])
+    nv["sequence"] = {"k": 10, "seed": 5, "payload": 2, "singles": singles,
+                      "bulk_after": [[int(x) for x in r] for r in bulk], "next_word": nxt}
+    out["naive"] = nv
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", os.path.join(HERE, "golden.json"))

@@ -108,6 +108,24 @@ def main():
     del o2
     torch.cuda.empty_cache()
 
+    # the naive per-level sampler (the paper's baseline, k uniforms per edge) at C3 shape
+    import ctypes
+    import math
+    mn = 1 << 28
+    on = torch.empty((mn, 2), dtype=torch.uint32, device=dev)
+    a_, b_, c_, _ = p.quadrants
+    args = N.NaiveArgs(k=28, out_width=4, count=mn, key0=1 ^ 0xFF51AFD7ED558CCD, key1=0,
+                       word_offset=0, out=on.data_ptr())
+    for i, tv in enumerate((a_, a_ + b_, a_ + b_ + c_)):
+        args.thresholds[i] = math.ceil(tv * 2.0 ** 53)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    dt = timed(lambda: N.check(N.lib().rmat_naive_edges(ctypes.byref(args), 0, st), "naive"))
+    res["naive_c3_shape"] = {"edges": mn, "seconds": dt, "edges_per_s": mn / dt,
+                             "note": "reference naive_edges semantics (28 numpy-Philox words "
+                                     "per edge), device only"}
+    del on
+    torch.cuda.empty_cache()
+
     # first-occurrence dedup (distinct tiles, dedup_local) on 2^28 C3 edges
     from paper_1905_03525_b200.device import DedupSet
     m4 = 1 << 28
