@@ -282,7 +282,7 @@ def main() -> None:
     if traffic is not None:
         traffic = traffic / world
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the CPU leg runs on rank 0 at N=1 only
         cpu = cpu_reference(1, 1, args.cpu_sample)
         cpu.pop("seconds_per_step", None)
     line = {
