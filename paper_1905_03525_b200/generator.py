@@ -38,7 +38,7 @@ __all__ = [
     "DEFAULT_BLOCK_SIZE", "FAST_STREAM_EDGES", "DOMAIN_BLOCK", "DOMAIN_TILE", "RNG_MODES",
     "Edge", "GenConfig", "GenResult", "generate", "generate_result", "generate_device",
     "generate_shard", "emit_block", "shard_rows", "stream_replay_words", "edge_dtype",
-    "naive_edge", "naive_edges", "DOMAIN_ORACLE",
+    "naive_edge", "naive_edges", "DOMAIN_ORACLE", "gather_device",
 ]
 
 #: Reference block size (reference generator.py:31) -- the default in "reference" mode.
@@ -182,6 +182,22 @@ def generate_device(config: GenConfig, count_samples: bool = False):
     if count_samples:
         return shards, sum(int(s.item()) for s in counters)
     return shards
+
+
+def gather_device(shards, device=None):
+    """Concatenate `generate_device` shards into one tensor on `device` (SURVEY §8 e:
+    the device-side gather, only on request; cross-GPU slices go as peer copies
+    over NVLink)."""
+    import torch
+
+    dev = require_cuda(device)
+    rows = sum(t.shape[0] for t, _ in shards)
+    dtype = shards[0][0].dtype if shards else torch.uint32
+    out = torch.empty((rows, 2), dtype=dtype, device=dev)
+    for t, r_lo in shards:
+        out[r_lo:r_lo + t.shape[0]].copy_(t, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    return out
 
 
 def _to_host_u64(t) -> np.ndarray:

@@ -94,3 +94,13 @@ def test_generate_streams_through_hbm_slices(cuda, monkeypatch, rng, block):
     res = generate_result(cfg)
     assert (res.edges == want).all() and res.samples_consumed == int(s.item())
     assert (generate(cfg) == want).all()
+
+
+def test_gather_device_concatenates_shards(cuda):
+    from paper_1905_03525_b200.generator import gather_device, generate_shard
+
+    cfg = GenConfig(params=params_for(G500, 20), table=table_for("v1024"), edge_count=100_003,
+                    seed=2, block_size=1000)
+    whole, _, _ = generate_shard(cfg)
+    shards = [generate_shard(cfg, r, 3)[:2] for r in range(3)]
+    assert torch.equal(gather_device(shards, cuda).view(torch.int32), whole.view(torch.int32))
