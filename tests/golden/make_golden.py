@@ -158,7 +158,8 @@ def main() -> None:
     # ---- partition plans (C4: less-skewed, k=36, m=2^33, t=3, 8 parts)
     pl = rmatgen.validate(*LESS, 36)
     plans = []
-    for k, t, m, seed, parts in ((36, 3, 1 << 33, 1, 8), (12, 2, 10**6, 7, 4), (20, 4, 123457, 3, 3)):
+    for k, t, m, seed, parts in ((36, 3, 1 << 33, 1, 8), (12, 2, 10**6, 7, 4), (20, 4, 123457, 3, 3),
+                                 (10, 0, 1000, 3, 3), (9, 1, 5000, 2, 5)):  # parts owning no rows
         plan = default_plan(k, t, m, seed, parts)
         pp = pl if k == 36 else rmatgen.validate(*G500, k)
         quads = "less" if k == 36 else "g500"
