@@ -437,11 +437,25 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       }
       const uint32_t d = prmt(cb.b[t], cb.seld[t]);
       // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
-      const uint32_t pw = 1u << d;
       const uint32_t tt = f + d;
-      // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
-      const uint32_t vr = mad_lo(cur_r, pw, r), vrh = mul_hi(cur_r, pw);
-      const uint32_t vc = mad_lo(cur_c, pw, c), vch = mul_hi(cur_c, pw);
+      uint32_t vr, vrh, vc, vch;
+#ifndef RMAT_REF_SHIFT_APPEND
+#define RMAT_REF_SHIFT_APPEND 1
+#endif
+      if constexpr (REF && RMAT_REF_SHIFT_APPEND) {
+        // numpy's Philox4x64 keeps the FMA pipe busy: append with ALU shifts
+        vr = (cur_r << d) | r;
+        vrh = __funnelshift_l(cur_r, 0u, d);
+        vc = (cur_c << d) | c;
+        vch = __funnelshift_l(cur_c, 0u, d);
+      } else {
+        // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
+        const uint32_t pw = 1u << d;
+        vr = mad_lo(cur_r, pw, r);
+        vrh = mul_hi(cur_r, pw);
+        vc = mad_lo(cur_c, pw, c);
+        vch = mul_hi(cur_c, pw);
+      }
       const bool emit = tt >= k;
       const uint32_t over = emit ? tt - k : tt;
       cur_r = vr;
