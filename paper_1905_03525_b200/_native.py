@@ -101,7 +101,14 @@ class RefArgs(ctypes.Structure):
                 ("samples_per_block", ctypes.c_void_p), ("samples_total", ctypes.c_void_p),
                 ("row_prefix", ctypes.c_uint64), ("col_prefix", ctypes.c_uint64),
                 ("word_offset", ctypes.c_uint64), ("post_flags", ctypes.c_uint32),
-                ("kernel", ctypes.c_int)]
+                ("kernel", ctypes.c_int), ("segments", ctypes.c_void_p),
+                ("n_segments", ctypes.c_uint64), ("segment_stream", ctypes.c_uint64)]
+
+
+class RefSegment(ctypes.Structure):
+    _fields_ = [("word_begin", ctypes.c_uint64), ("out_row", ctypes.c_uint64),
+                ("count", ctypes.c_uint64), ("lead", ctypes.c_uint32),
+                ("report_nf", ctypes.c_uint32)]
 
 
 class DedupArgs(ctypes.Structure):
@@ -141,7 +148,8 @@ KERNEL_NAMES = {1: "packed_smem", 2: "packed_global", 3: "generic"}
 EXPORTS = ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
            "rmat_replay_words", "rmat_generate_refstream", "rmat_refstream_depth_sum",
            "rmat_dedup_set_bytes", "rmat_dedup_scratch_bytes", "rmat_dedup", "rmat_postprocess",
-           "rmat_naive_edges", "rmat_strerror", "rmat_abi_version")
+           "rmat_naive_edges", "rmat_refstream_segment_depths", "rmat_strerror",
+           "rmat_abi_version")
 
 ABI_VERSION = 2
 
@@ -177,12 +185,14 @@ def lib() -> ctypes.CDLL:
     L.rmat_dedup_scratch_bytes.restype = ctypes.c_uint64
     L.rmat_dedup.argtypes = [ctypes.POINTER(DedupArgs), ctypes.c_int, vp]
     L.rmat_naive_edges.argtypes = [ctypes.POINTER(NaiveArgs), ctypes.c_int, vp]
+    L.rmat_refstream_segment_depths.argtypes = [vp] + [ctypes.c_uint64] * 5 + [vp, vp]
     L.rmat_strerror.argtypes = [ctypes.c_int]
     L.rmat_strerror.restype = ctypes.c_char_p
     L.rmat_abi_version.restype = ctypes.c_int
     for f in ("rmat_table_create", "rmat_table_destroy", "rmat_table_get_info", "rmat_generate",
               "rmat_replay_words", "rmat_generate_refstream", "rmat_postprocess",
-              "rmat_refstream_depth_sum", "rmat_dedup", "rmat_naive_edges"):
+              "rmat_refstream_depth_sum", "rmat_dedup", "rmat_naive_edges",
+              "rmat_refstream_segment_depths"):
         getattr(L, f).restype = ctypes.c_int
     return L
 

@@ -501,11 +501,13 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
     return RMAT_ERR_INVALID;
   if (a->out_width == 4 && a->k > 32) return RMAT_ERR_INVALID;
   if (a->post_flags & ~(uint32_t)RMAT_POST_UNDIRECTED) return RMAT_ERR_UNSUPPORTED;
-  if (a->n_blocks == 0) return RMAT_OK;
+  if ((a->segments ? a->n_segments : a->n_blocks) == 0) return RMAT_OK;
   if (!a->out) return RMAT_ERR_INVALID;
+  const bool seg_mode = a->segments != nullptr;
   const uint64_t nblocks_all = (a->edge_count + a->block_size - 1) / a->block_size;
-  if (a->first_block > nblocks_all || a->n_blocks > nblocks_all - a->first_block)
+  if (!seg_mode && (a->first_block > nblocks_all || a->n_blocks > nblocks_all - a->first_block))
     return RMAT_ERR_INVALID;
+  if (seg_mode && a->kernel == RMAT_KERNEL_PACKED_SMEM) return RMAT_ERR_UNSUPPORTED;
   const rmat_table* t = a->table;
   DeviceGuard guard(t->device);
   if (!guard.ok) return RMAT_ERR_DEVICE;
@@ -521,9 +523,9 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
   if ((a->kernel == RMAT_KERNEL_PACKED_SMEM && !thread_ok) ||
       (a->kernel == RMAT_KERNEL_PACKED_GLOBAL && !cta_packed_ok))
     return RMAT_ERR_UNSUPPORTED;
-  if (a->kernel == RMAT_KERNEL_PACKED_SMEM ||
+  if (!seg_mode && (a->kernel == RMAT_KERNEL_PACKED_SMEM ||
       (a->kernel == RMAT_KERNEL_AUTO && thread_ok &&
-       ref_thread_per_block_wins(a->n_blocks, num_sms(t->device)))) {
+       ref_thread_per_block_wins(a->n_blocks, num_sms(t->device))))) {
     const uint64_t rows = std::min<uint64_t>(a->n_blocks * E, a->edge_count - a->first_block * E);
     const uint64_t G = a->out_width == 8 ? 2 : 4;
     const bool prefix = a->row_prefix || a->col_prefix || (E % G) != 0;
@@ -691,6 +693,21 @@ rmat_status rmat_naive_edges(const rmat_naive_args* a, int device, void* cuda_st
     rmat::k_naive<true><<<blocks, 256, 0, st>>>(g);
   else
     rmat::k_naive<false><<<blocks, 256, 0, st>>>(g);
+  return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+}
+
+rmat_status rmat_refstream_segment_depths(const rmat_table* t, uint64_t key0, uint64_t key1,
+                                          uint64_t word_begin, uint64_t L, uint64_t nseg,
+                                          uint64_t* sums, void* cuda_stream) {
+  if (!t || !sums || L == 0) return RMAT_ERR_INVALID;
+  if (nseg == 0) return RMAT_OK;
+  if (word_begin + nseg * L < word_begin) return RMAT_ERR_INVALID;
+  DeviceGuard guard(t->device);
+  if (!guard.ok) return RMAT_ERR_DEVICE;
+  const unsigned blocks = (unsigned)std::min<uint64_t>(nseg, (uint64_t)num_sms(t->device) * 8);
+  rmat::k_ref_segment_depths<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      generic_view(t), key0, key1, word_begin, L, nseg,
+      reinterpret_cast<unsigned long long*>(sums));
   return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
 }
 

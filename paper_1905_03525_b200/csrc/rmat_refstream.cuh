@@ -40,7 +40,59 @@ struct RefLaunch {
   uint64_t rpre, cpre;
   uint64_t w0;    // first word of every block stream (continuation after an earlier _emit)
   uint32_t post;  // RMAT_POST_UNDIRECTED: fused to_undirected
+  // Segment mode (segs != nullptr): "block" bi is segment segs[bi] of ONE long
+  // stream keyed [key0, seg_key1]; nf counts words from nf_origin.
+  const struct RefSeg* segs;
+  uint64_t seg_key1;
+  uint64_t nf_origin;
 };
+
+// One segment of a long reference stream, cut so that many CTAs share it: it
+// starts reading at word_begin, whose first bit is `skip` bits before the next
+// edge boundary; `lead` = k - skip zero bits are prepended so the stream's
+// edge grid lines up, and the edge they complete is dropped.  It emits the
+// `count` edges that start inside it (reading past its end to finish the
+// last), written from out_row on; the segment holding the stream's last edge
+// reports nf.
+struct RefSeg {
+  uint64_t word_begin;
+  uint64_t out_row;
+  uint64_t count;
+  uint32_t lead;
+  uint32_t report_nf;
+};
+
+struct RefBlock {
+  uint64_t key1, w0, count, out_row, origin;
+  uint32_t lead, drop;
+  bool report;
+};
+
+__device__ __forceinline__ RefBlock ref_block(const RefLaunch& g, uint64_t bi) {
+  RefBlock r;
+  if (g.segs) {
+    const RefSeg sg = g.segs[bi];
+    r.key1 = g.seg_key1;
+    r.w0 = sg.word_begin;
+    r.lead = sg.lead;
+    r.drop = sg.lead ? 1u : 0u;
+    r.count = sg.count + r.drop;
+    r.out_row = sg.out_row;
+    r.origin = g.nf_origin;
+    r.report = sg.report_nf != 0;
+  } else {
+    const uint64_t b = g.first_block + bi;
+    r.key1 = b;
+    r.w0 = g.w0;
+    r.lead = 0;
+    r.drop = 0;
+    r.count = min(g.B, g.m - b * g.B);
+    r.out_row = bi * g.B;
+    r.origin = g.w0;
+    r.report = true;
+  }
+  return r;
+}
 
 // one output edge, optionally canonicalised (max, min) (postprocess.py:26-35)
 template <bool OUT64>
@@ -84,20 +136,20 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
   __shared__ uint32_t s_carry_len;
 
   const uint32_t tid = threadIdx.x;
-  const uint64_t b = g.first_block + blockIdx.x;
-  const uint64_t count = min(g.B, g.m - b * g.B);
+  const RefBlock blk = ref_block(g, blockIdx.x);
+  const uint64_t count = blk.count;
   const uint32_t k = g.k;
   const uint32_t n = tab.n;
   const bool pow2 = (n & (n - 1)) == 0;
   const uint64_t kmask = lowmask64(k);
-  const uint64_t key1 = b;
+  const uint64_t key1 = blk.key1;
 
-  if (tid == 0) { s_carry_r = 0; s_carry_c = 0; s_carry_len = 0; }
+  if (tid == 0) { s_carry_r = 0; s_carry_c = 0; s_carry_len = blk.lead; }
   __syncthreads();
 
   uint64_t emitted = 0;  // edges of this block already written
   // word index of this chunk's first fragment; words before w0 get depth 0
-  uint64_t chunk_base = g.w0 & ~3ull;
+  uint64_t chunk_base = blk.w0 & ~3ull;
   uint64_t nf = 0;
   while (emitted < count) {
     // 1. draw + select 4 fragments per thread
@@ -111,7 +163,7 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
       const uint32_t hi = (uint32_t)(w >> 32);
       const uint32_t idx = pow2 ? (hi & (n - 1)) : (hi % n);
       const uint32_t e = ((uint32_t)w < __ldg(tab.T + idx)) ? idx : __ldg(tab.alias + idx);
-      dq[q] = chunk_base + 4 * tid + q < g.w0 ? 0u : __ldg(tab.depth + e);
+      dq[q] = chunk_base + 4 * tid + q < blk.w0 ? 0u : __ldg(tab.depth + e);
       s_r[4 * tid + q] = __ldg(tab.row + e);
       s_c[4 * tid + q] = __ldg(tab.col + e);
       dsum += dq[q];
@@ -175,9 +227,9 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
           ++s;
         }
       }
-      const uint64_t row = b * g.B + emitted + e - g.first_block * g.B;
-      ref_store<OUT64>(reinterpret_cast<char*>(g.out), row, (ur & kmask) | g.rpre,
-                       (uc & kmask) | g.cpre, g.post);
+      if (emitted + e >= blk.drop)
+        ref_store<OUT64>(reinterpret_cast<char*>(g.out), blk.out_row + emitted + e - blk.drop,
+                         (ur & kmask) | g.rpre, (uc & kmask) | g.cpre, g.post);
     }
     // 4. carry / nf (one thread), then advance
     if (tid == 0) {
@@ -190,9 +242,9 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
             const int mid = (l + h) >> 1;
             if (s_end[mid] >= used) h = mid; else l = mid + 1;
           }
-          nf = chunk_base + l + 1 - g.w0;
+          nf = chunk_base + l + 1 - blk.origin;
         } else {
-          nf = chunk_base - g.w0;  // finished inside the carry: no fragment of this chunk used
+          nf = chunk_base - blk.origin;  // finished inside the carry: no fragment of this chunk
         }
       } else {
         // keep bits [used, ltot)
@@ -228,7 +280,7 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
     chunk_base += kRefChunk;
     __syncthreads();
   }
-  if (tid == 0) {
+  if (tid == 0 && blk.report) {
     if (count == 0) nf = 0;
     if (g.samples_per_block) g.samples_per_block[blockIdx.x] = nf;
     if (g.samples_total) atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)nf);
@@ -280,12 +332,13 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
   const uint32_t kmagic = (uint32_t)((0x100000000ull + k - 1) / k);
 
   for (uint64_t bi = blockIdx.x; bi < n_blocks; bi += gridDim.x) {
-    const uint64_t b = g.first_block + bi;
-    const uint64_t count = min(g.B, g.m - b * g.B);
-    char* const outb = reinterpret_cast<char*>(g.out) + bi * g.B * (OUT64 ? 16 : 8);
-    if (tid == 0) { s_carry_r = 0; s_carry_c = 0; s_carry_len = 0; }
+    const RefBlock blk = ref_block(g, bi);
+    const uint64_t b = blk.key1;
+    const uint64_t count = blk.count;
+    char* const outb = reinterpret_cast<char*>(g.out);
+    if (tid == 0) { s_carry_r = 0; s_carry_c = 0; s_carry_len = blk.lead; }
     __syncthreads();
-    uint64_t emitted = 0, chunk_base = g.w0 & ~3ull;  // words before w0 get depth 0
+    uint64_t emitted = 0, chunk_base = blk.w0 & ~3ull;  // words before w0 get depth 0
     while (emitted < count) {
       // 1. draw + select 4 fragments per thread
       const uint64_t call = chunk_base / 4 + tid;  // numpy counter = call + 1
@@ -303,7 +356,7 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
         if ((uint32_t)sum <= fm) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
         const uint32_t sel = ge ? 0x4432u : 0x4410u;
         const uint32_t r = prmt_ref(aw.x, sel), c = prmt_ref(aw.y, sel);
-        dq[q] = chunk_base + 4 * tid + q < g.w0 ? 0u : prmt_ref(bw, 0x4440u + ge);
+        dq[q] = chunk_base + 4 * tid + q < blk.w0 ? 0u : prmt_ref(bw, 0x4440u + ge);
         rcq[q] = r | (c << 16);
         dsum += dq[q];
       }
@@ -421,16 +474,17 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
           }
           // nf (generator.py:255-257): one past the fragment holding the last
           // edge's last bit
-          if (final_chunk && j + 1 == avail) s_nf = chunk_base + sidx - g.w0;
-          const uint64_t row = emitted + j;
-          ref_store<OUT64>(outb, row, (ur & kmask) | g.rpre, (uc & kmask) | g.cpre, g.post);
+          if (final_chunk && j + 1 == avail) s_nf = chunk_base + sidx - blk.origin;
+          if (emitted + j >= blk.drop)
+            ref_store<OUT64>(outb, blk.out_row + emitted + j - blk.drop, (ur & kmask) | g.rpre,
+                             (uc & kmask) | g.cpre, g.post);
         }
       }
       emitted += avail;
       chunk_base += kRefPChunk;
       __syncthreads();
     }
-    if (tid == 0) {
+    if (tid == 0 && blk.report) {
       const uint64_t nf = s_nf;
       if (g.samples_per_block) g.samples_per_block[bi] = nf;
       if (g.samples_total) atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)nf);
@@ -482,10 +536,12 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
   const uint32_t kmagic = (uint32_t)((0x100000000ull + k - 1) / k);
 
   for (uint64_t bi = blockIdx.x; bi < n_blocks; bi += gridDim.x) {
-    const uint64_t b = g.first_block + bi;
-    const uint64_t count = min(g.B, g.m - b * g.B);
-    char* const outb = reinterpret_cast<char*>(g.out) + bi * g.B * (OUT64 ? 16 : 8);
-    uint64_t emitted = 0, chunk_base = g.w0 & ~3ull;  // words before w0 get depth 0
+    const RefBlock blk = ref_block(g, bi);
+    const uint64_t b = blk.key1;
+    const uint64_t count = blk.count;
+    char* const outb = reinterpret_cast<char*>(g.out);
+    if (tid == 0) s_carry_len = blk.lead;  // zero bits aligning a mid-stream segment
+    uint64_t emitted = 0, chunk_base = blk.w0 & ~3ull;  // words before w0 get depth 0
     while (emitted < count) {
       // 1. draw + select 4 fragments per thread
       const uint64_t call = chunk_base / 4 + tid;  // numpy counter = call + 1
@@ -504,7 +560,7 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
         const uint32_t sel = ge ? 0x4432u : 0x4410u;
         rq[q] = prmt_ref(aw.x, sel);
         cq[q] = prmt_ref(aw.y, sel);
-        dq[q] = chunk_base + 4 * tid + q < g.w0 ? 0u : prmt_ref(bw, 0x4440u + ge);
+        dq[q] = chunk_base + 4 * tid + q < blk.w0 ? 0u : prmt_ref(bw, 0x4440u + ge);
         dsum += dq[q];
       }
       // 2. CTA exclusive scan of the depths behind the carried bits
@@ -560,7 +616,7 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
           }
           // nf (generator.py:255-257): one past the fragment holding the last needed bit
           if (final_chunk && start < target && target <= end)
-            s_nf = chunk_base + 4 * tid + q + 1 - g.w0;
+            s_nf = chunk_base + 4 * tid + q + 1 - blk.origin;
         }
         start = end;
       }
@@ -571,7 +627,9 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
         s_er[e] = 0;
         s_ec[e] = 0;
         if (e < avail) {
-          ref_store<OUT64>(outb, emitted + e, (uint64_t)(er & kmask32) | g.rpre,
+          if (emitted + e >= blk.drop)
+            ref_store<OUT64>(outb, blk.out_row + emitted + e - blk.drop,
+                             (uint64_t)(er & kmask32) | g.rpre,
                            (uint64_t)(ec & kmask32) | g.cpre, g.post);
         } else if (e == nfull && !final_chunk) {
           // partial edge: its bits sit at the top of the k-bit word
@@ -585,9 +643,12 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
       __syncthreads();
     }
     if (tid == 0) {
-      const uint64_t nf = s_nf;
-      if (g.samples_per_block) g.samples_per_block[bi] = nf;
-      if (g.samples_total) atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)nf);
+      if (blk.report) {
+        const uint64_t nf = s_nf;
+        if (g.samples_per_block) g.samples_per_block[bi] = nf;
+        if (g.samples_total)
+          atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)nf);
+      }
       s_carry_r = 0; s_carry_c = 0; s_carry_len = 0;
     }
     __syncthreads();
@@ -624,6 +685,41 @@ k_ref_depth_sum(const GenericTab tab, uint64_t key0, uint64_t key1, uint64_t w_b
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
 }
 
+// Per-segment depth sums of one reference stream: segment s covers words
+// [w_begin + s*L, w_begin + (s+1)*L); one CTA per segment (grid-stride).
+// The host scans them into each segment's first bit offset (segment mode).
+__global__ void __launch_bounds__(256)
+k_ref_segment_depths(const GenericTab tab, uint64_t key0, uint64_t key1, uint64_t w_begin,
+                     uint64_t L, uint64_t nseg, unsigned long long* sums) {
+  __shared__ unsigned long long s_acc;
+  const uint32_t n = tab.n;
+  const bool pow2 = (n & (n - 1)) == 0;
+  for (uint64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    if (threadIdx.x == 0) s_acc = 0;
+    __syncthreads();
+    const uint64_t lo = w_begin + sg * L, hi = lo + L;
+    uint64_t acc = 0;
+    for (uint64_t c = lo / 4 + threadIdx.x; c < (hi + 3) / 4; c += blockDim.x) {
+      const u64x4 w4 = philox4x64_10(c + 1, c + 1 == 0 ? 1 : 0, 0, 0, key0, key1);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t i = 4 * c + q;
+        const uint64_t w = q == 0 ? w4.x : q == 1 ? w4.y : q == 2 ? w4.z : w4.w;
+        const uint32_t hw = (uint32_t)(w >> 32);
+        const uint32_t idx = pow2 ? (hw & (n - 1)) : (hw % n);
+        const uint32_t e = ((uint32_t)w < __ldg(tab.T + idx)) ? idx : __ldg(tab.alias + idx);
+        if (i >= lo && i < hi) acc += __ldg(tab.depth + e);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_acc, (unsigned long long)acc);
+    __syncthreads();
+    if (threadIdx.x == 0) sums[sg] = s_acc;
+    __syncthreads();
+  }
+}
+
 inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
                                     const rmat_refstream_args& a, cudaStream_t st,
                                     const PackedTab* packed = nullptr, int sms = 148,
@@ -642,7 +738,10 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
   g.cpre = a.col_prefix;
   g.w0 = a.word_offset;
   g.post = a.post_flags;
-  const uint64_t nb = a.n_blocks;
+  g.segs = reinterpret_cast<const RefSeg*>(a.segments);
+  g.seg_key1 = a.segment_stream;
+  g.nf_origin = a.word_offset;
+  const uint64_t nb = a.segments ? a.n_segments : a.n_blocks;
   if (packed && a.k <= 32 && dmax <= a.k) {
     // scatter variant: buckets + this chunk's edge words (carry < k bits)
     const uint32_t max_edges = (uint32_t)((a.k - 1 + (uint64_t)kRefPChunk * dmax) / a.k + 1);
@@ -675,8 +774,12 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
   for (uint64_t done = 0; done < nb;) {
     const uint64_t cnt = std::min<uint64_t>(nb - done, 1u << 30);
     RefLaunch gg = g;
-    gg.first_block = g.first_block + done;
-    gg.out = (char*)g.out + (size_t)done * g.B * (a.out_width == 8 ? 16 : 8);
+    if (g.segs) {
+      gg.segs = g.segs + done;  // rows are absolute in segment mode
+    } else {
+      gg.first_block = g.first_block + done;
+      gg.out = (char*)g.out + (size_t)done * g.B * (a.out_width == 8 ? 16 : 8);
+    }
     if (gg.samples_per_block) gg.samples_per_block += done;
     if (a.out_width == 8)
       k_refstream<true><<<(unsigned)cnt, kRefThreads, 0, st>>>(tab, gg);

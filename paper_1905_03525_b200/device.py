@@ -139,6 +139,19 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
     import torch
 
     assert out.device == dt.device and out.is_contiguous()
+    if (kernel == N.KERNEL_AUTO and 0 < n_blocks <= LONG_STREAM_MAX_BLOCKS
+            and min(block_size, edge_count - first_block * block_size) >= LONG_STREAM_EDGES
+            and samples_per_block is None):
+        # few long blocks: cut each into segments that run on many CTAs
+        for i in range(n_blocks):
+            b = first_block + i
+            cnt = min(block_size, edge_count - b * block_size)
+            launch_refstream_segments(dt, k, (seed ^ domain) & _M64, b, cnt,
+                                      out[i * block_size:i * block_size + cnt],
+                                      word_offset=word_offset, samples_total=samples_total,
+                                      row_prefix=row_prefix, col_prefix=col_prefix,
+                                      post_flags=post_flags)
+        return
     args = N.RefArgs(
         table=dt.handle, k=k, out_width=out.element_size(), seed=seed & (2**64 - 1),
         domain=domain, block_size=block_size, edge_count=edge_count, first_block=first_block,
@@ -151,6 +164,68 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
     with torch.cuda.device(dt.device):
         N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), _stream_ptr(dt.device)),
                 "rmat_generate_refstream")
+
+
+#: a launch of at most this many reference blocks of at least LONG_STREAM_EDGES
+#: edges each runs every block in segment mode (one CTA per ~2^16 words)
+LONG_STREAM_MAX_BLOCKS = 16
+LONG_STREAM_EDGES = 1 << 20
+SEGMENT_WORDS = 1 << 16
+_M64 = (1 << 64) - 1
+
+
+def launch_refstream_segments(dt: DeviceTable, k: int, key0: int, key1: int, count: int, out, *,
+                              word_offset: int = 0, samples_total=None, row_prefix: int = 0,
+                              col_prefix: int = 0, post_flags: int = 0,
+                              words_per_segment: int = SEGMENT_WORDS) -> None:
+    """`count` edges of ONE reference stream keyed [key0, key1] from word `word_offset`,
+    spread over many CTAs: per-segment depth sums (device) -> host scan -> a
+    segment table (rmat_ref_segment) -> one segment-mode rmat_generate_refstream."""
+    import torch
+
+    if count == 0:
+        return
+    L = int(words_per_segment)
+    need = count * k
+    mean = float(dt.table.mean_depth)
+    nseg = int(need / mean / L * 1.02) + 2
+    with torch.cuda.device(dt.device):
+        while True:
+            sums = torch.empty(nseg, dtype=torch.int64, device=dt.device)
+            N.check(N.lib().rmat_refstream_segment_depths(
+                dt.handle, key0 & _M64, key1 & _M64, word_offset, L, nseg, sums.data_ptr(),
+                _stream_ptr(dt.device)), "rmat_refstream_segment_depths")
+            cs = np.cumsum(sums.cpu().numpy().astype(np.uint64), dtype=np.uint64)
+            if int(cs[-1]) >= need:
+                break
+            nseg = int(nseg * 1.25) + 2
+        last = int(np.searchsorted(cs, np.uint64(need), side="left"))  # holds bit need-1
+        off = np.concatenate([np.zeros(1, dtype=np.uint64), cs[:last]])  # first bit of each segment
+        kk = np.uint64(k)
+        e0 = (off + kk - np.uint64(1)) // kk
+        e1 = np.minimum(np.concatenate([e0[1:], [np.uint64(count)]]), np.uint64(count))
+        e1[-1] = count
+        skip = e0 * kk - off
+        segs = np.zeros(last + 1, dtype=[("word_begin", "<u8"), ("out_row", "<u8"),
+                                          ("count", "<u8"), ("lead", "<u4"),
+                                          ("report_nf", "<u4")])
+        segs["word_begin"] = word_offset + np.arange(last + 1, dtype=np.uint64) * np.uint64(L)
+        segs["out_row"] = e0
+        segs["count"] = e1 - e0
+        segs["lead"] = np.where(skip > 0, kk - skip, np.uint64(0)).astype(np.uint32)
+        segs["report_nf"][-1] = 1
+        dseg = torch.from_numpy(segs.view(np.uint8)).to(dt.device)
+        args = N.RefArgs(
+            table=dt.handle, k=k, out_width=out.element_size(), seed=key0 & _M64, domain=0,
+            block_size=1, edge_count=1, first_block=0, n_blocks=0, out=out.data_ptr(),
+            samples_per_block=None,
+            samples_total=samples_total.data_ptr() if samples_total is not None else None,
+            row_prefix=row_prefix, col_prefix=col_prefix, word_offset=word_offset,
+            post_flags=post_flags, kernel=N.KERNEL_AUTO, segments=dseg.data_ptr(),
+            n_segments=last + 1, segment_stream=key1 & _M64)
+        N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), _stream_ptr(dt.device)),
+                "rmat_generate_refstream (segments)")
+        torch.cuda.current_stream(dt.device).synchronize()  # dseg must outlive the launch
 
 
 def replay_words(dt: DeviceTable, seed: int, domain: int, sid: int, count: int, start: int = 0):

@@ -126,6 +126,7 @@ def test_ctypes_structs_match_the_header(tmp_path):
         "rmat_segment": N.Segment, "rmat_gen_args": N.GenArgs,
         "rmat_refstream_args": N.RefArgs, "rmat_post_args": N.PostArgs,
         "rmat_dedup_args": N.DedupArgs, "rmat_naive_args": N.NaiveArgs,
+        "rmat_ref_segment": N.RefSegment,
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"',
              "int main(void) {", 'printf("{");']

@@ -231,3 +231,30 @@ def test_reference_mode_thread_kernel_undirected(cuda):
     a, _, _ = generate_shard(GenConfig(**base, undirected=True), kernel=N.KERNEL_PACKED_SMEM)
     b, _, _ = generate_shard(GenConfig(**base, undirected=True), kernel=N.KERNEL_PACKED_GLOBAL)
     assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+
+
+@pytest.mark.parametrize("tag,k,count,L,w0", [
+    ("v16384", 28, 200_000, 64, 0),      # scatter kernel, many tiny segments
+    ("v16384", 28, 200_000, 4096, 13),   # unaligned stream start (continuation)
+    ("v1024", 33, 150_000, 1000, 5),     # packed walk kernel (k > 32)
+    ("v253", 20, 100_000, 777, 2),       # generic kernel (non power-of-two table)
+    ("f2", 9, 300_000, 5, 0),            # fixed-depth table, 5-word segments
+    ("v1024", 3, 50_000, 64, 1),         # k below the max depth
+])
+def test_reference_stream_segment_mode(cuda, tag, k, count, L, w0):
+    """One long reference stream cut into segments on many CTAs == the sequential stream."""
+    from paper_1905_03525_b200.device import device_table, launch_refstream_segments
+    from paper_1905_03525_b200.generator import edge_dtype
+
+    dt = device_table(table_for(tag), cuda)
+    key0, key1 = 0x1234567890ABCDEF, 77
+    out = torch.empty((count, 2), dtype=edge_dtype(k), device=cuda)
+    tot = torch.zeros(1, dtype=torch.int64, device=cuda)
+    rp, cp = (1 << 40, 3 << 40) if k <= 33 and edge_dtype(k) == torch.uint64 else (0, 0)
+    launch_refstream_segments(dt, k, key0, key1, count, out, word_offset=w0, samples_total=tot,
+                              row_prefix=rp, col_prefix=cp, words_per_segment=L)
+    want, nf = oracle.ref_stream_from(oracle_table(tag), k, count, key0, key1, w0, rp, cp)
+    got = out.view(torch.int32 if k <= 32 else torch.int64).cpu().numpy()
+    got = got.view(np.uint32).astype(np.uint64) if k <= 32 else got.view(np.uint64)
+    assert (got == want).all()
+    assert int(tot.item()) == nf
