@@ -502,7 +502,9 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
 // The partial edge after the chunk's last complete one stays positioned in
 // its word and becomes edge 0 of the next chunk (the carry).
 // ---------------------------------------------------------------------------
-template <bool OUT64>
+// W: edge word type -- uint32_t for k <= 32, unsigned long long for k <= 64 (the
+// k = 33 tiles of C4); smem atomicOr exists for both widths.
+template <bool OUT64, typename W>
 __global__ void __launch_bounds__(kRefPThreads, 1)
 k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
                     uint32_t max_edges) {
@@ -519,10 +521,11 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
   }
   const uint2* sA = reinterpret_cast<const uint2*>(smem);
   const uint32_t* sB = reinterpret_cast<const uint32_t*>(smem + abytes);
-  uint32_t* s_er = reinterpret_cast<uint32_t*>(smem + abytes + bbytes);  // row words of the chunk
-  uint32_t* s_ec = s_er + max_edges;                                     // column words
+  W* s_er = reinterpret_cast<W*>(smem + abytes + bbytes);  // row words of the chunk
+  W* s_ec = s_er + max_edges;                              // column words
   __shared__ uint32_t s_warp[kRefPThreads / 32];
-  __shared__ uint32_t s_total, s_carry_r, s_carry_c, s_carry_len;
+  __shared__ uint32_t s_total, s_carry_len;
+  __shared__ W s_carry_r, s_carry_c;
   __shared__ uint64_t s_nf;
   for (uint32_t i = threadIdx.x; i < 2 * max_edges; i += kRefPThreads) s_er[i] = 0;
   if (threadIdx.x == 0) { s_carry_r = 0; s_carry_c = 0; s_carry_len = 0; }
@@ -530,7 +533,8 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
 
   const uint32_t tid = threadIdx.x;
   const uint32_t k = g.k;
-  const uint32_t kmask32 = k >= 32 ? 0xFFFFFFFFu : (1u << k) - 1u;
+  constexpr uint32_t WB = sizeof(W) * 8;
+  const W kmaskw = k >= WB ? ~(W)0 : (((W)1 << k) - 1);
   const uint32_t fm = tab.fm, one = tab.one, nmask = n - 1;
   // ceil(2^32 / k); floor(x / k) = umulhi(x + k, kmagic) - 1 for the < 2^17 offsets here
   const uint32_t kmagic = (uint32_t)((0x100000000ull + k - 1) / k);
@@ -603,15 +607,15 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
           const uint32_t jend = (j + 1) * k;  // end of edge j
           if (end <= jend) {
             const uint32_t sh = jend - end;
-            atomicOr(s_er + j, rq[q] << sh);
-            atomicOr(s_ec + j, cq[q] << sh);
+            atomicOr(s_er + j, (W)rq[q] << sh);
+            atomicOr(s_ec + j, (W)cq[q] << sh);
           } else {  // straddles into edge j + 1 (depth <= k: no further)
             const uint32_t over = end - jend;
-            atomicOr(s_er + j, rq[q] >> over);
-            atomicOr(s_ec + j, cq[q] >> over);
-            if (k - over < 32) {
-              atomicOr(s_er + j + 1, rq[q] << (k - over));
-              atomicOr(s_ec + j + 1, cq[q] << (k - over));
+            atomicOr(s_er + j, (W)(rq[q] >> over));
+            atomicOr(s_ec + j, (W)(cq[q] >> over));
+            if (k - over < WB) {
+              atomicOr(s_er + j + 1, (W)rq[q] << (k - over));
+              atomicOr(s_ec + j + 1, (W)cq[q] << (k - over));
             }
           }
           // nf (generator.py:255-257): one past the fragment holding the last needed bit
@@ -623,14 +627,14 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
       __syncthreads();
       // 4. coalesced write-out; clear the words for the next chunk; keep the carry
       for (uint32_t e = tid; e <= nfull; e += kRefPThreads) {
-        const uint32_t er = s_er[e], ec = s_ec[e];
+        const W er = s_er[e], ec = s_ec[e];
         s_er[e] = 0;
         s_ec[e] = 0;
         if (e < avail) {
           if (emitted + e >= blk.drop)
             ref_store<OUT64>(outb, blk.out_row + emitted + e - blk.drop,
-                             (uint64_t)(er & kmask32) | g.rpre,
-                           (uint64_t)(ec & kmask32) | g.cpre, g.post);
+                             (uint64_t)(er & kmaskw) | g.rpre,
+                           (uint64_t)(ec & kmaskw) | g.cpre, g.post);
         } else if (e == nfull && !final_chunk) {
           // partial edge: its bits sit at the top of the k-bit word
           s_carry_r = er;
@@ -742,12 +746,17 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
   g.seg_key1 = a.segment_stream;
   g.nf_origin = a.word_offset;
   const uint64_t nb = a.segments ? a.n_segments : a.n_blocks;
-  if (packed && a.k <= 32 && dmax <= a.k) {
+  // (64-bit edge words for k = 33 measured slower than the walk kernel: 1.44e10
+  // vs 1.57e10 edges/s on C4 tiles -- 64-bit shared atomics)
+  if (packed && dmax <= a.k && a.k <= 32) {
     // scatter variant: buckets + this chunk's edge words (carry < k bits)
+    const bool w64 = false;
     const uint32_t max_edges = (uint32_t)((a.k - 1 + (uint64_t)kRefPChunk * dmax) / a.k + 1);
-    const size_t smem = (size_t)packed->n * 12 + (size_t)max_edges * 8;
+    const size_t smem = (size_t)packed->n * 12 + (size_t)max_edges * 2 * (w64 ? 8 : 4);
     if (smem <= packed_smem_limit) {
-      auto kern = a.out_width == 8 ? k_refstream_scatter<true> : k_refstream_scatter<false>;
+      auto kern = w64 ? k_refstream_scatter<true, unsigned long long>
+                      : (a.out_width == 8 ? k_refstream_scatter<true, uint32_t>
+                                          : k_refstream_scatter<false, uint32_t>);
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess)
         return RMAT_ERR_CUDA;
