@@ -393,10 +393,18 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
 
   const bool out64 = a->out_width == 8;
   const bool count = a->samples_total || a->samples_per_stream;
+  // The packed kernels store whole 32-byte sectors relative to `out`: address
+  // rows from the sector below `out` (rows before the first one are never
+  // written: partial head sectors go slot by slot).
+  const uint64_t eb = 2ull * a->out_width;
+  const uintptr_t mis = reinterpret_cast<uintptr_t>(a->out) & 31;
+  if (mis % eb) return RMAT_ERR_INVALID;  // not even row-aligned
+  const uint64_t row_shift = mis / eb;
+  void* const out_base = reinterpret_cast<char*>(a->out) - mis;
   // The non-PREFIX fast path assumes every stream starts on a 32-byte sector;
   // anything else (tiles, odd stream lengths) takes the general variant.
   const uint64_t G = out64 ? 2 : 4;
-  bool aligned = (E % G) == 0;
+  bool aligned = (E % G) == 0 && row_shift == 0;
   for (uint32_t i = 0; i < a->n_segments; ++i) aligned = aligned && (a->segments[i].out_row % G) == 0;
   prefix = prefix || !aligned;
   int kernel = a->kernel;
@@ -422,7 +430,7 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
     g.k1 = (uint32_t)(key >> 32);
     rmat::philox4x32_key_schedule(g.k0, g.k1, g.rk);
     g.E = E;
-    g.out = a->out;
+    g.out = out_base;
     g.samples_total = a->samples_total;
     g.samples_per_stream = a->samples_per_stream;
     g.post = a->post_flags;
@@ -433,7 +441,7 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
       rmat::SegDev& dv = g.segs[nseg++];
       dv.sid_base = s.sid_base;
       dv.edge_count = s.edge_count;
-      dv.out_row = s.out_row;
+      dv.out_row = s.out_row + row_shift;
       dv.row_prefix = s.row_prefix;
       dv.col_prefix = s.col_prefix;
       dv.stream_begin = stream_begin;
@@ -507,7 +515,8 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
   const uint64_t nblocks_all = (a->edge_count + a->block_size - 1) / a->block_size;
   if (!seg_mode && (a->first_block > nblocks_all || a->n_blocks > nblocks_all - a->first_block))
     return RMAT_ERR_INVALID;
-  if (seg_mode && a->kernel == RMAT_KERNEL_PACKED_SMEM) return RMAT_ERR_UNSUPPORTED;
+  if (seg_mode && a->kernel == RMAT_KERNEL_PACKED_SMEM && (a->word_offset & 3))
+    return RMAT_ERR_UNSUPPORTED;  // per-thread segments start on whole Philox calls
   const rmat_table* t = a->table;
   DeviceGuard guard(t->device);
   if (!guard.ok) return RMAT_ERR_DEVICE;
@@ -520,6 +529,34 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
                          a->k <= 33 && a->word_offset == 0 &&
                          (double)E * a->k / t->dmin < 17179869184.0;
   const bool cta_packed_ok = t->fb == 16 && t->scheme_p;
+  if (seg_mode && a->kernel == RMAT_KERNEL_PACKED_SMEM) {
+    // segments of one long stream, one thread each (k_packed<..., REF>)
+    if (!(t->fb == 16 && t->scheme_p && t->packed_smem && t->dmax <= a->k && a->k <= 33))
+      return RMAT_ERR_UNSUPPORTED;
+    const uint64_t key = a->seed ^ a->domain;
+    rmat::GenLaunch g;
+    std::memset(&g, 0, sizeof g);
+    g.k = a->k;
+    g.k0 = (uint32_t)key;
+    g.k1 = (uint32_t)(key >> 32);
+    g.E = 1;
+    const uint64_t eb = 2ull * a->out_width;
+    const uintptr_t mis = reinterpret_cast<uintptr_t>(a->out) & 31;  // see rmat_generate
+    if (mis % eb) return RMAT_ERR_INVALID;
+    g.out = reinterpret_cast<char*>(a->out) - mis;
+    g.rseg_row_shift = mis / eb;
+    g.samples_total = a->samples_total;
+    g.post = a->post_flags;
+    g.rsegs = reinterpret_cast<const rmat::RefSeg*>(a->segments);
+    g.rseg_key1 = a->segment_stream;
+    g.nf_origin = a->word_offset;
+    g.rseg_rpre = a->row_prefix;
+    g.rseg_cpre = a->col_prefix;
+    g.total_streams = a->n_segments;
+    return launch_ref_thread(t, g, a->out_width == 8, /*prefix=*/true,
+                             a->samples_total != nullptr,
+                             reinterpret_cast<cudaStream_t>(cuda_stream));
+  }
   if ((a->kernel == RMAT_KERNEL_PACKED_SMEM && !thread_ok) ||
       (a->kernel == RMAT_KERNEL_PACKED_GLOBAL && !cta_packed_ok))
     return RMAT_ERR_UNSUPPORTED;
@@ -528,7 +565,11 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
        ref_thread_per_block_wins(a->n_blocks, num_sms(t->device))))) {
     const uint64_t rows = std::min<uint64_t>(a->n_blocks * E, a->edge_count - a->first_block * E);
     const uint64_t G = a->out_width == 8 ? 2 : 4;
-    const bool prefix = a->row_prefix || a->col_prefix || (E % G) != 0;
+    const uint64_t eb = 2ull * a->out_width;
+    const uintptr_t mis = reinterpret_cast<uintptr_t>(a->out) & 31;  // see rmat_generate
+    if (mis % eb) return RMAT_ERR_INVALID;
+    const uint64_t row_shift = mis / eb;
+    const bool prefix = a->row_prefix || a->col_prefix || (E % G) != 0 || row_shift != 0;
     const bool count = a->samples_total || a->samples_per_block;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
     const uint64_t key = a->seed ^ a->domain;
@@ -540,7 +581,7 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
       g.k0 = (uint32_t)key;
       g.k1 = (uint32_t)(key >> 32);
       g.E = E;
-      g.out = a->out;
+      g.out = reinterpret_cast<char*>(a->out) - mis;
       g.samples_total = a->samples_total;
       g.samples_per_stream = a->samples_per_block ? a->samples_per_block + done : nullptr;
       g.post = a->post_flags;
@@ -548,7 +589,7 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
       rmat::SegDev& dv = g.segs[0];
       dv.sid_base = a->first_block + done;
       dv.edge_count = std::min<uint64_t>(nb * E, rows - done * E);
-      dv.out_row = done * E;
+      dv.out_row = done * E + row_shift;
       dv.row_prefix = a->row_prefix;
       dv.col_prefix = a->col_prefix;
       dv.stream_begin = 0;

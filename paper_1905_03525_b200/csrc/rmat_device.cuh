@@ -55,6 +55,21 @@ struct GenericTab {
   uint32_t lg;
 };
 
+// One segment of a long reference stream (rmat_ref_segment), cut so that many
+// CTAs / threads share it: it starts reading at word_begin, whose first bit is
+// `skip` bits before the next edge boundary; `lead` = k - skip zero bits are
+// prepended so the stream's edge grid lines up, and the edge they complete is
+// dropped.  It emits the `count` edges that start inside it (reading past its
+// end to finish the last), written from out_row on; the segment holding the
+// stream's last edge reports nf.
+struct RefSeg {
+  uint64_t word_begin;
+  uint64_t out_row;
+  uint64_t count;
+  uint32_t lead;
+  uint32_t report_nf;
+};
+
 struct GenLaunch {
   uint32_t k;           // bits per endpoint emitted by the stream
   uint32_t k0, k1;      // Philox key = seed ^ domain
@@ -66,6 +81,10 @@ struct GenLaunch {
   uint64_t* samples_total;
   uint64_t* samples_per_stream;
   uint32_t post;        // RMAT_POST_UNDIRECTED: fused to_undirected
+  // REF segment mode: stream s = rsegs[s] of one reference stream keyed
+  // [k1:k0, rseg_key1]; nf counted from word nf_origin; one row/col prefix.
+  const RefSeg* rsegs;
+  uint64_t rseg_key1, nf_origin, rseg_rpre, rseg_cpre, rseg_row_shift;
   SegDev segs[kMaxSegsPerLaunch];
 };
 

@@ -47,6 +47,11 @@ struct StreamPos {
   uint64_t row;       // first output row
   uint64_t rpre, cpre;
   uint32_t k0, k1;    // segment key
+  uint64_t wcall;     // REF: first Philox call of the stream (word_begin / 4)
+  uint64_t nf_base;   // REF: nf offset (4 wcall - origin)
+  uint32_t lead;      // REF segments: zero bits prepended to align the edge grid
+  uint32_t drop;      // 1: the first edge (completed by the lead bits) is not output
+  bool report;        // add this stream's nf to the sample counters
   bool valid;
 };
 
@@ -54,6 +59,27 @@ __device__ __forceinline__ StreamPos open_stream(const GenLaunch& g, uint64_t s)
   StreamPos p;
   p.valid = s < g.total_streams;
   if (!p.valid) return p;
+  p.wcall = 0;
+  p.nf_base = 0;
+  p.lead = 0;
+  p.drop = 0;
+  p.report = true;
+  if (g.rsegs) {
+    const RefSeg sg = g.rsegs[s];
+    p.sid = g.rseg_key1;
+    p.lead = sg.lead;
+    p.drop = sg.lead ? 1u : 0u;
+    p.left = sg.count + p.drop;
+    p.row = sg.out_row - p.drop + g.rseg_row_shift;
+    p.rpre = g.rseg_rpre;
+    p.cpre = g.rseg_cpre;
+    p.k0 = g.k0;
+    p.k1 = g.k1;
+    p.wcall = sg.word_begin >> 2;  // the host aligns segment starts to whole calls
+    p.nf_base = (sg.word_begin & ~3ull) - g.nf_origin;
+    p.report = sg.report_nf != 0;
+    return p;
+  }
   const SegDev& sg = g.segs[find_segment(g, s)];
   uint64_t j = s - sg.stream_begin;
   uint64_t first = j * g.E;
@@ -332,7 +358,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   PhiloxPre pre{};
   if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
   uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
-  uint32_t cur_r = 0, cur_c = 0, f = 0;
+  uint32_t cur_r = 0, cur_c = 0, f = p.lead;
   uint64_t total_nf = 0;
   uint32_t ebits = 0;                // COUNT: samples of the current call that produced an edge
   // Output bookkeeping.  stage + roff = ring slot of the next edge (roff =
@@ -346,6 +372,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   uint32_t half = roff / (G * STRIDE);
   uint32_t lo = roff / STRIDE & (G - 1);
   L += lo;  // count the head's missing slots as already "staged"
+  lo += p.drop;  // a dropped first edge is staged but never flushed (lo may reach G)
   char* gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
   auto staged = [&]() { return ((roff / STRIDE) - half * G) & (R - 1); };
 
@@ -361,7 +388,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     Batch q;
     if constexpr (REF) {
       // numpy counter = call + 1; key = [segment key, block]
-      const u64x4 w4 = philox4x64_10((uint64_t)jj + 1, 0, 0, 0,
+      const u64x4 w4 = philox4x64_10(p.wcall + jj + 1, 0, 0, 0,
                                      ((uint64_t)p.k1 << 32) | p.k0, p.sid);
       const uint64_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
@@ -565,21 +592,24 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       if (COUNT) {
         // nf (generator.py:255-257): the highest sample of call j-1 that
         // produced an edge this stream needed.
-        const uint64_t nf = 4ull * (j - 1) + (32 - __clz(ebits));
-        total_nf += nf;
-        if (g.samples_per_stream) g.samples_per_stream[s] = nf;
+        const uint64_t nf = 4ull * (j - 1) + (32 - __clz(ebits)) + p.nf_base;
+        if (p.report) {
+          total_nf += nf;
+          if (g.samples_per_stream) g.samples_per_stream[s] = nf;
+        }
       }
       s += T;
       p = open_stream(g, s);
       if (!p.valid) break;
       stream_keys();
       if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
-      j = 0; cur_r = cur_c = f = 0;
+      j = 0; cur_r = cur_c = 0; f = p.lead;
       L = (uint32_t)p.left;
       roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
       half = roff / (G * STRIDE);
       lo = roff / STRIDE & (G - 1);
       L += lo;
+      lo += p.drop;
       gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
       continue;
     }

@@ -47,21 +47,6 @@ struct RefLaunch {
   uint64_t nf_origin;
 };
 
-// One segment of a long reference stream, cut so that many CTAs share it: it
-// starts reading at word_begin, whose first bit is `skip` bits before the next
-// edge boundary; `lead` = k - skip zero bits are prepended so the stream's
-// edge grid lines up, and the edge they complete is dropped.  It emits the
-// `count` edges that start inside it (reading past its end to finish the
-// last), written from out_row on; the segment holding the stream's last edge
-// reports nf.
-struct RefSeg {
-  uint64_t word_begin;
-  uint64_t out_row;
-  uint64_t count;
-  uint32_t lead;
-  uint32_t report_nf;
-};
-
 struct RefBlock {
   uint64_t key1, w0, count, out_row, origin;
   uint32_t lead, drop;

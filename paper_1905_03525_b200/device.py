@@ -169,15 +169,16 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
 #: a launch of at most this many reference blocks of at least LONG_STREAM_EDGES
 #: edges each runs every block in segment mode (one CTA per ~2^16 words)
 LONG_STREAM_MAX_BLOCKS = 16
-LONG_STREAM_EDGES = 1 << 20
-SEGMENT_WORDS = 1 << 16
+LONG_STREAM_EDGES = 1 << 15
+SEGMENT_WORDS = 1 << 18         # CTA per segment (tools/seg_probe2.py)
+THREAD_SEGMENT_WORDS = 1 << 14  # thread per segment
 _M64 = (1 << 64) - 1
 
 
 def launch_refstream_segments(dt: DeviceTable, k: int, key0: int, key1: int, count: int, out, *,
                               word_offset: int = 0, samples_total=None, row_prefix: int = 0,
                               col_prefix: int = 0, post_flags: int = 0,
-                              words_per_segment: int = SEGMENT_WORDS) -> None:
+                              words_per_segment: int | None = None, mode: str = "auto") -> None:
     """`count` edges of ONE reference stream keyed [key0, key1] from word `word_offset`,
     spread over many CTAs: per-segment depth sums (device) -> host scan -> a
     segment table (rmat_ref_segment) -> one segment-mode rmat_generate_refstream."""
@@ -185,9 +186,30 @@ def launch_refstream_segments(dt: DeviceTable, k: int, key0: int, key1: int, cou
 
     if count == 0:
         return
-    L = int(words_per_segment)
+    info = dt.info
+    # one thread per segment (the fast path's kernel on numpy words) when the table
+    # and k allow it: small segments so that a single stream fills the GPU
+    eligible = (info.packed_width == 16 and info.scheme_p and info.packed_smem
+                and info.max_depth <= k <= 33 and word_offset % 4 == 0)
+    if mode not in ("auto", "thread", "cta"):
+        raise ValueError(f"mode must be auto, thread or cta, got {mode!r}")
+    thread = mode == "thread" or (mode == "auto" and eligible)
     need = count * k
     mean = float(dt.table.mean_depth)
+    if words_per_segment:
+        L = int(words_per_segment)
+    elif thread:
+        # a segment is one thread's sequential work: long enough to amortise the
+        # per-stream setup (2^14 words measured best), short enough that the
+        # stream still spreads over ~2 waves of the GPU's threads
+        threads = 2 * 512 * torch.cuda.get_device_properties(dt.device).multi_processor_count
+        L = THREAD_SEGMENT_WORDS
+        while L > 1024 and need / mean / L < threads:
+            L //= 2
+    else:
+        L = SEGMENT_WORDS
+    if thread and L % 4:
+        raise ValueError("thread-per-segment mode needs whole Philox calls per segment")
     nseg = int(need / mean / L * 1.02) + 2
     with torch.cuda.device(dt.device):
         while True:
@@ -221,11 +243,13 @@ def launch_refstream_segments(dt: DeviceTable, k: int, key0: int, key1: int, cou
             samples_per_block=None,
             samples_total=samples_total.data_ptr() if samples_total is not None else None,
             row_prefix=row_prefix, col_prefix=col_prefix, word_offset=word_offset,
-            post_flags=post_flags, kernel=N.KERNEL_AUTO, segments=dseg.data_ptr(),
+            post_flags=post_flags, kernel=N.KERNEL_PACKED_SMEM if thread else N.KERNEL_AUTO,
+            segments=dseg.data_ptr(),
             n_segments=last + 1, segment_stream=key1 & _M64)
         N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), _stream_ptr(dt.device)),
                 "rmat_generate_refstream (segments)")
-        torch.cuda.current_stream(dt.device).synchronize()  # dseg must outlive the launch
+        # dseg may be freed now: the caching allocator only hands its memory to
+        # later work on this same stream, which runs after the launch
 
 
 def replay_words(dt: DeviceTable, seed: int, domain: int, sid: int, count: int, start: int = 0):

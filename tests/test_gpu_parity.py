@@ -241,8 +241,16 @@ def test_reference_mode_thread_kernel_undirected(cuda):
     ("f2", 9, 300_000, 5, 0),            # fixed-depth table, 5-word segments
     ("v1024", 3, 50_000, 64, 1),         # k below the max depth
 ])
-def test_reference_stream_segment_mode(cuda, tag, k, count, L, w0):
-    """One long reference stream cut into segments on many CTAs == the sequential stream."""
+@pytest.mark.parametrize("mode", ["cta", "thread"])
+def test_reference_stream_segment_mode(cuda, tag, k, count, L, w0, mode):
+    """One long reference stream cut into segments (one CTA or one thread each) ==
+    the sequential stream."""
+    from paper_1905_03525_b200.device import device_table as _dtab
+    if mode == "thread":
+        info = _dtab(table_for(tag), cuda).info
+        if not (info.packed_width == 16 and info.scheme_p and info.max_depth <= k <= 33):
+            pytest.skip("thread-per-segment needs the packed 16-bit table and depth <= k <= 33")
+        L, w0 = (L + 3) // 4 * 4, w0 // 4 * 4
     from paper_1905_03525_b200.device import device_table, launch_refstream_segments
     from paper_1905_03525_b200.generator import edge_dtype
 
@@ -252,7 +260,7 @@ def test_reference_stream_segment_mode(cuda, tag, k, count, L, w0):
     tot = torch.zeros(1, dtype=torch.int64, device=cuda)
     rp, cp = (1 << 40, 3 << 40) if k <= 33 and edge_dtype(k) == torch.uint64 else (0, 0)
     launch_refstream_segments(dt, k, key0, key1, count, out, word_offset=w0, samples_total=tot,
-                              row_prefix=rp, col_prefix=cp, words_per_segment=L)
+                              row_prefix=rp, col_prefix=cp, words_per_segment=L, mode=mode)
     want, nf = oracle.ref_stream_from(oracle_table(tag), k, count, key0, key1, w0, rp, cp)
     got = out.view(torch.int32 if k <= 32 else torch.int64).cpu().numpy()
     got = got.view(np.uint32).astype(np.uint64) if k <= 32 else got.view(np.uint64)

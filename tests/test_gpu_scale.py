@@ -298,3 +298,26 @@ def test_c3_reference_mode_full_size_thread_per_block(cuda):
     assert int(s_auto.item()) == int(s_cta.item())
     del out, v
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("width_k", [20, 33])
+def test_misaligned_output_pointers(cuda, width_k):
+    """Output slices that do not start on a 32-byte sector (sliced tensors): the
+    packed kernels address whole sectors from below and never touch earlier rows."""
+    from paper_1905_03525_b200.device import launch_refstream
+    from paper_1905_03525_b200.generator import edge_dtype
+
+    k = width_k
+    dt = device_table(table_for("v1024"), cuda)
+    wide = torch.int32 if k <= 32 else torch.int64
+    for off in (1, 2, 3):
+        buf = torch.full((4100 + off, 2), -1, dtype=wide, device=cuda)
+        out = buf.view(edge_dtype(k))[off:]
+        launch_generate(dt, k, 9, DOMAIN_BLOCK, 1024, [(0, 4100, 0, 0, 0)], out)
+        ref = torch.empty((4100, 2), dtype=edge_dtype(k), device=cuda)
+        launch_generate(dt, k, 9, DOMAIN_BLOCK, 1024, [(0, 4100, 0, 0, 0)], ref)
+        assert torch.equal(buf[off:], ref.view(wide)) and bool((buf[:off] == -1).all())
+        buf.fill_(-1)
+        launch_refstream(dt, k, 9, DOMAIN_BLOCK, 1024, 4100, 0, 5, out, kernel=N.KERNEL_PACKED_SMEM)
+        launch_refstream(dt, k, 9, DOMAIN_BLOCK, 1024, 4100, 0, 5, ref, kernel=N.KERNEL_PACKED_GLOBAL)
+        assert torch.equal(buf[off:], ref.view(wide)) and bool((buf[:off] == -1).all())
