@@ -125,3 +125,34 @@ def test_fuzz_partitioned(cuda, tag, quads, k, t, m, parts, seed, rngmode):
     # part owning no tile rows still receives it
     empty_parts = sum(1 for lo, hi in plan.owner_rows if lo == hi)
     assert total == m * (1 + (empty_parts if t == 0 else 0))
+
+
+def distinct_configs(n, seed):
+    rng = np.random.default_rng(seed)
+    for i in range(n):
+        tag = ["v253", "v1024", "f2", "f4", "v4096"][int(rng.integers(5))]
+        # not SKEWED (0.9, ...): tens of thousands of distinct cells of a 0.9-skewed
+        # tile are a coupon-collector problem for the reference loop itself
+        quads = [G500, LESS_SKEWED, UNIFORM][int(rng.integers(3))]
+        t = int(rng.integers(0, 4))
+        inner = int(rng.integers(1, 12))
+        k = t + inner
+        cells = 4 ** inner
+        # at most half the cells: filling every cell of a skewed tile is a coupon-collector
+        # tail of many tiny resampling rounds (tested once, uniform-ish, in test_distinct.py)
+        count = int(min(max(cells // 8, 1), rng.choice([1, 10, 500, 5000, 40000])))
+        tile = (int(rng.integers(0, 1 << t)), int(rng.integers(0, 1 << t)))
+        s = int(rng.integers(0, 2**63))
+        yield pytest.param(tag, quads, k, t, tile, count, s, id=f"{i}-{tag}-k{k}t{t}-{count}")
+
+
+@pytest.mark.parametrize("tag,quads,k,t,tile,count,seed", list(distinct_configs(24, 11)))
+def test_fuzz_distinct_tiles_reference_mode(cuda, tag, quads, k, t, tile, count, seed):
+    """generate_tile(distinct=True, rng="reference") == the oracle's restatement of the
+    reference's distinct loop (continuation words, dedup_local, resampling)."""
+    from paper_1905_03525_b200 import generate_tile
+
+    got = generate_tile(tile, count, params_for(quads, k), table_for(tag, quads), k, t, seed,
+                        distinct=True, rng="reference")
+    want, _ = oracle.ref_tile(oracle_table(tag, quads), k, t, *tile, count, seed, distinct=True)
+    assert (got == want).all()
