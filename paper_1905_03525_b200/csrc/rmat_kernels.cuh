@@ -55,6 +55,7 @@ struct StreamPos {
   bool valid;
 };
 
+template <bool REF = false>
 __device__ __forceinline__ StreamPos open_stream(const GenLaunch& g, uint64_t s) {
   StreamPos p;
   p.valid = s < g.total_streams;
@@ -64,7 +65,7 @@ __device__ __forceinline__ StreamPos open_stream(const GenLaunch& g, uint64_t s)
   p.lead = 0;
   p.drop = 0;
   p.report = true;
-  if (g.rsegs) {
+  if (REF && g.rsegs) {
     const RefSeg sg = g.rsegs[s];
     p.sid = g.rseg_key1;
     p.lead = sg.lead;
@@ -339,7 +340,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   const uint64_t T = (uint64_t)gridDim.x * THREADS;
   uint64_t s = (uint64_t)blockIdx.x * THREADS + threadIdx.x;
 
-  StreamPos p = open_stream(g, s);
+  StreamPos p = open_stream<REF>(g, s);
   if (!p.valid) return;
   // Tile segments carry their own key: rebuild the round keys per stream.
   auto stream_keys = [&]() {
@@ -358,7 +359,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   PhiloxPre pre{};
   if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
   uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
-  uint32_t cur_r = 0, cur_c = 0, f = p.lead;
+  uint32_t cur_r = 0, cur_c = 0, f = REF ? p.lead : 0u;
   uint64_t total_nf = 0;
   uint32_t ebits = 0;                // COUNT: samples of the current call that produced an edge
   // Output bookkeeping.  stage + roff = ring slot of the next edge (roff =
@@ -372,7 +373,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   uint32_t half = roff / (G * STRIDE);
   uint32_t lo = roff / STRIDE & (G - 1);
   L += lo;  // count the head's missing slots as already "staged"
-  lo += p.drop;  // a dropped first edge is staged but never flushed (lo may reach G)
+  if (REF) lo += p.drop;  // a dropped first edge is staged but never flushed (lo may reach G)
   char* gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
   auto staged = [&]() { return ((roff / STRIDE) - half * G) & (R - 1); };
 
@@ -592,24 +593,24 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       if (COUNT) {
         // nf (generator.py:255-257): the highest sample of call j-1 that
         // produced an edge this stream needed.
-        const uint64_t nf = 4ull * (j - 1) + (32 - __clz(ebits)) + p.nf_base;
-        if (p.report) {
+        const uint64_t nf = 4ull * (j - 1) + (32 - __clz(ebits)) + (REF ? p.nf_base : 0ull);
+        if (!REF || p.report) {
           total_nf += nf;
           if (g.samples_per_stream) g.samples_per_stream[s] = nf;
         }
       }
       s += T;
-      p = open_stream(g, s);
+      p = open_stream<REF>(g, s);
       if (!p.valid) break;
       stream_keys();
       if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
-      j = 0; cur_r = cur_c = 0; f = p.lead;
+      j = 0; cur_r = cur_c = 0; f = REF ? p.lead : 0u;
       L = (uint32_t)p.left;
       roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
       half = roff / (G * STRIDE);
       lo = roff / STRIDE & (G - 1);
       L += lo;
-      lo += p.drop;
+      if (REF) lo += p.drop;
       gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
       continue;
     }
