@@ -23,6 +23,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--plan", choices=["balanced", "rows"], default="balanced")
+    ap.add_argument("--rng", choices=["philox4x32", "reference"], default="philox4x32")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     args = ap.parse_args()
@@ -55,7 +56,8 @@ def main() -> None:
 
     def run():
         for p in mine:
-            out, _, _ = generate_part_device(plan, pl, table, p, device=dev, tiles=tiles[p])
+            out, _, _ = generate_part_device(plan, pl, table, p, device=dev, tiles=tiles[p],
+                                             rng=args.rng)
             del out
 
     for _ in range(args.warmup):
@@ -76,7 +78,7 @@ def main() -> None:
     if rank == 0:
         print(json.dumps({
             "metric": "edges/sec", "value": m / float(tmax.item()), "unit": "edges/s",
-            "n_gpus": world, "plan": args.plan, "parts_per_rank": len(mine),
+            "n_gpus": world, "plan": args.plan, "rng": args.rng, "parts_per_rank": len(mine),
             "rank0_edges": rows, "seconds": float(tmax.item()),
             "config": {"workload": "C4: less-skewed k=36 m=2^33 t=3, 8 parts, uint64 pairs",
                        "table_size": 1 << 14, "seed": 1}}), flush=True)
