@@ -159,6 +159,27 @@ def traffic_from_profile() -> float | None:
         return None
 
 
+def issue_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
+    """The kernel's second ceiling: SASS instructions per edge (committed ncu capture)
+    against the SM issue rate (4 warp-instructions per SM per cycle)."""
+    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        with open(path) as f:
+            s = json.load(f)
+        ipe = float(s["thread_instructions_per_edge"])
+        hz = float(s["sm_clock_hz"])
+    except (OSError, KeyError, ValueError, TypeError):
+        return None
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ceiling = sms * 4 * 32 * hz / ipe  # edges/s with every issue slot busy
+    achieved = edges / kernel_s
+    return {"bound": "issue", "thread_instructions_per_edge": ipe,
+            "ceiling_edges_per_s": ceiling, "achieved_edges_per_s": achieved,
+            "frac": achieved / ceiling, "source": "profiles/ncu_full_summary.json"}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -294,7 +315,8 @@ def main() -> None:
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "k_packed<16,smem> (rmat_generate)",
                      "algorithmic_bytes_per_launch": rows * BYTES_PER_EDGE,
-                     "frac_of_8TBps_nominal": achieved / 8000.0},
+                     "frac_of_8TBps_nominal": achieved / 8000.0,
+                     "issue_bound": issue_bound_from_profile(kernel_ms / 1e3, rows)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps,
