@@ -144,28 +144,32 @@ typedef struct {
   int kernel;                 /* RMAT_KERNEL_AUTO; PACKED_SMEM = one thread per block (the
                                  fast path's kernel on numpy words), PACKED_GLOBAL = one CTA
                                  per block (packed buckets), GENERIC = one CTA per block */
-  /* Segment mode (segments != NULL): ONE long stream keyed [seed ^ domain,
-   * segment_stream] cut into n_segments pieces that run on separate CTAs;
-   * block_size / edge_count / first_block / n_blocks are ignored, word_offset is
-   * the stream position nf is counted from.  Build the table from
-   * rmat_refstream_segment_depths (see rmat_ref_segment). */
+  /* Segment mode (segments != NULL): long streams keyed [seed ^ domain,
+   * segment.stream] cut into n_segments pieces that run on separate CTAs or
+   * threads; block_size / edge_count / first_block / n_blocks / row_prefix /
+   * col_prefix / word_offset are ignored (each segment carries its own).
+   * Build the table from rmat_refstream_segment_depths (see rmat_ref_segment). */
   const void* segments;       /* device array of rmat_ref_segment */
   uint64_t n_segments;
-  uint64_t segment_stream;
+  uint64_t reserved;          /* 0 */
 } rmat_refstream_args;
 
 /* One piece of a long reference stream: reading starts at word_begin, whose
  * first bit lies `skip` bits before the next edge boundary; lead = (k - skip)
  * % k zero bits are prepended and the edge they complete is dropped.  The
  * piece emits the `count` edges that START inside it (reading on to finish the
- * last) to rows [out_row, out_row + count); report_nf = 1 on the piece holding
- * the stream's last edge. */
+ * last) to rows [out_row, out_row + count), OR-ing the prefixes in;
+ * report_nf = 1 on the piece holding its stream's last edge, whose nf counts
+ * words from nf_origin (the stream's first word). */
 typedef struct {
   uint64_t word_begin;
   uint64_t out_row;
   uint64_t count;
   uint32_t lead;
   uint32_t report_nf;
+  uint64_t stream;            /* second Philox key word: the block / tile payload */
+  uint64_t row_prefix, col_prefix;
+  uint64_t nf_origin;
 } rmat_ref_segment;
 
 /* Depth sums of words [word_begin + s*L, word_begin + (s+1)*L) for s in

@@ -102,13 +102,15 @@ class RefArgs(ctypes.Structure):
                 ("row_prefix", ctypes.c_uint64), ("col_prefix", ctypes.c_uint64),
                 ("word_offset", ctypes.c_uint64), ("post_flags", ctypes.c_uint32),
                 ("kernel", ctypes.c_int), ("segments", ctypes.c_void_p),
-                ("n_segments", ctypes.c_uint64), ("segment_stream", ctypes.c_uint64)]
+                ("n_segments", ctypes.c_uint64), ("reserved", ctypes.c_uint64)]
 
 
 class RefSegment(ctypes.Structure):
     _fields_ = [("word_begin", ctypes.c_uint64), ("out_row", ctypes.c_uint64),
                 ("count", ctypes.c_uint64), ("lead", ctypes.c_uint32),
-                ("report_nf", ctypes.c_uint32)]
+                ("report_nf", ctypes.c_uint32), ("stream", ctypes.c_uint64),
+                ("row_prefix", ctypes.c_uint64), ("col_prefix", ctypes.c_uint64),
+                ("nf_origin", ctypes.c_uint64)]
 
 
 class DedupArgs(ctypes.Structure):

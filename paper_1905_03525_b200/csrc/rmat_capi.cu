@@ -515,8 +515,7 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
   const uint64_t nblocks_all = (a->edge_count + a->block_size - 1) / a->block_size;
   if (!seg_mode && (a->first_block > nblocks_all || a->n_blocks > nblocks_all - a->first_block))
     return RMAT_ERR_INVALID;
-  if (seg_mode && a->kernel == RMAT_KERNEL_PACKED_SMEM && (a->word_offset & 3))
-    return RMAT_ERR_UNSUPPORTED;  // per-thread segments start on whole Philox calls
+  // (per-thread segments must start on whole Philox calls: the host guarantees it)
   const rmat_table* t = a->table;
   DeviceGuard guard(t->device);
   if (!guard.ok) return RMAT_ERR_DEVICE;
@@ -548,10 +547,6 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
     g.samples_total = a->samples_total;
     g.post = a->post_flags;
     g.rsegs = reinterpret_cast<const rmat::RefSeg*>(a->segments);
-    g.rseg_key1 = a->segment_stream;
-    g.nf_origin = a->word_offset;
-    g.rseg_rpre = a->row_prefix;
-    g.rseg_cpre = a->col_prefix;
     g.total_streams = a->n_segments;
     return launch_ref_thread(t, g, a->out_width == 8, /*prefix=*/true,
                              a->samples_total != nullptr,

@@ -68,6 +68,9 @@ struct RefSeg {
   uint64_t count;
   uint32_t lead;
   uint32_t report_nf;
+  uint64_t stream;
+  uint64_t row_prefix, col_prefix;
+  uint64_t nf_origin;
 };
 
 struct GenLaunch {
@@ -81,10 +84,10 @@ struct GenLaunch {
   uint64_t* samples_total;
   uint64_t* samples_per_stream;
   uint32_t post;        // RMAT_POST_UNDIRECTED: fused to_undirected
-  // REF segment mode: stream s = rsegs[s] of one reference stream keyed
-  // [k1:k0, rseg_key1]; nf counted from word nf_origin; one row/col prefix.
+  // REF segment mode: stream s = rsegs[s], a piece of a reference stream keyed
+  // [k1:k0, rsegs[s].stream]; rows shifted by rseg_row_shift (sector alignment).
   const RefSeg* rsegs;
-  uint64_t rseg_key1, nf_origin, rseg_rpre, rseg_cpre, rseg_row_shift;
+  uint64_t rseg_row_shift;
   SegDev segs[kMaxSegsPerLaunch];
 };
 

@@ -67,17 +67,17 @@ __device__ __forceinline__ StreamPos open_stream(const GenLaunch& g, uint64_t s)
   p.report = true;
   if (REF && g.rsegs) {
     const RefSeg sg = g.rsegs[s];
-    p.sid = g.rseg_key1;
+    p.sid = sg.stream;
     p.lead = sg.lead;
     p.drop = sg.lead ? 1u : 0u;
     p.left = sg.count + p.drop;
     p.row = sg.out_row - p.drop + g.rseg_row_shift;
-    p.rpre = g.rseg_rpre;
-    p.cpre = g.rseg_cpre;
+    p.rpre = sg.row_prefix;
+    p.cpre = sg.col_prefix;
     p.k0 = g.k0;
     p.k1 = g.k1;
     p.wcall = sg.word_begin >> 2;  // the host aligns segment starts to whole calls
-    p.nf_base = (sg.word_begin & ~3ull) - g.nf_origin;
+    p.nf_base = (sg.word_begin & ~3ull) - sg.nf_origin;
     p.report = sg.report_nf != 0;
     return p;
   }

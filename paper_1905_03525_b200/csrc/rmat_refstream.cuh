@@ -40,15 +40,13 @@ struct RefLaunch {
   uint64_t rpre, cpre;
   uint64_t w0;    // first word of every block stream (continuation after an earlier _emit)
   uint32_t post;  // RMAT_POST_UNDIRECTED: fused to_undirected
-  // Segment mode (segs != nullptr): "block" bi is segment segs[bi] of ONE long
-  // stream keyed [key0, seg_key1]; nf counts words from nf_origin.
+  // Segment mode (segs != nullptr): "block" bi is segment segs[bi], a piece of
+  // the stream keyed [key0, segs[bi].stream] (own prefixes and nf origin).
   const struct RefSeg* segs;
-  uint64_t seg_key1;
-  uint64_t nf_origin;
 };
 
 struct RefBlock {
-  uint64_t key1, w0, count, out_row, origin;
+  uint64_t key1, w0, count, out_row, origin, rpre, cpre;
   uint32_t lead, drop;
   bool report;
 };
@@ -57,13 +55,15 @@ __device__ __forceinline__ RefBlock ref_block(const RefLaunch& g, uint64_t bi) {
   RefBlock r;
   if (g.segs) {
     const RefSeg sg = g.segs[bi];
-    r.key1 = g.seg_key1;
+    r.key1 = sg.stream;
     r.w0 = sg.word_begin;
     r.lead = sg.lead;
     r.drop = sg.lead ? 1u : 0u;
     r.count = sg.count + r.drop;
     r.out_row = sg.out_row;
-    r.origin = g.nf_origin;
+    r.origin = sg.nf_origin;
+    r.rpre = sg.row_prefix;
+    r.cpre = sg.col_prefix;
     r.report = sg.report_nf != 0;
   } else {
     const uint64_t b = g.first_block + bi;
@@ -74,6 +74,8 @@ __device__ __forceinline__ RefBlock ref_block(const RefLaunch& g, uint64_t bi) {
     r.count = min(g.B, g.m - b * g.B);
     r.out_row = bi * g.B;
     r.origin = g.w0;
+    r.rpre = g.rpre;
+    r.cpre = g.cpre;
     r.report = true;
   }
   return r;
@@ -214,7 +216,7 @@ k_refstream(const GenericTab tab, const RefLaunch g) {
       }
       if (emitted + e >= blk.drop)
         ref_store<OUT64>(reinterpret_cast<char*>(g.out), blk.out_row + emitted + e - blk.drop,
-                         (ur & kmask) | g.rpre, (uc & kmask) | g.cpre, g.post);
+                         (ur & kmask) | blk.rpre, (uc & kmask) | blk.cpre, g.post);
     }
     // 4. carry / nf (one thread), then advance
     if (tid == 0) {
@@ -461,8 +463,8 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
           // edge's last bit
           if (final_chunk && j + 1 == avail) s_nf = chunk_base + sidx - blk.origin;
           if (emitted + j >= blk.drop)
-            ref_store<OUT64>(outb, blk.out_row + emitted + j - blk.drop, (ur & kmask) | g.rpre,
-                             (uc & kmask) | g.cpre, g.post);
+            ref_store<OUT64>(outb, blk.out_row + emitted + j - blk.drop, (ur & kmask) | blk.rpre,
+                             (uc & kmask) | blk.cpre, g.post);
         }
       }
       emitted += avail;
@@ -618,8 +620,8 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
         if (e < avail) {
           if (emitted + e >= blk.drop)
             ref_store<OUT64>(outb, blk.out_row + emitted + e - blk.drop,
-                             (uint64_t)(er & kmaskw) | g.rpre,
-                           (uint64_t)(ec & kmaskw) | g.cpre, g.post);
+                             (uint64_t)(er & kmaskw) | blk.rpre,
+                           (uint64_t)(ec & kmaskw) | blk.cpre, g.post);
         } else if (e == nfull && !final_chunk) {
           // partial edge: its bits sit at the top of the k-bit word
           s_carry_r = er;
@@ -728,8 +730,6 @@ inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
   g.w0 = a.word_offset;
   g.post = a.post_flags;
   g.segs = reinterpret_cast<const RefSeg*>(a.segments);
-  g.seg_key1 = a.segment_stream;
-  g.nf_origin = a.word_offset;
   const uint64_t nb = a.segments ? a.n_segments : a.n_blocks;
   // (64-bit edge words for k = 33 measured slower than the walk kernel: 1.44e10
   // vs 1.57e10 edges/s on C4 tiles -- 64-bit shared atomics)

@@ -142,15 +142,14 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
     if (kernel == N.KERNEL_AUTO and 0 < n_blocks <= LONG_STREAM_MAX_BLOCKS
             and min(block_size, edge_count - first_block * block_size) >= LONG_STREAM_EDGES
             and samples_per_block is None):
-        # few long blocks: cut each into segments that run on many CTAs
+        # few long blocks: cut them into segments that run on many threads / CTAs
+        jobs = []
         for i in range(n_blocks):
             b = first_block + i
             cnt = min(block_size, edge_count - b * block_size)
-            launch_refstream_segments(dt, k, (seed ^ domain) & _M64, b, cnt,
-                                      out[i * block_size:i * block_size + cnt],
-                                      word_offset=word_offset, samples_total=samples_total,
-                                      row_prefix=row_prefix, col_prefix=col_prefix,
-                                      post_flags=post_flags)
+            jobs.append((b, cnt, i * block_size, row_prefix, col_prefix, word_offset))
+        launch_refstream_streams(dt, k, (seed ^ domain) & _M64, jobs, out,
+                                 samples_total=samples_total, post_flags=post_flags)
         return
     args = N.RefArgs(
         table=dt.handle, k=k, out_width=out.element_size(), seed=seed & (2**64 - 1),
@@ -180,76 +179,116 @@ def launch_refstream_segments(dt: DeviceTable, k: int, key0: int, key1: int, cou
                               col_prefix: int = 0, post_flags: int = 0,
                               words_per_segment: int | None = None, mode: str = "auto") -> None:
     """`count` edges of ONE reference stream keyed [key0, key1] from word `word_offset`,
-    spread over many CTAs: per-segment depth sums (device) -> host scan -> a
-    segment table (rmat_ref_segment) -> one segment-mode rmat_generate_refstream."""
+    spread over many threads / CTAs (see launch_refstream_streams)."""
+    launch_refstream_streams(dt, k, key0, [(key1, count, 0, row_prefix, col_prefix, word_offset)],
+                             out, samples_total=samples_total, post_flags=post_flags,
+                             words_per_segment=words_per_segment, mode=mode)
+
+
+def launch_refstream_streams(dt: DeviceTable, k: int, key0: int, streams, out, *,
+                             samples_total=None, post_flags: int = 0,
+                             words_per_segment: int | None = None, mode: str = "auto") -> None:
+    """Several long reference streams in ONE segment-mode launch.
+
+    streams: (key1, count, out_row, row_prefix, col_prefix, word_offset) per stream
+    (e.g. every tile of a part).  Per-segment depth sums for all streams are
+    launched back to back and read once; the host scans them into segment
+    tables (rmat_ref_segment); one rmat_generate_refstream runs every segment
+    of every stream -- one thread each when the table allows it (the fast
+    path's kernel on numpy words), else one CTA each.
+    """
     import torch
 
-    if count == 0:
+    streams = [tuple(int(x) for x in st) for st in streams if st[1] > 0]
+    if not streams:
         return
     info = dt.info
-    # one thread per segment (the fast path's kernel on numpy words) when the table
-    # and k allow it: small segments so that a single stream fills the GPU
     eligible = (info.packed_width == 16 and info.scheme_p and info.packed_smem
-                and info.max_depth <= k <= 33 and word_offset % 4 == 0)
+                and info.max_depth <= k <= 33 and all(st[5] % 4 == 0 for st in streams))
     if mode not in ("auto", "thread", "cta"):
         raise ValueError(f"mode must be auto, thread or cta, got {mode!r}")
     thread = mode == "thread" or (mode == "auto" and eligible)
-    need = count * k
     mean = float(dt.table.mean_depth)
+    total_words = sum(st[1] * k for st in streams) / mean
     if words_per_segment:
         L = int(words_per_segment)
     elif thread:
         # a segment is one thread's sequential work: long enough to amortise the
-        # per-stream setup (2^14 words measured best), short enough that the
-        # stream still spreads over ~2 waves of the GPU's threads
+        # per-stream setup (2^14 words measured best), short enough that all the
+        # streams together still spread over ~2 waves of the GPU's threads
         threads = 2 * 512 * torch.cuda.get_device_properties(dt.device).multi_processor_count
         L = THREAD_SEGMENT_WORDS
-        while L > 1024 and need / mean / L < threads:
+        while L > 1024 and total_words / L < threads:
             L //= 2
     else:
         L = SEGMENT_WORDS
     if thread and L % 4:
         raise ValueError("thread-per-segment mode needs whole Philox calls per segment")
-    nseg = int(need / mean / L * 1.02) + 2
+    stream_ptr = _stream_ptr(dt.device)
+    nsegs = [int(st[1] * k / mean / L * 1.02) + 2 for st in streams]
     with torch.cuda.device(dt.device):
-        while True:
-            sums = torch.empty(nseg, dtype=torch.int64, device=dt.device)
-            N.check(N.lib().rmat_refstream_segment_depths(
-                dt.handle, key0 & _M64, key1 & _M64, word_offset, L, nseg, sums.data_ptr(),
-                _stream_ptr(dt.device)), "rmat_refstream_segment_depths")
-            cs = np.cumsum(sums.cpu().numpy().astype(np.uint64), dtype=np.uint64)
-            if int(cs[-1]) >= need:
-                break
-            nseg = int(nseg * 1.25) + 2
-        last = int(np.searchsorted(cs, np.uint64(need), side="left"))  # holds bit need-1
-        off = np.concatenate([np.zeros(1, dtype=np.uint64), cs[:last]])  # first bit of each segment
+        pending = list(range(len(streams)))
+        cums: dict[int, np.ndarray] = {}
+        while pending:
+            sums = torch.empty(sum(nsegs[i] for i in pending), dtype=torch.int64,
+                               device=dt.device)
+            at = 0
+            for i in pending:
+                key1, count, _, _, _, w0 = streams[i]
+                N.check(N.lib().rmat_refstream_segment_depths(
+                    dt.handle, key0 & _M64, key1 & _M64, w0, L, nsegs[i],
+                    sums.data_ptr() + 8 * at, stream_ptr), "rmat_refstream_segment_depths")
+                at += nsegs[i]
+            host = sums.cpu().numpy().astype(np.uint64)  # one sync for every stream
+            at, again = 0, []
+            for i in pending:
+                cs = np.cumsum(host[at:at + nsegs[i]], dtype=np.uint64)
+                at += nsegs[i]
+                if int(cs[-1]) >= streams[i][1] * k:
+                    cums[i] = cs
+                else:
+                    nsegs[i] = int(nsegs[i] * 1.25) + 2
+                    again.append(i)
+            pending = again
+        tables = []
         kk = np.uint64(k)
-        e0 = (off + kk - np.uint64(1)) // kk
-        e1 = np.minimum(np.concatenate([e0[1:], [np.uint64(count)]]), np.uint64(count))
-        e1[-1] = count
-        skip = e0 * kk - off
-        segs = np.zeros(last + 1, dtype=[("word_begin", "<u8"), ("out_row", "<u8"),
-                                          ("count", "<u8"), ("lead", "<u4"),
-                                          ("report_nf", "<u4")])
-        segs["word_begin"] = word_offset + np.arange(last + 1, dtype=np.uint64) * np.uint64(L)
-        segs["out_row"] = e0
-        segs["count"] = e1 - e0
-        segs["lead"] = np.where(skip > 0, kk - skip, np.uint64(0)).astype(np.uint32)
-        segs["report_nf"][-1] = 1
+        for i, (key1, count, out_row, rp, cp, w0) in enumerate(streams):
+            cs = cums[i]
+            last = int(np.searchsorted(cs, np.uint64(count * k), side="left"))
+            off = np.concatenate([np.zeros(1, dtype=np.uint64), cs[:last]])
+            e0 = (off + kk - np.uint64(1)) // kk
+            e1 = np.minimum(np.concatenate([e0[1:], [np.uint64(count)]]), np.uint64(count))
+            e1[-1] = count
+            skip = e0 * kk - off
+            t = np.zeros(last + 1, dtype=_REFSEG_DTYPE)
+            t["word_begin"] = w0 + np.arange(last + 1, dtype=np.uint64) * np.uint64(L)
+            t["out_row"] = e0 + np.uint64(out_row)
+            t["count"] = e1 - e0
+            t["lead"] = np.where(skip > 0, kk - skip, np.uint64(0)).astype(np.uint32)
+            t["report_nf"][-1] = 1
+            t["stream"] = key1 & _M64
+            t["row_prefix"] = rp
+            t["col_prefix"] = cp
+            t["nf_origin"] = w0
+            tables.append(t)
+        segs = np.concatenate(tables)
         dseg = torch.from_numpy(segs.view(np.uint8)).to(dt.device)
         args = N.RefArgs(
             table=dt.handle, k=k, out_width=out.element_size(), seed=key0 & _M64, domain=0,
             block_size=1, edge_count=1, first_block=0, n_blocks=0, out=out.data_ptr(),
             samples_per_block=None,
             samples_total=samples_total.data_ptr() if samples_total is not None else None,
-            row_prefix=row_prefix, col_prefix=col_prefix, word_offset=word_offset,
             post_flags=post_flags, kernel=N.KERNEL_PACKED_SMEM if thread else N.KERNEL_AUTO,
-            segments=dseg.data_ptr(),
-            n_segments=last + 1, segment_stream=key1 & _M64)
-        N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), _stream_ptr(dt.device)),
+            segments=dseg.data_ptr(), n_segments=len(segs))
+        N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), stream_ptr),
                 "rmat_generate_refstream (segments)")
         # dseg may be freed now: the caching allocator only hands its memory to
         # later work on this same stream, which runs after the launch
+
+
+_REFSEG_DTYPE = np.dtype([("word_begin", "<u8"), ("out_row", "<u8"), ("count", "<u8"),
+                          ("lead", "<u4"), ("report_nf", "<u4"), ("stream", "<u8"),
+                          ("row_prefix", "<u8"), ("col_prefix", "<u8"), ("nf_origin", "<u8")])
 
 
 def replay_words(dt: DeviceTable, seed: int, domain: int, sid: int, count: int, start: int = 0):

@@ -42,7 +42,7 @@ import numpy as np
 
 from . import _native as N
 from .device import (DedupSet, device_table, launch_generate, launch_refstream,
-                     refstream_depth_sum, require_cuda)
+                     launch_refstream_streams, refstream_depth_sum, require_cuda)
 from .generator import DOMAIN_NODE, DOMAIN_TILE, FAST_STREAM_EDGES, RNG_MODES, edge_dtype
 from .params import RmatParams, check_k
 from .table import FragmentTable
@@ -320,15 +320,16 @@ def generate_part_device(plan: PartitionPlan, params: RmatParams, table: Fragmen
                                rng, out[r:r + tc.count], samples, dset, tmp)
             r += tc.count
     elif rng == "reference":
-        r = 0
+        # every tile is one numpy stream keyed [seed ^ DOMAIN_TILE, payload]: all of
+        # them in one segment-mode launch (partition.py:154-162)
+        jobs, r = [], 0
         for tc in tiles:
             if tc.count:
-                payload = (tc.tile_row << t) | tc.tile_col
-                launch_refstream(dt, inner, plan.seed, DOMAIN_TILE, tc.count,
-                                 (payload + 1) * tc.count, payload, 1, out[r:r + tc.count],
-                                 samples_total=samples, row_prefix=tc.tile_row << inner,
-                                 col_prefix=tc.tile_col << inner)
+                jobs.append(((tc.tile_row << t) | tc.tile_col, tc.count, r,
+                             tc.tile_row << inner, tc.tile_col << inner, 0))
             r += tc.count
+        launch_refstream_streams(dt, inner, (plan.seed ^ DOMAIN_TILE) & _M64, jobs, out,
+                                 samples_total=samples)
     else:
         segs, _ = part_segments(tiles, k, t, edges_per_stream)
         launch_generate(dt, inner, plan.seed, DOMAIN_TILE, edges_per_stream, segs, out,
