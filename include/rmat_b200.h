@@ -197,9 +197,9 @@ rmat_status rmat_refstream_depth_sum(const rmat_table* table, uint64_t key0, uin
  * -- and is not repeated earlier in `in` -- are written to `out` in input
  * order; *kept (device) receives their number.  `in` and `out` must not
  * overlap.  Workspace: `set` of rmat_dedup_set_bytes(capacity) bytes, 32-byte
- * aligned (capacity
- * a power of two above the number of distinct keys the set will hold; half
- * full or less keeps probing short), `scratch` of rmat_dedup_scratch_bytes(rows).
+ * aligned (capacity = slots, any size above the number of distinct keys the set
+ * will hold; 2/3 full or less keeps probing short), `scratch` of
+ * rmat_dedup_scratch_bytes(rows).
  * *status (device, optional) gets RMAT_DEDUP_STATUS_* bits OR'd in. */
 enum { RMAT_DEDUP_RESET = 1, RMAT_DEDUP_CHECK_RANGE = 2 };
 enum { RMAT_DEDUP_STATUS_RANGE = 1, RMAT_DEDUP_STATUS_FULL = 2 };
@@ -213,7 +213,7 @@ typedef struct {
   void* out;               /* device, up to rows x 2 */
   uint64_t index_base;     /* priority of in[0]; must exceed every earlier row of this set */
   void* set;               /* device workspace */
-  uint64_t capacity;       /* slots, power of two */
+  uint64_t capacity;       /* slots (>= 2) */
   void* scratch;           /* device workspace */
   uint64_t* kept;          /* device: rows written to out */
   uint32_t* status;        /* device, optional */

@@ -634,7 +634,7 @@ uint64_t rmat_dedup_scratch_bytes(uint64_t rows) {
 
 rmat_status rmat_dedup(const rmat_dedup_args* a, int device, void* cuda_stream) {
   if (!a || (a->width != 4 && a->width != 8) || (a->flags & ~3u)) return RMAT_ERR_INVALID;
-  if (!a->set || a->capacity < 2 || (a->capacity & (a->capacity - 1)) || !a->kept)
+  if (!a->set || a->capacity < 2 || !a->kept)
     return RMAT_ERR_INVALID;
   if ((reinterpret_cast<uintptr_t>(a->set) & 31) != 0) return RMAT_ERR_INVALID;
   if (a->rows && (!a->in || !a->out || !a->scratch)) return RMAT_ERR_INVALID;
@@ -655,7 +655,7 @@ rmat_status rmat_dedup(const rmat_dedup_args* a, int device, void* cuda_stream) 
   g.out = a->out;
   g.base = a->index_base;
   g.slots = reinterpret_cast<ulonglong4*>(a->set);
-  g.mask = a->capacity - 1;
+  g.capacity = a->capacity;
   g.slot_of = reinterpret_cast<uint64_t*>(a->scratch);
   g.ntiles = (a->rows + rmat::kDedupTile - 1) / rmat::kDedupTile;
   g.tile_off = g.slot_of + a->rows;

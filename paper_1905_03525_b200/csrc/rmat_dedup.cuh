@@ -17,7 +17,7 @@
 //   slot.key   16 B  (u, v) as two u64, empty = all ones
 //   slot.first  8 B  lowest priority seen for the key
 //   (8 B pad)
-// Linear probing from splitmix64(u ^ splitmix64(v)); slots are claimed with a
+// Linear probing from splitmix64(u ^ splitmix64(v)) range-reduced to the capacity; slots are claimed with a
 // single 128-bit CAS (sm_90+ atom.cas.b128), so an edge of any width is one key.
 //
 // Kernels (all HBM/L2-latency bound, one pass each over the rows):
@@ -44,7 +44,7 @@ struct DedupLaunch {
   void* out;
   uint64_t base;
   ulonglong4* slots;
-  uint64_t mask;  // capacity - 1
+  uint64_t capacity;  // slots (any size >= 2: hashes are range-reduced, not masked)
   uint64_t* slot_of;
   uint8_t* keep;
   uint64_t* tile_off;
@@ -90,14 +90,15 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const DedupLaunch g) {
     if (g.check_range &&
         (e.x < g.row_lo || e.x >= g.row_hi || e.y < g.col_lo || e.y >= g.col_hi))
       atomicOr(g.status, RMAT_DEDUP_STATUS_RANGE);
-    uint64_t h = splitmix_fin(e.x ^ splitmix_fin(e.y)) & g.mask;
+    // multiply-high range reduction: any capacity, no power-of-two rounding
+    uint64_t h = __umul64hi(splitmix_fin(e.x ^ splitmix_fin(e.y)), g.capacity);
     uint64_t probes = 0;
     for (;;) {
       const ulonglong2 prev =
           cas128(reinterpret_cast<ulonglong2*>(g.slots + h), make_ulonglong2(~0ull, ~0ull), e);
       if ((prev.x == ~0ull && prev.y == ~0ull) || (prev.x == e.x && prev.y == e.y)) break;
-      h = (h + 1) & g.mask;
-      if (++probes > g.mask) {  // every slot holds another key: caller under-sized the set
+      h = h + 1 == g.capacity ? 0 : h + 1;
+      if (++probes >= g.capacity) {  // every slot holds another key: caller under-sized the set
         atomicOr(g.status, RMAT_DEDUP_STATUS_FULL);
         h = ~0ull;
         break;

@@ -319,15 +319,14 @@ def refstream_depth_sum(dt: DeviceTable, key0: int, key1: int, word_begin: int, 
 
 
 class DedupSet:
-    """Device hash set for first-occurrence dedup (rmat_dedup); `capacity` >= 2x the keys held."""
+    """Device hash set for first-occurrence dedup (rmat_dedup): 2 slots per key it may hold
+    (half full at most: short probes; no power-of-two rounding, hashes are range-reduced)."""
 
     def __init__(self, keys: int, device=None):
         import torch
 
         self.device = require_cuda(device)
-        cap = 2
-        while cap < 2 * max(int(keys), 1):
-            cap <<= 1
+        cap = max(2, 2 * max(int(keys), 1))
         self.capacity = cap
         nbytes = int(N.lib().rmat_dedup_set_bytes(cap))
         self._set = torch.empty(nbytes // 8, dtype=torch.int64, device=self.device)

@@ -51,7 +51,7 @@ def test_pure_host_entry_points():
     assert L.rmat_refstream_depth_sum(None, 0, 0, 0, 1, None, None) == 1
     assert L.rmat_dedup(None, 0, None) == 1
     # argument validation happens before any CUDA call
-    a = N.DedupArgs(width=4, rows=0, set=64, capacity=3, kept=64)  # capacity not a power of 2
+    a = N.DedupArgs(width=4, rows=0, set=64, capacity=1, kept=64)  # capacity below 2
     assert L.rmat_dedup(ctypes.byref(a), 0, None) == 1
     a = N.DedupArgs(width=2, rows=0, set=64, capacity=4, kept=64)  # bad width
     assert L.rmat_dedup(ctypes.byref(a), 0, None) == 1
