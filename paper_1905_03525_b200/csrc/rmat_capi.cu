@@ -741,9 +741,20 @@ rmat_status rmat_refstream_segment_depths(const rmat_table* t, uint64_t key0, ui
   DeviceGuard guard(t->device);
   if (!guard.ok) return RMAT_ERR_DEVICE;
   const unsigned blocks = (unsigned)std::min<uint64_t>(nseg, (uint64_t)num_sms(t->device) * 8);
-  rmat::k_ref_segment_depths<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
-      generic_view(t), key0, key1, word_begin, L, nseg,
-      reinterpret_cast<unsigned long long*>(sums));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  const size_t bbytes = (size_t)t->n * 4;
+  if (t->fb == 16 && t->scheme_p && bbytes <= 96 * 1024) {
+    auto kern = rmat::k_ref_segment_depths_packed;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bbytes) !=
+        cudaSuccess)
+      return RMAT_ERR_CUDA;
+    kern<<<blocks, 256, bbytes, st>>>(packed_view(t), key0, key1, word_begin, L, nseg,
+                                      reinterpret_cast<unsigned long long*>(sums));
+  } else {
+    rmat::k_ref_segment_depths<<<blocks, 256, 0, st>>>(
+        generic_view(t), key0, key1, word_begin, L, nseg,
+        reinterpret_cast<unsigned long long*>(sums));
+  }
   return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
 }
 

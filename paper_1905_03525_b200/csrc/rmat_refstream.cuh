@@ -711,6 +711,51 @@ k_ref_segment_depths(const GenericTab tab, uint64_t key0, uint64_t key1, uint64_
   }
 }
 
+// Packed variant (16-bit packed tables): the B words (complemented threshold
+// top bits + both depths, rmat_device.cuh) staged in shared memory; one load,
+// one IMAD compare and one PRMT per word instead of three dependent gathers.
+__global__ void __launch_bounds__(256)
+k_ref_segment_depths_packed(const PackedTab tab, uint64_t key0, uint64_t key1, uint64_t w_begin,
+                            uint64_t L, uint64_t nseg, unsigned long long* sums) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ unsigned long long s_acc;
+  const uint32_t n = tab.n;
+  uint32_t* sB = reinterpret_cast<uint32_t*>(smem);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(tab.B);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    for (uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  const uint32_t fm = tab.fm, one = tab.one, nmask = n - 1;
+  for (uint64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    if (threadIdx.x == 0) s_acc = 0;
+    __syncthreads();
+    const uint64_t lo = w_begin + sg * L, hi = lo + L;
+    uint64_t acc = 0;
+    for (uint64_t c = lo / 4 + threadIdx.x; c < (hi + 3) / 4; c += blockDim.x) {
+      const u64x4 w4 = philox4x64_10(c + 1, c + 1 == 0 ? 1 : 0, 0, 0, key0, key1);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t i = 4 * c + q;
+        const uint64_t w = q == 0 ? w4.x : q == 1 ? w4.y : q == 2 ? w4.z : w4.w;
+        const uint32_t idx = (uint32_t)(w >> 32) & nmask;
+        const uint32_t frac = (uint32_t)w;
+        const uint32_t bw = sB[idx];
+        const uint64_t sum = mad_wide_ref(frac | fm, one, bw);
+        uint32_t ge = (uint32_t)(sum >> 32);
+        if ((uint32_t)sum <= fm) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
+        if (i >= lo && i < hi) acc += prmt_ref(bw, 0x4440u + ge);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_acc, (unsigned long long)acc);
+    __syncthreads();
+    if (threadIdx.x == 0) sums[sg] = s_acc;
+    __syncthreads();
+  }
+}
+
 inline rmat_status launch_refstream(const GenericTab tab, uint32_t dmax,
                                     const rmat_refstream_args& a, cudaStream_t st,
                                     const PackedTab* packed = nullptr, int sms = 148,

@@ -227,68 +227,77 @@ def launch_refstream_streams(dt: DeviceTable, k: int, key0: int, streams, out, *
     stream_ptr = _stream_ptr(dt.device)
     nsegs = [int(st[1] * k / mean / L * 1.02) + 2 for st in streams]
     with torch.cuda.device(dt.device):
+        # depth sums of every segment of every stream, scanned on the device; the
+        # host reads back only each stream's coverage and used-segment count
         pending = list(range(len(streams)))
-        cums: dict[int, np.ndarray] = {}
+        cums: dict[int, tuple] = {}
         while pending:
             sums = torch.empty(sum(nsegs[i] for i in pending), dtype=torch.int64,
                                device=dt.device)
-            at = 0
+            at, views = 0, []
             for i in pending:
                 key1, count, _, _, _, w0 = streams[i]
                 N.check(N.lib().rmat_refstream_segment_depths(
                     dt.handle, key0 & _M64, key1 & _M64, w0, L, nsegs[i],
                     sums.data_ptr() + 8 * at, stream_ptr), "rmat_refstream_segment_depths")
+                views.append(sums[at:at + nsegs[i]])
                 at += nsegs[i]
-            host = sums.cpu().numpy().astype(np.uint64)  # one sync for every stream
-            at, again = 0, []
-            for i in pending:
-                cs = np.cumsum(host[at:at + nsegs[i]], dtype=np.uint64)
-                at += nsegs[i]
-                if int(cs[-1]) >= streams[i][1] * k:
-                    cums[i] = cs
+            cs_list = [torch.cumsum(v, 0) for v in views]
+            need_t = torch.tensor([streams[i][1] * k for i in pending], dtype=torch.int64,
+                                  device=dt.device)
+            lasts = torch.stack([torch.searchsorted(c, need_t[j:j + 1]).squeeze(0)
+                                 for j, c in enumerate(cs_list)])
+            tot = torch.stack([c[-1] for c in cs_list])
+            info_h = torch.stack([tot, lasts]).cpu().numpy()  # one sync for every stream
+            again = []
+            for j, i in enumerate(pending):
+                if int(info_h[0, j]) >= streams[i][1] * k:
+                    cums[i] = (cs_list[j], int(info_h[1, j]))
                 else:
                     nsegs[i] = int(nsegs[i] * 1.25) + 2
                     again.append(i)
             pending = again
         tables = []
-        kk = np.uint64(k)
         for i, (key1, count, out_row, rp, cp, w0) in enumerate(streams):
-            cs = cums[i]
-            last = int(np.searchsorted(cs, np.uint64(count * k), side="left"))
-            off = np.concatenate([np.zeros(1, dtype=np.uint64), cs[:last]])
-            e0 = (off + kk - np.uint64(1)) // kk
-            e1 = np.minimum(np.concatenate([e0[1:], [np.uint64(count)]]), np.uint64(count))
+            cs, last = cums[i]
+            n_used = last + 1
+            off = torch.zeros(n_used, dtype=torch.int64, device=dt.device)
+            off[1:] = cs[:last]
+            e0 = (off + (k - 1)) // k
+            e1 = torch.empty_like(e0)
+            e1[:-1] = e0[1:]
             e1[-1] = count
-            skip = e0 * kk - off
-            t = np.zeros(last + 1, dtype=_REFSEG_DTYPE)
-            t["word_begin"] = w0 + np.arange(last + 1, dtype=np.uint64) * np.uint64(L)
-            t["out_row"] = e0 + np.uint64(out_row)
-            t["count"] = e1 - e0
-            t["lead"] = np.where(skip > 0, kk - skip, np.uint64(0)).astype(np.uint32)
-            t["report_nf"][-1] = 1
-            t["stream"] = key1 & _M64
-            t["row_prefix"] = rp
-            t["col_prefix"] = cp
-            t["nf_origin"] = w0
+            e1.clamp_(max=count)
+            skip = e0 * k - off
+            t = torch.empty((n_used, 8), dtype=torch.int64, device=dt.device)
+            t[:, 0] = w0 + torch.arange(n_used, dtype=torch.int64, device=dt.device) * L
+            t[:, 1] = e0 + out_row
+            t[:, 2] = e1 - e0
+            t[:, 3] = torch.where(skip > 0, k - skip, torch.zeros_like(skip))  # lead | report<<32
+            t[-1, 3] += 1 << 32
+            t[:, 4] = _as_i64(key1)
+            t[:, 5] = _as_i64(rp)
+            t[:, 6] = _as_i64(cp)
+            t[:, 7] = w0
             tables.append(t)
-        segs = np.concatenate(tables)
-        dseg = torch.from_numpy(segs.view(np.uint8)).to(dt.device)
+        dseg = tables[0] if len(tables) == 1 else torch.cat(tables)  # rmat_ref_segment rows
         args = N.RefArgs(
             table=dt.handle, k=k, out_width=out.element_size(), seed=key0 & _M64, domain=0,
             block_size=1, edge_count=1, first_block=0, n_blocks=0, out=out.data_ptr(),
             samples_per_block=None,
             samples_total=samples_total.data_ptr() if samples_total is not None else None,
             post_flags=post_flags, kernel=N.KERNEL_PACKED_SMEM if thread else N.KERNEL_AUTO,
-            segments=dseg.data_ptr(), n_segments=len(segs))
+            segments=dseg.data_ptr(), n_segments=dseg.shape[0])
         N.check(N.lib().rmat_generate_refstream(ctypes.byref(args), stream_ptr),
                 "rmat_generate_refstream (segments)")
         # dseg may be freed now: the caching allocator only hands its memory to
         # later work on this same stream, which runs after the launch
 
 
-_REFSEG_DTYPE = np.dtype([("word_begin", "<u8"), ("out_row", "<u8"), ("count", "<u8"),
-                          ("lead", "<u4"), ("report_nf", "<u4"), ("stream", "<u8"),
-                          ("row_prefix", "<u8"), ("col_prefix", "<u8"), ("nf_origin", "<u8")])
+def _as_i64(x: int) -> int:
+    x &= _M64
+    return x - (1 << 64) if x >= 1 << 63 else x
+
 
 
 def replay_words(dt: DeviceTable, seed: int, domain: int, sid: int, count: int, start: int = 0):
