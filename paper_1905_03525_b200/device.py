@@ -139,7 +139,7 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
     import torch
 
     assert out.device == dt.device and out.is_contiguous()
-    if (kernel == N.KERNEL_AUTO and 0 < n_blocks <= LONG_STREAM_MAX_BLOCKS
+    if (kernel == N.KERNEL_AUTO and 0 < n_blocks <= _long_stream_max_blocks(dt)
             and min(block_size, edge_count - first_block * block_size) >= LONG_STREAM_EDGES
             and samples_per_block is None):
         # few long blocks: cut them into segments that run on many threads / CTAs
@@ -165,9 +165,17 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
                 "rmat_generate_refstream")
 
 
-#: a launch of at most this many reference blocks of at least LONG_STREAM_EDGES
-#: edges each runs every block in segment mode (one CTA per ~2^16 words)
-LONG_STREAM_MAX_BLOCKS = 16
+#: a launch of fewer reference blocks than the GPU has SMs (one CTA each would
+#: leave SMs idle), each of at least LONG_STREAM_EDGES edges, runs in segment mode
+LONG_STREAM_MAX_BLOCKS = None  # None: the device's SM count
+
+
+def _long_stream_max_blocks(dt) -> int:
+    import torch
+
+    if LONG_STREAM_MAX_BLOCKS is not None:
+        return LONG_STREAM_MAX_BLOCKS
+    return torch.cuda.get_device_properties(dt.device).multi_processor_count
 LONG_STREAM_EDGES = 1 << 15
 SEGMENT_WORDS = 1 << 18         # CTA per segment (tools/seg_probe2.py)
 THREAD_SEGMENT_WORDS = 1 << 14  # thread per segment
