@@ -12,6 +12,7 @@ parallel.
 from __future__ import annotations
 
 import os
+import threading
 from concurrent.futures import ThreadPoolExecutor, wait
 
 import numpy as np
@@ -24,23 +25,28 @@ STAGING_BYTES = 256 << 20
 _THREADS = max(2, min(32, os.cpu_count() or 4))
 _POOL: ThreadPoolExecutor | None = None
 _STAGING: dict = {}
+_LOCK = threading.Lock()  # guards _POOL / _STAGING creation
 
 
 def _pool() -> ThreadPoolExecutor:
     global _POOL
-    if _POOL is None:
-        _POOL = ThreadPoolExecutor(max_workers=_THREADS)
-    return _POOL
+    with _LOCK:
+        if _POOL is None:
+            _POOL = ThreadPoolExecutor(max_workers=_THREADS)
+        return _POOL
 
 
 def _staging(dev):
     import torch
 
     key = (dev.type, dev.index)
-    if key not in _STAGING:
-        bufs = [torch.empty(STAGING_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-        _STAGING[key] = (bufs, torch.cuda.Stream(dev), [torch.cuda.Event() for _ in range(2)])
-    return _STAGING[key]
+    with _LOCK:
+        if key not in _STAGING:
+            bufs = [torch.empty(STAGING_BYTES, dtype=torch.uint8, pin_memory=True)
+                    for _ in range(2)]
+            _STAGING[key] = (bufs, torch.cuda.Stream(dev), [torch.cuda.Event() for _ in range(2)],
+                             threading.Lock())
+        return _STAGING[key]
 
 
 def copy_to_host_u64(t, dst: np.ndarray) -> np.ndarray:
@@ -54,7 +60,14 @@ def copy_to_host_u64(t, dst: np.ndarray) -> np.ndarray:
         return dst
     width = t.element_size()
     src = t.contiguous().view(torch.int32 if width == 4 else torch.int64)
-    bufs, cs, evs = _staging(t.device)
+    bufs, cs, evs, busy = _staging(t.device)
+    with busy:  # one transfer at a time per device: the staging pair is shared
+        return _copy(t, src, width, rows, dst, bufs, cs, evs)
+
+
+def _copy(t, src, width, rows, dst, bufs, cs, evs):
+    import torch
+
     chunk = STAGING_BYTES // (2 * width)
     pool = _pool()
     nthreads = _THREADS

@@ -104,3 +104,19 @@ def test_gather_device_concatenates_shards(cuda):
     whole, _, _ = generate_shard(cfg)
     shards = [generate_shard(cfg, r, 3)[:2] for r in range(3)]
     assert torch.equal(gather_device(shards, cuda).view(torch.int32), whole.view(torch.int32))
+
+
+def test_generate_from_several_host_threads(cuda):
+    """The drop-in API is re-entrant: concurrent generate() calls (shared staging
+    buffers, table cache, thread pool) give the sequential results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cfgs = [GenConfig(params=params_for(G500, 20), table=table_for("v1024"),
+                      edge_count=300_000 + 7 * i, seed=i, rng=("reference" if i % 2 else
+                                                               "philox4x32"))
+            for i in range(6)]
+    want = [generate(c) for c in cfgs]
+    with ThreadPoolExecutor(6) as ex:
+        got = list(ex.map(generate, cfgs))
+    for w, g in zip(want, got):
+        assert (w == g).all()
