@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _native as N
 from .device import device_table, launch_generate, launch_refstream, replay_words, require_cuda
-from .params import MAX_K, BadExponent, RmatParams, check_k
+from .params import RmatParams, check_k
 from .table import FragmentTable
 
 __all__ = [
