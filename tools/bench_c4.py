@@ -24,6 +24,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--plan", choices=["balanced", "rows"], default="balanced")
     ap.add_argument("--rng", choices=["philox4x32", "reference"], default="philox4x32")
+    ap.add_argument("--t", type=int, default=3, help="tile bits (3: one tile row per part)")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     args = ap.parse_args()
@@ -43,7 +44,7 @@ def main() -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    parts, k, t, m = 8, 36, 3, 1 << 33
+    parts, k, t, m = 8, 36, args.t, 1 << 33
     pl = validate(0.45, 0.22, 0.22, 0.11, k)
     table = build_variable_table(pl, 1 << 14)
     plan = default_plan(k, t, m, 1, parts)
@@ -80,7 +81,7 @@ def main() -> None:
             "metric": "edges/sec", "value": m / float(tmax.item()), "unit": "edges/s",
             "n_gpus": world, "plan": args.plan, "rng": args.rng, "parts_per_rank": len(mine),
             "rank0_edges": rows, "seconds": float(tmax.item()),
-            "config": {"workload": "C4: less-skewed k=36 m=2^33 t=3, 8 parts, uint64 pairs",
+            "config": {"workload": f"C4: less-skewed k=36 m=2^33 t={t}, 8 parts, uint64 pairs",
                        "table_size": 1 << 14, "seed": 1}}), flush=True)
     if world > 1:
         dist.destroy_process_group()
