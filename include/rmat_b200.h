@@ -172,7 +172,10 @@ typedef struct {
   uint64_t nf_origin;
 } rmat_ref_segment;
 
-/* Depth sums of words [word_begin + s*L, word_begin + (s+1)*L) for s in
+/* Segment mode replaces one long `_emit(comp, k - t, count, gen)` per tile
+ * (partition.py:154; generator.py:235-290) -- a sequential stream -- with
+ * independent pieces whose starting bit offsets come from these sums.
+ * Depth sums of words [word_begin + s*L, word_begin + (s+1)*L) for s in
  * [0, n_segments) of the reference stream keyed [key0, key1], written to
  * sums[s] (device) -- the scan input for a segment table. */
 rmat_status rmat_refstream_segment_depths(const rmat_table* table, uint64_t key0, uint64_t key1,
