@@ -130,9 +130,10 @@ rmat::GenericTab generic_view(const rmat_table* t) {
   return g;
 }
 
-template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false>
+template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
+          bool W64 = false>
 rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF>;
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64>;
   const int sms = num_sms(t->device);
   int threads, blocks;
   size_t smem = 0;
@@ -207,6 +208,21 @@ rmat_status launch_ref_thread(const rmat_table* t, const rmat::GenLaunch& g, boo
                  : launch_ref_thread_c<false, true, false>(t, g, st);
   return count ? launch_ref_thread_c<false, false, true>(t, g, st)
                : launch_ref_thread_c<false, false, false>(t, g, st);
+}
+
+// 33 < k <= 48 with 16-bit fragments staged in shared memory: 64-bit accumulators
+template <bool PREFIX, bool COUNT>
+rmat_status launch_w64_c(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
+  return (g.post & RMAT_POST_UNDIRECTED)
+             ? launch_packed_t<16, true, true, PREFIX, COUNT, true, false, true>(t, g, st)
+             : launch_packed_t<16, true, true, PREFIX, COUNT, false, false, true>(t, g, st);
+}
+
+rmat_status launch_w64(const rmat_table* t, const rmat::GenLaunch& g, bool prefix, bool count,
+                       cudaStream_t st) {
+  if (prefix)
+    return count ? launch_w64_c<true, true>(t, g, st) : launch_w64_c<true, false>(t, g, st);
+  return count ? launch_w64_c<false, true>(t, g, st) : launch_w64_c<false, false>(t, g, st);
 }
 
 rmat_status launch_generic(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
@@ -412,10 +428,15 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
   // 32-bit Philox call index: E * k / dmin samples < 2^34.
   const bool packed_ok = t->fb != 0 && t->dmax <= a->k && a->k <= 33 &&
                          (double)E * a->k / t->dmin < 17179869184.0;
+  // 33 < k <= 48: the shared-memory packed kernel with 64-bit accumulators
+  const bool w64 = !packed_ok && t->fb == 16 && t->packed_smem && t->dmax <= a->k &&
+                   a->k > 33 && a->k <= 48 && a->out_width == 8 &&
+                   (double)E * a->k / t->dmin < 17179869184.0;
   if (kernel == RMAT_KERNEL_AUTO)
     kernel = packed_ok ? (t->packed_smem ? RMAT_KERNEL_PACKED_SMEM : RMAT_KERNEL_PACKED_GLOBAL)
+             : w64     ? RMAT_KERNEL_PACKED_SMEM
                        : RMAT_KERNEL_GENERIC;
-  if ((kernel == RMAT_KERNEL_PACKED_SMEM && !(packed_ok && t->packed_smem)) ||
+  if ((kernel == RMAT_KERNEL_PACKED_SMEM && !((packed_ok && t->packed_smem) || w64)) ||
       (kernel == RMAT_KERNEL_PACKED_GLOBAL && !packed_ok) || kernel < 0 || kernel > 3)
     return RMAT_ERR_UNSUPPORTED;
   if (a->kernel_used) *a->kernel_used = kernel;
@@ -459,8 +480,9 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
     rmat_status rs;
     switch (kernel) {
       case RMAT_KERNEL_PACKED_SMEM:
-        rs = t->fb == 16 ? launch_packed_fb<16, true>(t, g, out64, prefix, count, st)
-                         : launch_packed_fb<32, true>(t, g, out64, prefix, count, st);
+        rs = w64           ? launch_w64(t, g, prefix, count, st)
+             : t->fb == 16 ? launch_packed_fb<16, true>(t, g, out64, prefix, count, st)
+                           : launch_packed_fb<32, true>(t, g, out64, prefix, count, st);
         break;
       case RMAT_KERNEL_PACKED_GLOBAL:
         rs = t->fb == 16 ? launch_packed_fb<16, false>(t, g, out64, prefix, count, st)

@@ -266,13 +266,15 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 // TLO.  One thread walks one whole block, so the output equals
 // rmatgen.generate() byte for byte with the fast path's emission machinery
 // (used when there are enough blocks to fill the GPU).
-template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF>
+// W64: 33 < k <= 48 -- 64-bit accumulators (f + d <= 47 + 16 = 63 bits), uint64 output.
 #ifndef RMAT_GLOBAL_MINB
 #define RMAT_GLOBAL_MINB 1
 #endif
 #ifndef RMAT_GLOBAL_CPI
 #define RMAT_GLOBAL_CPI RMAT_CALLS_PER_ITER
 #endif
+template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF,
+          bool W64 = false>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
@@ -360,6 +362,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
   uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
   uint32_t cur_r = 0, cur_c = 0, f = REF ? p.lead : 0u;
+  uint64_t cur_r64 = 0, cur_c64 = 0;  // W64 accumulators
+  const uint64_t kmask64 = k >= 64 ? ~0ull : ((1ull << k) - 1);
   uint64_t total_nf = 0;
   uint32_t ebits = 0;                // COUNT: samples of the current call that produced an edge
   // Output bookkeeping.  stage + roff = ring slot of the next edge (roff =
@@ -464,48 +468,63 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         c = lt ? cb.a[t].z : cb.a[t].w;
       }
       const uint32_t d = prmt(cb.b[t], cb.seld[t]);
-      // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
-      const uint32_t tt = f + d;
-      uint32_t vr, vrh, vc, vch;
-#ifndef RMAT_REF_SHIFT_APPEND
-#define RMAT_REF_SHIFT_APPEND 1
-#endif
-      if constexpr (REF && RMAT_REF_SHIFT_APPEND) {
-        // numpy's Philox4x64 keeps the FMA pipe busy: append with ALU shifts
-        vr = (cur_r << d) | r;
-        vrh = __funnelshift_l(cur_r, 0u, d);
-        vc = (cur_c << d) | c;
-        vch = __funnelshift_l(cur_c, 0u, d);
-      } else {
-        // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
-        const uint32_t pw = 1u << d;
-        vr = mad_lo(cur_r, pw, r);
-        vrh = mul_hi(cur_r, pw);
-        vc = mad_lo(cur_c, pw, c);
-        vch = mul_hi(cur_c, pw);
-      }
-      const bool emit = tt >= k;
-      const uint32_t over = emit ? tt - k : tt;
-      cur_r = vr;
-      cur_c = vc;
-      f = over;
-      const bool st = CAREFUL ? (emit && left != 0) : emit;
+      bool st;
       uint64_t u, v;
-      if constexpr (OUT64) {
-        // (hi:lo) halves, each one LOP3 (a & b) | prefix: bit 32 of a 33-bit
-        // edge comes from the high accumulator word (hmask = 1 iff k = 33)
-        const uint32_t rlo = PREFIX ? (uint32_t)p.rpre : 0u, rhi = PREFIX ? (uint32_t)(p.rpre >> 32) : 0u;
-        const uint32_t clo = PREFIX ? (uint32_t)p.cpre : 0u, chi = PREFIX ? (uint32_t)(p.cpre >> 32) : 0u;
-        u = ((uint64_t)and_or(vrh >> over, hmask, rhi) << 32) |
-            and_or(__funnelshift_r(vr, vrh, over), kmask, rlo);
-        v = ((uint64_t)and_or(vch >> over, hmask, chi) << 32) |
-            and_or(__funnelshift_r(vc, vch, over), kmask, clo);
-      } else if constexpr (PREFIX) {
-        u = and_or(__funnelshift_r(vr, vrh, over), kmask, (uint32_t)p.rpre);
-        v = and_or(__funnelshift_r(vc, vch, over), kmask, (uint32_t)p.cpre);
+      if constexpr (W64) {
+        // 64-bit accumulators: V = cur << d | bits, edge = (V >> over) & kmask
+        const uint32_t tt = f + d;
+        const uint64_t vr64 = (cur_r64 << d) | r, vc64 = (cur_c64 << d) | c;
+        const bool emit = tt >= k;
+        const uint32_t over = emit ? tt - k : tt;
+        cur_r64 = vr64;
+        cur_c64 = vc64;
+        f = over;
+        st = CAREFUL ? (emit && left != 0) : emit;
+        u = ((vr64 >> over) & kmask64) | (PREFIX ? p.rpre : 0ull);
+        v = ((vc64 >> over) & kmask64) | (PREFIX ? p.cpre : 0ull);
       } else {
-        u = __funnelshift_r(vr, vrh, over) & kmask;
-        v = __funnelshift_r(vc, vch, over) & kmask;
+        // Append d bits: V = cur * 2^d + bits, as (hi, lo) 32-bit halves.
+        const uint32_t tt = f + d;
+        uint32_t vr, vrh, vc, vch;
+  #ifndef RMAT_REF_SHIFT_APPEND
+  #define RMAT_REF_SHIFT_APPEND 1
+  #endif
+        if constexpr (REF && RMAT_REF_SHIFT_APPEND) {
+          // numpy's Philox4x64 keeps the FMA pipe busy: append with ALU shifts
+          vr = (cur_r << d) | r;
+          vrh = __funnelshift_l(cur_r, 0u, d);
+          vc = (cur_c << d) | c;
+          vch = __funnelshift_l(cur_c, 0u, d);
+        } else {
+          // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
+          const uint32_t pw = 1u << d;
+          vr = mad_lo(cur_r, pw, r);
+          vrh = mul_hi(cur_r, pw);
+          vc = mad_lo(cur_c, pw, c);
+          vch = mul_hi(cur_c, pw);
+        }
+        const bool emit = tt >= k;
+        const uint32_t over = emit ? tt - k : tt;
+        cur_r = vr;
+        cur_c = vc;
+        f = over;
+        st = CAREFUL ? (emit && left != 0) : emit;
+        if constexpr (OUT64) {
+          // (hi:lo) halves, each one LOP3 (a & b) | prefix: bit 32 of a 33-bit
+          // edge comes from the high accumulator word (hmask = 1 iff k = 33)
+          const uint32_t rlo = PREFIX ? (uint32_t)p.rpre : 0u, rhi = PREFIX ? (uint32_t)(p.rpre >> 32) : 0u;
+          const uint32_t clo = PREFIX ? (uint32_t)p.cpre : 0u, chi = PREFIX ? (uint32_t)(p.cpre >> 32) : 0u;
+          u = ((uint64_t)and_or(vrh >> over, hmask, rhi) << 32) |
+              and_or(__funnelshift_r(vr, vrh, over), kmask, rlo);
+          v = ((uint64_t)and_or(vch >> over, hmask, chi) << 32) |
+              and_or(__funnelshift_r(vc, vch, over), kmask, clo);
+        } else if constexpr (PREFIX) {
+          u = and_or(__funnelshift_r(vr, vrh, over), kmask, (uint32_t)p.rpre);
+          v = and_or(__funnelshift_r(vc, vch, over), kmask, (uint32_t)p.cpre);
+        } else {
+          u = __funnelshift_r(vr, vrh, over) & kmask;
+          v = __funnelshift_r(vc, vch, over) & kmask;
+        }
       }
       if constexpr (UND) {
         if constexpr (OUT64) {
@@ -605,6 +624,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       stream_keys();
       if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
       j = 0; cur_r = cur_c = 0; f = REF ? p.lead : 0u;
+      cur_r64 = cur_c64 = 0;
       L = (uint32_t)p.left;
       roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
       half = roff / (G * STRIDE);

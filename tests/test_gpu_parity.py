@@ -266,3 +266,24 @@ def test_reference_stream_segment_mode(cuda, tag, k, count, L, w0, mode):
     got = got.view(np.uint32).astype(np.uint64) if k <= 32 else got.view(np.uint64)
     assert (got == want).all()
     assert int(tot.item()) == nf
+
+
+@pytest.mark.parametrize("k", [34, 36, 41, 48])
+@pytest.mark.parametrize("block", [1024, 1021])
+def test_packed_w64_matches_generic_and_oracle(cuda, k, block):
+    """33 < k <= 48 runs the shared-memory packed kernel with 64-bit accumulators."""
+    table = table_for("v16384")
+    cfg = GenConfig(params=params_for(G500, k), table=table, edge_count=200_003, seed=11,
+                    block_size=block)
+    used = []
+    a, _, sa = generate_shard(cfg, count_samples=True)
+    b, _, sb = generate_shard(cfg, kernel=N.KERNEL_GENERIC, count_samples=True)
+    assert torch.equal(a.view(torch.int64), b.view(torch.int64))
+    assert int(sa.item()) == int(sb.item())
+    want, _ = oracle.fast_stream(oracle_table("v16384"), k, block, 11, 7)
+    got = a.view(torch.int64)[7 * block:8 * block].cpu().numpy().view(np.uint64)
+    assert (got == want).all()
+    dt = device_table(table, cuda)
+    assert launch_generate(dt, k, 11, DOMAIN_BLOCK, block, [(0, 4096, 0, 0, 0)],
+                           torch.empty((4096, 2), dtype=torch.uint64, device=cuda)) == \
+        N.KERNEL_PACKED_SMEM
