@@ -32,7 +32,9 @@ struct rmat_table {
   uint64_t* col;
   uint8_t* depth;
   // packed layout (optional)
-  uint32_t fb;  // 0 = absent
+  uint32_t fb;  // 0 = absent (scheme P tables only)
+  uint32_t gpacked;  // 1: the packed layout was built for a scheme-G (non power of two) table
+  uint64_t fastmod_m;  // ceil(2^64 / n): exact bucket = hi mod n (scheme G)
   uint32_t* pB;
   void* pA;
   uint32_t* ptlo;
@@ -109,9 +111,10 @@ rmat::PackedTab packed_view(const rmat_table* t) {
   p.A = t->pA;
   p.tlo = t->ptlo;
   p.idxmask4 = (uint32_t)((t->n - 1) << 2);
-  p.fm = (1u << rmat::scheme_p_fbits(t->lg)) - 1u;
+  p.fm = t->gpacked ? 0xFFFFu : (1u << rmat::scheme_p_fbits(t->lg)) - 1u;
   p.n = (uint32_t)t->n;
-  p.fb = t->fb;
+  p.fb = t->gpacked ? 16 : t->fb;
+  p.fastmod_m = t->fastmod_m;
   p.one = 1;
   p.zero = 0;
   return p;
@@ -131,9 +134,9 @@ rmat::GenericTab generic_view(const rmat_table* t) {
 }
 
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
-          bool W64 = false>
+          bool W64 = false, bool SG = false>
 rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64>;
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG>;
   const int sms = num_sms(t->device);
   int threads, blocks;
   size_t smem = 0;
@@ -225,6 +228,26 @@ rmat_status launch_w64(const rmat_table* t, const rmat::GenLaunch& g, bool prefi
   return count ? launch_w64_c<false, true>(t, g, st) : launch_w64_c<false, false>(t, g, st);
 }
 
+// scheme-G (non power of two) tables with 16-bit fragments in shared memory
+template <bool OUT64, bool PREFIX, bool COUNT>
+rmat_status launch_sg_c(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
+  return (g.post & RMAT_POST_UNDIRECTED)
+             ? launch_packed_t<16, true, OUT64, PREFIX, COUNT, true, false, false, true>(t, g, st)
+             : launch_packed_t<16, true, OUT64, PREFIX, COUNT, false, false, false, true>(t, g, st);
+}
+
+rmat_status launch_sg(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
+                      bool count, cudaStream_t st) {
+  if (out64) {
+    if (prefix)
+      return count ? launch_sg_c<true, true, true>(t, g, st) : launch_sg_c<true, true, false>(t, g, st);
+    return count ? launch_sg_c<true, false, true>(t, g, st) : launch_sg_c<true, false, false>(t, g, st);
+  }
+  if (prefix)
+    return count ? launch_sg_c<false, true, true>(t, g, st) : launch_sg_c<false, true, false>(t, g, st);
+  return count ? launch_sg_c<false, false, true>(t, g, st) : launch_sg_c<false, false, false>(t, g, st);
+}
+
 rmat_status launch_generic(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
                            cudaStream_t st) {
   const int threads = 256;
@@ -307,12 +330,16 @@ rmat_status rmat_table_create(int device, const rmat_table_desc* d, rmat_table**
     return st;
   }
 
-  // Packed bucket layout (scheme P; see rmat_device.cuh).
+  // Packed bucket layout (see rmat_device.cuh): scheme P tables with 16- or
+  // 32-bit fragments; scheme G (other sizes) tables with 16-bit fragments,
+  // whose samples carry a full 32-bit fraction (F = 16, ties from the word).
   uint32_t fb = 0;
+  const bool g_pack = !t->scheme_p && n >= 2 && n < (1ull << 32) && dmax <= 16;
   if (t->scheme_p && lg >= 2 && dmax <= 16) fb = 16;
   else if (t->scheme_p && dmax <= 31) fb = 32;
+  else if (g_pack) fb = 16;
   if (fb) {
-    const uint32_t fm = (1u << rmat::scheme_p_fbits(lg)) - 1u;
+    const uint32_t fm = g_pack ? 0xFFFFu : (1u << rmat::scheme_p_fbits(lg)) - 1u;
     std::vector<uint32_t> B(n), tlo(n);
     for (uint64_t i = 0; i < n; ++i) {
       const uint32_t a = al[i];
@@ -344,8 +371,15 @@ rmat_status rmat_table_create(int device, const rmat_table_desc* d, rmat_table**
       t->pA = dA;
     }
     if (st) { free_table(t); return st; }
-    t->fb = fb;
-    t->packed_bytes = n * (fb == 16 ? 12ull : 20ull);
+    if (g_pack) {  // kept apart from `fb`: every scheme-P packed path checks fb
+      t->gpacked = 1;
+      t->fastmod_m = ~0ull / n + 1;
+      fb = 16;
+    } else {
+      t->fb = fb;
+    }
+    // shared-memory image: A and B each padded to 16 bytes (rmat_kernels.cuh)
+    t->packed_bytes = ((n * (fb == 16 ? 8ull : 16ull) + 15) & ~15ull) + ((n * 4 + 15) & ~15ull);
     t->packed_smem =
         t->packed_bytes + (uint64_t)rmat::kSmemStrideThreads * rmat::kRingBytes <=
             (uint64_t)max_smem_optin(device) ? 1u : 0u;
@@ -428,15 +462,18 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
   // 32-bit Philox call index: E * k / dmin samples < 2^34.
   const bool packed_ok = t->fb != 0 && t->dmax <= a->k && a->k <= 33 &&
                          (double)E * a->k / t->dmin < 17179869184.0;
+  // scheme-G tables (size not a power of two) with 16-bit fragments in shared memory
+  const bool sg = t->gpacked && t->packed_smem && t->dmax <= a->k && a->k <= 33 &&
+                  (double)E * a->k / t->dmin < 8589934592.0;
   // 33 < k <= 48: the shared-memory packed kernel with 64-bit accumulators
   const bool w64 = !packed_ok && t->fb == 16 && t->packed_smem && t->dmax <= a->k &&
                    a->k > 33 && a->k <= 48 && a->out_width == 8 &&
                    (double)E * a->k / t->dmin < 17179869184.0;
   if (kernel == RMAT_KERNEL_AUTO)
     kernel = packed_ok ? (t->packed_smem ? RMAT_KERNEL_PACKED_SMEM : RMAT_KERNEL_PACKED_GLOBAL)
-             : w64     ? RMAT_KERNEL_PACKED_SMEM
-                       : RMAT_KERNEL_GENERIC;
-  if ((kernel == RMAT_KERNEL_PACKED_SMEM && !((packed_ok && t->packed_smem) || w64)) ||
+             : (w64 || sg) ? RMAT_KERNEL_PACKED_SMEM
+                           : RMAT_KERNEL_GENERIC;
+  if ((kernel == RMAT_KERNEL_PACKED_SMEM && !((packed_ok && t->packed_smem) || w64 || sg)) ||
       (kernel == RMAT_KERNEL_PACKED_GLOBAL && !packed_ok) || kernel < 0 || kernel > 3)
     return RMAT_ERR_UNSUPPORTED;
   if (a->kernel_used) *a->kernel_used = kernel;
@@ -480,7 +517,8 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
     rmat_status rs;
     switch (kernel) {
       case RMAT_KERNEL_PACKED_SMEM:
-        rs = w64           ? launch_w64(t, g, prefix, count, st)
+        rs = sg            ? launch_sg(t, g, out64, prefix, count, st)
+             : w64         ? launch_w64(t, g, prefix, count, st)
              : t->fb == 16 ? launch_packed_fb<16, true>(t, g, out64, prefix, count, st)
                            : launch_packed_fb<32, true>(t, g, out64, prefix, count, st);
         break;

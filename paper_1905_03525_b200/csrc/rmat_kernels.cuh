@@ -273,8 +273,11 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 #ifndef RMAT_GLOBAL_CPI
 #define RMAT_GLOBAL_CPI RMAT_CALLS_PER_ITER
 #endif
+// SG: scheme-G tables (size not a power of two): sample i = words (hi, lo) of
+// Philox call i/2 (pairs of the 4 outputs), bucket = hi mod n (exact fastmod),
+// fraction = lo -- a full 32-bit fraction, so ties are settled from the word.
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF,
-          bool W64 = false>
+          bool W64 = false, bool SG = false>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
@@ -294,16 +297,22 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     const uint32_t n = tab.n;
     const size_t abytes = (size_t)n * sizeof(AE);
     const size_t bbytes = (size_t)n * 4;
+    // 16-byte aligned sections (n need not be a multiple of 4 for scheme-G tables)
+    const size_t boff = (abytes + 15) & ~(size_t)15, soff = (boff + bbytes + 15) & ~(size_t)15;
     const uint4* srcA = reinterpret_cast<const uint4*>(tab.A);
     uint4* dstA = reinterpret_cast<uint4*>(smem);
     for (size_t i = threadIdx.x; i < abytes / 16; i += THREADS) dstA[i] = __ldg(srcA + i);
     const uint4* srcB = reinterpret_cast<const uint4*>(tab.B);
-    uint4* dstB = reinterpret_cast<uint4*>(smem + abytes);
+    uint4* dstB = reinterpret_cast<uint4*>(smem + boff);
     for (size_t i = threadIdx.x; i < bbytes / 16; i += THREADS) dstB[i] = __ldg(srcB + i);
+    for (size_t i = abytes / 16 * 4 + threadIdx.x; i < abytes / 4; i += THREADS)  // tails
+      reinterpret_cast<uint32_t*>(smem)[i] = __ldg(reinterpret_cast<const uint32_t*>(tab.A) + i);
+    for (size_t i = bbytes / 16 * 4 + threadIdx.x; i < n; i += THREADS)
+      reinterpret_cast<uint32_t*>(smem + boff)[i] = __ldg(tab.B + i);
     __syncthreads();
     baseA = smem;
-    baseB = smem + abytes;
-    stage = smem + abytes + bbytes;
+    baseB = smem + boff;
+    stage = smem + soff;
   } else {
     baseA = reinterpret_cast<const uint8_t*>(tab.A);
     baseB = reinterpret_cast<const uint8_t*>(tab.B);
@@ -401,6 +410,19 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         q.w[t] = (uint32_t)ww[t];
         q.x[t] = ((uint32_t)(ww[t] >> 32) << 2) & idxmask4;
       }
+    } else if constexpr (SG) {
+      // four samples = calls 2jj and 2jj+1, two (hi, lo) pairs each
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const u32x4 w4 = philox4x32_10_pre(2 * jj + h, pre, rk);
+        const uint32_t his[2] = {w4.x, w4.z}, los[2] = {w4.y, w4.w};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint64_t low = tab.fastmod_m * his[e];  // Lemire: hi mod n, exact
+          q.x[2 * h + e] = (uint32_t)__umul64hi(low, (uint64_t)tab.n) << 2;
+          q.w[2 * h + e] = los[e];
+        }
+      }
     } else {
       // primary call: rounds 1-2 partly precomputed per stream (philox.cuh)
       const u32x4 w4 = philox4x32_10_pre(jj, pre, rk);
@@ -408,7 +430,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const uint32_t a4 = REF ? q.x[t] : (q.w[t] & idxmask4);
+      const uint32_t a4 = (REF || SG) ? q.x[t] : (q.w[t] & idxmask4);
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
       q.a[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
     }
@@ -431,7 +453,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // Rare (2^-(32-F) per sample): decide fraction ties with the lazy word.
   auto resolve_ties = [&](Batch& cb, uint32_t jj) {
     if (!cb.tie) return;
-    if constexpr (REF) {  // the reference word carries its full fraction
+    if constexpr (REF || SG) {  // the word carries its full 32-bit fraction
 #pragma unroll
       for (int t = 0; t < 4; ++t)
         if ((uint32_t)mad_wide(cb.w[t] | fm, one, cb.b[t]) <= fm) {
@@ -583,7 +605,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #ifndef RMAT_WIDE_CPI
 #define RMAT_WIDE_CPI 1
 #endif
-    constexpr int CPI = (SMEM && FB == 32) ? 1
+    constexpr int CPI = (SG || (SMEM && FB == 32)) ? 1
                         : (SMEM && (PREFIX || OUT64)) ? RMAT_WIDE_CPI
                         : REF ? RMAT_REF_CPI
                         : !SMEM ? RMAT_GLOBAL_CPI : RMAT_CALLS_PER_ITER;

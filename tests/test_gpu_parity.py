@@ -287,3 +287,29 @@ def test_packed_w64_matches_generic_and_oracle(cuda, k, block):
     assert launch_generate(dt, k, 11, DOMAIN_BLOCK, block, [(0, 4096, 0, 0, 0)],
                            torch.empty((4096, 2), dtype=torch.uint64, device=cuda)) == \
         N.KERNEL_PACKED_SMEM
+
+
+@pytest.mark.parametrize("tag", ["v253", "v1021", "v8191"])
+@pytest.mark.parametrize("k,block", [(16, 1024), (28, 1021), (33, 512), (13, 7)])
+def test_packed_scheme_g_tables(cuda, tag, k, block):
+    """Table sizes that are not powers of two (e.g. build_variable_table(., 2^13) -> 8191
+    entries) run the packed kernel with two-word samples and an exact fastmod bucket."""
+    from paper_1905_03525_b200.generator import edge_dtype
+
+    table = table_for(tag)
+    if int(table.depths.max()) > k:
+        pytest.skip("depth > k takes the generic kernel")
+    cfg = GenConfig(params=params_for(G500, k), table=table, edge_count=150_001, seed=21,
+                    block_size=block)
+    a, _, sa = generate_shard(cfg, count_samples=True)
+    b, _, sb = generate_shard(cfg, kernel=N.KERNEL_GENERIC, count_samples=True)
+    wide = torch.int32 if k <= 32 else torch.int64
+    assert torch.equal(a.view(wide), b.view(wide)) and int(sa.item()) == int(sb.item())
+    got = a.view(wide)[5 * block:6 * block].cpu().numpy()
+    got = got.view(np.uint32).astype(np.uint64) if k <= 32 else got.view(np.uint64)
+    want, _ = oracle.fast_stream(oracle_table(tag), k, block, 21, 5)
+    assert (got == want).all()
+    dt = device_table(table, cuda)
+    assert launch_generate(dt, k, 21, DOMAIN_BLOCK, block, [(0, 64, 0, 0, 0)],
+                           torch.empty((64, 2), dtype=edge_dtype(k), device=cuda)) == \
+        N.KERNEL_PACKED_SMEM
