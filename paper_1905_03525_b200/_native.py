@@ -14,12 +14,39 @@ from functools import lru_cache
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.environ.get("RMAT_LIB") or os.path.join(_PKG, "_build", "librmat_b200.so")
-_SOURCES = [os.path.join(_PKG, "csrc", f) for f in
-            ("rmat_capi.cu", "rmat_kernels.cuh", "rmat_refstream.cuh", "rmat_device.cuh",
-             "rmat_post.cuh", "philox.cuh")] + [os.path.join(_ROOT, "include", "rmat_b200.h")]
+#: translation units of librmat_b200.so, compiled in parallel (rmat_internal.cuh)
+_UNITS = ("rmat_capi.cu", "rmat_packed16.cu", "rmat_packed32.cu", "rmat_packed_extra.cu")
+_SOURCES = ([os.path.join(_PKG, "csrc", f) for f in os.listdir(os.path.join(_PKG, "csrc"))
+             if f.endswith((".cu", ".cuh"))] + [os.path.join(_ROOT, "include", "rmat_b200.h")])
 
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+
+
+def _compile_units(out: str, defines=()) -> str:
+    """nvcc every unit to an object in parallel, then link the shared library."""
+    import tempfile
+
+    with tempfile.TemporaryDirectory(prefix="rmat_build_") as tmpd:
+        procs = []
+        for u in _UNITS:
+            obj = os.path.join(tmpd, u.replace(".cu", ".o"))
+            cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c",
+                   os.path.join(_PKG, "csrc", u), "-o", obj]
+            procs.append((obj, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                                stderr=subprocess.PIPE, text=True)))
+        logs = []
+        for obj, pr in procs:
+            _, err = pr.communicate()
+            if pr.returncode != 0:
+                raise RuntimeError(f"nvcc failed:\n{err}")
+            logs.append(err)
+        link = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+                *[obj for obj, _ in procs], "-o", out]
+        res = subprocess.run(link, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc link failed:\n{res.stderr}")
+    return "\n".join(logs)
 
 
 class NativeUnavailable(RuntimeError):
@@ -40,23 +67,16 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         return LIB_PATH  # an explicitly chosen prebuilt library (experiments)
     if out is not None:
         os.makedirs(os.path.dirname(out), exist_ok=True)
-        cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines],
-               os.path.join(_PKG, "csrc", "rmat_capi.cu"), "-o", out]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError(f"nvcc failed:\n{res.stderr}")
+        _compile_units(out, defines)
         return out
     newest = max(os.path.getmtime(p) for p in _SOURCES)
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
     os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
     tmp = LIB_PATH + ".tmp"
-    cmd = ["nvcc", *NVCC_FLAGS, os.path.join(_PKG, "csrc", "rmat_capi.cu"), "-o", tmp]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{res.stderr}")
+    log = _compile_units(tmp, defines)
     if verbose:
-        print(res.stderr)
+        print(log)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

@@ -14,34 +14,57 @@
 #include "../../include/rmat_b200.h"
 #include "philox.cuh"
 #include "rmat_device.cuh"
+#include "rmat_internal.cuh"
 #include "rmat_kernels.cuh"
 #include "rmat_post.cuh"
 #include "rmat_refstream.cuh"
 #include "rmat_dedup.cuh"
 #include "rmat_naive.cuh"
 
-struct rmat_table {
-  int device;
-  uint64_t n;
-  uint32_t dmin, dmax;
-  uint32_t scheme_p, lg;
-  // generic layout
-  uint32_t* T;
-  uint32_t* alias;
-  uint64_t* row;
-  uint64_t* col;
-  uint8_t* depth;
-  // packed layout (optional)
-  uint32_t fb;  // 0 = absent (scheme P tables only)
-  uint32_t gpacked;  // 1: the packed layout was built for a scheme-G (non power of two) table
-  uint64_t fastmod_m;  // ceil(2^64 / n): exact bucket = hi mod n (scheme G)
-  uint32_t* pB;
-  void* pA;
-  uint32_t* ptlo;
-  uint64_t packed_bytes;
-  uint32_t packed_smem;
-  uint64_t device_bytes;
-};
+
+
+namespace rmat_impl {
+
+int max_smem_optin(int dev) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v;
+}
+int num_sms(int dev) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
+rmat::PackedTab packed_view(const rmat_table* t) {
+  rmat::PackedTab p;
+  p.B = t->pB;
+  p.A = t->pA;
+  p.tlo = t->ptlo;
+  p.idxmask4 = (uint32_t)((t->n - 1) << 2);
+  p.fm = t->gpacked ? 0xFFFFu : (1u << rmat::scheme_p_fbits(t->lg)) - 1u;
+  p.n = (uint32_t)t->n;
+  p.fb = t->gpacked ? 16 : t->fb;
+  p.fastmod_m = t->fastmod_m;
+  p.one = 1;
+  p.zero = 0;
+  return p;
+}
+rmat::GenericTab generic_view(const rmat_table* t) {
+  rmat::GenericTab g;
+  g.T = t->T;
+  g.alias = t->alias;
+  g.row = t->row;
+  g.col = t->col;
+  g.depth = t->depth;
+  g.n = (uint32_t)t->n;
+  g.scheme_p = t->scheme_p;
+  g.lg = t->lg;
+  return g;
+}
+
+}  // namespace rmat_impl
+
+using namespace rmat_impl;
 
 namespace {
 
@@ -93,160 +116,9 @@ void free_table(rmat_table* t) {
   delete t;
 }
 
-int max_smem_optin(int dev) {
-  int v = 0;
-  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  return v;
-}
 
-int num_sms(int dev) {
-  int v = 0;
-  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-  return v;
-}
 
-rmat::PackedTab packed_view(const rmat_table* t) {
-  rmat::PackedTab p;
-  p.B = t->pB;
-  p.A = t->pA;
-  p.tlo = t->ptlo;
-  p.idxmask4 = (uint32_t)((t->n - 1) << 2);
-  p.fm = t->gpacked ? 0xFFFFu : (1u << rmat::scheme_p_fbits(t->lg)) - 1u;
-  p.n = (uint32_t)t->n;
-  p.fb = t->gpacked ? 16 : t->fb;
-  p.fastmod_m = t->fastmod_m;
-  p.one = 1;
-  p.zero = 0;
-  return p;
-}
 
-rmat::GenericTab generic_view(const rmat_table* t) {
-  rmat::GenericTab g;
-  g.T = t->T;
-  g.alias = t->alias;
-  g.row = t->row;
-  g.col = t->col;
-  g.depth = t->depth;
-  g.n = (uint32_t)t->n;
-  g.scheme_p = t->scheme_p;
-  g.lg = t->lg;
-  return g;
-}
-
-template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
-          bool W64 = false, bool SG = false>
-rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG>;
-  const int sms = num_sms(t->device);
-  int threads, blocks;
-  size_t smem = 0;
-  if (SMEM) {
-    threads = rmat::kSmemThreads;
-    smem = t->packed_bytes + (size_t)rmat::kSmemStrideThreads * rmat::kRingBytes;
-    blocks = sms;
-  } else {
-    threads = rmat::kGlobalThreads;
-    smem = (size_t)threads * rmat::kRingBytes;
-  }
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return RMAT_ERR_CUDA;
-  if (!SMEM) {
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess)
-      return RMAT_ERR_CUDA;
-    blocks = sms * std::max(per_sm, 1);
-  }
-  uint64_t need = (g.total_streams + threads - 1) / threads;
-  blocks = (int)std::min<uint64_t>((uint64_t)blocks, std::max<uint64_t>(need, 1));
-  kern<<<blocks, threads, smem, st>>>(packed_view(t), g);
-  return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
-}
-
-template <int FB, bool SMEM, bool UND>
-rmat_status launch_packed_fu(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
-                             bool count, cudaStream_t st) {
-  if (out64) {
-    if (prefix)
-      return count ? launch_packed_t<FB, SMEM, true, true, true, UND>(t, g, st)
-                   : launch_packed_t<FB, SMEM, true, true, false, UND>(t, g, st);
-    return count ? launch_packed_t<FB, SMEM, true, false, true, UND>(t, g, st)
-                 : launch_packed_t<FB, SMEM, true, false, false, UND>(t, g, st);
-  }
-  if (prefix)
-    return count ? launch_packed_t<FB, SMEM, false, true, true, UND>(t, g, st)
-                 : launch_packed_t<FB, SMEM, false, true, false, UND>(t, g, st);
-  return count ? launch_packed_t<FB, SMEM, false, false, true, UND>(t, g, st)
-               : launch_packed_t<FB, SMEM, false, false, false, UND>(t, g, st);
-}
-
-template <int FB, bool SMEM>
-rmat_status launch_packed_fb(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
-                             bool count, cudaStream_t st) {
-  return (g.post & RMAT_POST_UNDIRECTED)
-             ? launch_packed_fu<FB, SMEM, true>(t, g, out64, prefix, count, st)
-             : launch_packed_fu<FB, SMEM, false>(t, g, out64, prefix, count, st);
-}
-
-// Reference blocks through the per-thread fast-path machinery (k_packed<..., REF>):
-// one thread per reference block; packed 16-bit buckets in shared memory.
-template <bool OUT64, bool PREFIX, bool COUNT>
-rmat_status launch_ref_thread_c(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  return (g.post & RMAT_POST_UNDIRECTED)
-             ? launch_packed_t<16, true, OUT64, PREFIX, COUNT, true, true>(t, g, st)
-             : launch_packed_t<16, true, OUT64, PREFIX, COUNT, false, true>(t, g, st);
-}
-
-rmat_status launch_ref_thread(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
-                              bool prefix, bool count, cudaStream_t st) {
-  if (out64) {
-    if (prefix)
-      return count ? launch_ref_thread_c<true, true, true>(t, g, st)
-                   : launch_ref_thread_c<true, true, false>(t, g, st);
-    return count ? launch_ref_thread_c<true, false, true>(t, g, st)
-                 : launch_ref_thread_c<true, false, false>(t, g, st);
-  }
-  if (prefix)
-    return count ? launch_ref_thread_c<false, true, true>(t, g, st)
-                 : launch_ref_thread_c<false, true, false>(t, g, st);
-  return count ? launch_ref_thread_c<false, false, true>(t, g, st)
-               : launch_ref_thread_c<false, false, false>(t, g, st);
-}
-
-// 33 < k <= 48 with 16-bit fragments staged in shared memory: 64-bit accumulators
-template <bool PREFIX, bool COUNT>
-rmat_status launch_w64_c(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  return (g.post & RMAT_POST_UNDIRECTED)
-             ? launch_packed_t<16, true, true, PREFIX, COUNT, true, false, true>(t, g, st)
-             : launch_packed_t<16, true, true, PREFIX, COUNT, false, false, true>(t, g, st);
-}
-
-rmat_status launch_w64(const rmat_table* t, const rmat::GenLaunch& g, bool prefix, bool count,
-                       cudaStream_t st) {
-  if (prefix)
-    return count ? launch_w64_c<true, true>(t, g, st) : launch_w64_c<true, false>(t, g, st);
-  return count ? launch_w64_c<false, true>(t, g, st) : launch_w64_c<false, false>(t, g, st);
-}
-
-// scheme-G (non power of two) tables with 16-bit fragments in shared memory
-template <bool OUT64, bool PREFIX, bool COUNT>
-rmat_status launch_sg_c(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  return (g.post & RMAT_POST_UNDIRECTED)
-             ? launch_packed_t<16, true, OUT64, PREFIX, COUNT, true, false, false, true>(t, g, st)
-             : launch_packed_t<16, true, OUT64, PREFIX, COUNT, false, false, false, true>(t, g, st);
-}
-
-rmat_status launch_sg(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
-                      bool count, cudaStream_t st) {
-  if (out64) {
-    if (prefix)
-      return count ? launch_sg_c<true, true, true>(t, g, st) : launch_sg_c<true, true, false>(t, g, st);
-    return count ? launch_sg_c<true, false, true>(t, g, st) : launch_sg_c<true, false, false>(t, g, st);
-  }
-  if (prefix)
-    return count ? launch_sg_c<false, true, true>(t, g, st) : launch_sg_c<false, true, false>(t, g, st);
-  return count ? launch_sg_c<false, false, true>(t, g, st) : launch_sg_c<false, false, false>(t, g, st);
-}
 
 rmat_status launch_generic(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
                            cudaStream_t st) {
@@ -519,12 +391,12 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
       case RMAT_KERNEL_PACKED_SMEM:
         rs = sg            ? launch_sg(t, g, out64, prefix, count, st)
              : w64         ? launch_w64(t, g, prefix, count, st)
-             : t->fb == 16 ? launch_packed_fb<16, true>(t, g, out64, prefix, count, st)
-                           : launch_packed_fb<32, true>(t, g, out64, prefix, count, st);
+             : t->fb == 16 ? launch_packed_p16(t, g, true, out64, prefix, count, st)
+                           : launch_packed_p32(t, g, true, out64, prefix, count, st);
         break;
       case RMAT_KERNEL_PACKED_GLOBAL:
-        rs = t->fb == 16 ? launch_packed_fb<16, false>(t, g, out64, prefix, count, st)
-                         : launch_packed_fb<32, false>(t, g, out64, prefix, count, st);
+        rs = t->fb == 16 ? launch_packed_p16(t, g, false, out64, prefix, count, st)
+                         : launch_packed_p32(t, g, false, out64, prefix, count, st);
         break;
       default:
         rs = launch_generic(t, g, out64, st);

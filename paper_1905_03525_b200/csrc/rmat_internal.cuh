@@ -1,0 +1,89 @@
+// Internal declarations shared by the translation units of librmat_b200.so
+// (split so nvcc compiles the kernel families in parallel; no device code
+// crosses units).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "../../include/rmat_b200.h"
+#include "philox.cuh"
+#include "rmat_device.cuh"
+#include "rmat_kernels.cuh"
+
+struct rmat_table {
+  int device;
+  uint64_t n;
+  uint32_t dmin, dmax;
+  uint32_t scheme_p, lg;
+  // generic layout
+  uint32_t* T;
+  uint32_t* alias;
+  uint64_t* row;
+  uint64_t* col;
+  uint8_t* depth;
+  // packed layout (optional)
+  uint32_t fb;  // 0 = absent (scheme P tables only)
+  uint32_t gpacked;  // 1: the packed layout was built for a scheme-G (non power of two) table
+  uint64_t fastmod_m;  // ceil(2^64 / n): exact bucket = hi mod n (scheme G)
+  uint32_t* pB;
+  void* pA;
+  uint32_t* ptlo;
+  uint64_t packed_bytes;
+  uint32_t packed_smem;
+  uint64_t device_bytes;
+};
+
+namespace rmat_impl {
+
+int max_smem_optin(int dev);
+int num_sms(int dev);
+rmat::PackedTab packed_view(const rmat_table* t);
+rmat::GenericTab generic_view(const rmat_table* t);
+
+template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
+          bool W64 = false, bool SG = false>
+inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG>;
+  const int sms = num_sms(t->device);
+  int threads, blocks;
+  size_t smem = 0;
+  if (SMEM) {
+    threads = rmat::kSmemThreads;
+    smem = t->packed_bytes + (size_t)rmat::kSmemStrideThreads * rmat::kRingBytes;
+    blocks = sms;
+  } else {
+    threads = rmat::kGlobalThreads;
+    smem = (size_t)threads * rmat::kRingBytes;
+  }
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return RMAT_ERR_CUDA;
+  if (!SMEM) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess)
+      return RMAT_ERR_CUDA;
+    blocks = sms * std::max(per_sm, 1);
+  }
+  uint64_t need = (g.total_streams + threads - 1) / threads;
+  blocks = (int)std::min<uint64_t>((uint64_t)blocks, std::max<uint64_t>(need, 1));
+  kern<<<blocks, threads, smem, st>>>(packed_view(t), g);
+  return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
+}
+
+
+// scheme-P packed kernels (rmat_packed16.cu / rmat_packed32.cu)
+rmat_status launch_packed_p16(const rmat_table* t, const rmat::GenLaunch& g, bool smem, bool out64,
+                              bool prefix, bool count, cudaStream_t st);
+rmat_status launch_packed_p32(const rmat_table* t, const rmat::GenLaunch& g, bool smem, bool out64,
+                              bool prefix, bool count, cudaStream_t st);
+// reference blocks per thread, 33 < k <= 48, scheme-G tables (rmat_packed_extra.cu)
+rmat_status launch_ref_thread(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
+                              bool prefix, bool count, cudaStream_t st);
+rmat_status launch_w64(const rmat_table* t, const rmat::GenLaunch& g, bool prefix, bool count,
+                       cudaStream_t st);
+rmat_status launch_sg(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
+                      bool count, cudaStream_t st);
+
+}  // namespace rmat_impl

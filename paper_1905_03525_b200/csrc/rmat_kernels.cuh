@@ -732,7 +732,7 @@ k_generic(const GenericTab tab, const __grid_constant__ GenLaunch g) {
 // ---------------------------------------------------------------------------
 // Oracle mode: replay words of one stream.
 // ---------------------------------------------------------------------------
-__global__ void k_replay_words(int scheme_p, uint32_t lg, uint64_t sid, uint32_t k0, uint32_t k1,
+static __global__ void k_replay_words(int scheme_p, uint32_t lg, uint64_t sid, uint32_t k0, uint32_t k1,
                                uint64_t start, uint64_t count, uint64_t* out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
        i += (uint64_t)gridDim.x * blockDim.x)
