@@ -12,6 +12,8 @@ from paper_1905_03525_b200 import _native as N
 from paper_1905_03525_b200.generator import generate_shard
 
 pytestmark = pytest.mark.gpu
+# RMAT_FUZZ_SEED shifts every sweep's seed (default 0 = the committed cases)
+_SHIFT = int(__import__("os").environ.get("RMAT_FUZZ_SEED", "0"))
 
 TAGS = ["f1", "f2", "f4", "f5", "v253", "v256", "v1024", "v4096", "v16384"]
 QUADS = [G500, LESS_SKEWED, SKEWED, UNIFORM]
@@ -35,7 +37,7 @@ def host_u64(t, k):
     return v.view(np.uint32).astype(np.uint64) if k <= 32 else v.view(np.uint64)
 
 
-@pytest.mark.parametrize("tag,quads,k,m,block,seed", list(configs(40, 2024)))
+@pytest.mark.parametrize("tag,quads,k,m,block,seed", list(configs(40, 2024 + _SHIFT)))
 def test_fuzz_fast_mode(cuda, tag, quads, k, m, block, seed):
     ot = oracle_table(tag, quads)
     cfg = GenConfig(params=params_for(quads, k), table=table_for(tag, quads), edge_count=m,
@@ -48,7 +50,7 @@ def test_fuzz_fast_mode(cuda, tag, quads, k, m, block, seed):
         assert int(s.item()) == samples, kern
 
 
-@pytest.mark.parametrize("tag,quads,k,m,block,seed", list(configs(30, 77)))
+@pytest.mark.parametrize("tag,quads,k,m,block,seed", list(configs(30, 77 + _SHIFT)))
 def test_fuzz_reference_mode(cuda, tag, quads, k, m, block, seed):
     ot = oracle_table(tag, quads)
     cfg = GenConfig(params=params_for(quads, k), table=table_for(tag, quads), edge_count=m,
@@ -82,7 +84,7 @@ def part_configs(n, seed):
                            id=f"{i}-{tag}-k{k}t{t}-m{m}-p{parts}-{rngmode[:4]}")
 
 
-@pytest.mark.parametrize("tag,quads,k,t,m,parts,seed,rngmode", list(part_configs(24, 5)))
+@pytest.mark.parametrize("tag,quads,k,t,m,parts,seed,rngmode", list(part_configs(24, 5 + _SHIFT)))
 def test_fuzz_partitioned(cuda, tag, quads, k, t, m, parts, seed, rngmode):
     """generate_part over every part: tile-by-tile equal to the oracle's tile streams."""
     from paper_1905_03525_b200 import DOMAIN_TILE
@@ -146,7 +148,7 @@ def distinct_configs(n, seed):
         yield pytest.param(tag, quads, k, t, tile, count, s, id=f"{i}-{tag}-k{k}t{t}-{count}")
 
 
-@pytest.mark.parametrize("tag,quads,k,t,tile,count,seed", list(distinct_configs(24, 11)))
+@pytest.mark.parametrize("tag,quads,k,t,tile,count,seed", list(distinct_configs(24, 11 + _SHIFT)))
 def test_fuzz_distinct_tiles_reference_mode(cuda, tag, quads, k, t, tile, count, seed):
     """generate_tile(distinct=True, rng="reference") == the oracle's restatement of the
     reference's distinct loop (continuation words, dedup_local, resampling)."""
