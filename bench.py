@@ -180,6 +180,32 @@ def issue_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
             "frac": achieved / ceiling, "source": "profiles/ncu_full_summary.json"}
 
 
+def lsu_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
+    """The binding ceiling of the fast path: L1 data-pipe (LSU) wavefronts per edge
+    from the committed ncu capture (random bucket gathers from shared memory, ring
+    staging, sector stores) against one wavefront per SM per cycle."""
+    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        with open(path) as f:
+            s = json.load(f)
+        wpe = float(s["lsu_wavefronts_per_edge"])
+        hz = float(s["sm_clock_hz"])
+        pct = float(s["lsu_wavefronts_pct"])
+        parts = s.get("lsu_breakdown_per_warp_edge")
+    except (OSError, KeyError, ValueError, TypeError):
+        return None
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ceiling = sms * hz / wpe
+    achieved = edges / kernel_s
+    return {"bound": "l1_data_pipe", "wavefronts_per_edge": wpe,
+            "wavefronts_per_32_edges_by_role": parts,
+            "ceiling_edges_per_s": ceiling, "achieved_edges_per_s": achieved,
+            "frac": achieved / ceiling, "ncu_pct_of_peak": pct,
+            "source": "profiles/ncu_full_summary.json"}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -316,7 +342,8 @@ def main() -> None:
                      "kernel": "k_packed<16,smem> (rmat_generate)",
                      "algorithmic_bytes_per_launch": rows * BYTES_PER_EDGE,
                      "frac_of_8TBps_nominal": achieved / 8000.0,
-                     "issue_bound": issue_bound_from_profile(kernel_ms / 1e3, rows)},
+                     "issue_bound": issue_bound_from_profile(kernel_ms / 1e3, rows),
+                     "lsu_bound": lsu_bound_from_profile(kernel_ms / 1e3, rows)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps,

@@ -9,6 +9,7 @@ import argparse
 import csv
 import io
 import json
+import re
 import subprocess
 
 
@@ -30,12 +31,49 @@ def num(d, k, scale_units=True):
     return x
 
 
+def sass_breakdown(path: str, edges: int, global_wavefronts: float) -> dict:
+    """Shared-memory wavefronts per 32 edges by role, from the per-instruction
+    source page: full-warp LDS / LDS.64 = bucket gathers, predicated STS =
+    ring staging, predicated LDS = sector flush reads; the remaining L1 data-pipe
+    wavefronts are the global sector stores."""
+    rows = list(csv.reader(open(path)))
+    hdr = rows[1]
+    ix = hdr.index
+    out = {"bucket_B_lds32": 0.0, "bucket_A_lds64": 0.0, "ring_sts": 0.0, "ring_flush_lds": 0.0,
+           "other_shared": 0.0}
+    for r in rows[2:]:
+        if len(r) < len(hdr):
+            continue
+        try:
+            wf = float(r[ix("L1 Wavefronts Shared")].replace(",", ""))
+            thr = float(r[ix("Avg. Predicated-On Threads Executed")].replace(",", ""))
+        except ValueError:
+            continue
+        if wf <= 0:
+            continue
+        src = r[ix("Source")]
+        if "STS" in src and src.lstrip().startswith("@"):
+            out["ring_sts"] += wf
+        elif "LDS" in src and src.lstrip().startswith("@"):
+            out["ring_flush_lds"] += wf
+        elif "LDS.64" in src and thr >= 24:
+            out["bucket_A_lds64"] += wf
+        elif re.search(r"\bLDS\b", src) and thr >= 24:
+            out["bucket_B_lds32"] += wf
+        else:
+            out["other_shared"] += wf
+    out["global_sector_stores"] = global_wavefronts
+    warp_edges = edges / 32
+    return {k: v / warp_edges for k, v in out.items()}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("out")
     ap.add_argument("--edges", type=int, default=1 << 32)
     ap.add_argument("--bytes-per-edge", type=int, default=8)
+    ap.add_argument("--sass", help="ncu --page source --csv --print-source sass export of the same report")
     a = ap.parse_args()
     d = raw(a.rep)
     s = {
@@ -63,6 +101,18 @@ def main():
             for k in d if k.startswith("smsp__average_warps_issue_stalled_")
             and k.endswith("_per_issue_active.ratio") and num(d, k, False) > 0.02},
     }
+    # L1 data pipe (LSU): one wavefront per cycle per SM.  Shared-memory gathers,
+    # staging stores/reads and global stores all pass through it.
+    lsu_avg = next(k for k in d if k.endswith("l1tex__data_pipe_lsu_wavefronts.avg"))
+    s["lsu_wavefronts"] = num(d, lsu_avg, False) * num(d, "device__attribute_multiprocessor_count", False)
+    s["lsu_wavefronts_pct"] = num(d, "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", False)
+    s["shared_ld_wavefronts"] = num(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", False)
+    s["shared_st_wavefronts"] = num(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum", False)
+    s["lsu_wavefronts_per_edge"] = s["lsu_wavefronts"] / a.edges
+    if a.sass:
+        s["lsu_breakdown_per_warp_edge"] = sass_breakdown(a.sass, a.edges, s["lsu_wavefronts"]
+                                                          - s["shared_ld_wavefronts"]
+                                                          - s["shared_st_wavefronts"])
     s["dram_bytes_per_edge"] = (s["dram_read_bytes"] + s["dram_write_bytes"]) / a.edges
     s["thread_instructions_per_edge"] = s["warp_instructions"] * 32 / a.edges
     s["achieved_gbs_under_ncu"] = s["algorithmic_bytes"] / s["duration_s"] / 1e9
