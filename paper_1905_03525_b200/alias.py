@@ -57,24 +57,23 @@ class AliasTable:
         return int(self.threshold.shape[0])
 
     def reconstructed_probs(self) -> np.ndarray:
-        """Selection probability per index implied by (threshold, alias)."""
-        mass = self.threshold.copy()
-        np.add.at(mass, self.alias, 1.0 - self.threshold)
-        return mass / self.size
+        """Selection probability per index implied by (threshold, alias):
+        own keep-mass plus the spill of every bucket aliased to it, over n."""
+        spill = np.bincount(self.alias, weights=1.0 - self.threshold, minlength=self.size)
+        return (self.threshold + spill) / self.size
 
 
 def build_alias(weights) -> AliasTable:
     """Vose's alias construction over non-negative weights (reference alias.py:58-109)."""
     w = np.asarray(weights, dtype=np.float64)
-    if w.ndim != 1 or w.size == 0:
-        raise EmptyInput("need a non-empty 1-d weight sequence")
-    if not np.isfinite(w).all():
-        raise NegativeWeight(f"weights must be finite, got {w[~np.isfinite(w)][:4]}")
-    if (w < 0).any():
-        raise NegativeWeight("weights must be non-negative")
+    if w.ndim != 1 or not w.size:
+        raise EmptyInput(f"weights must be a non-empty vector, got shape {w.shape}")
+    bad = ~np.isfinite(w) | (w < 0)
+    if bad.any():
+        raise NegativeWeight(f"weights must be finite and >= 0; first offenders {w[bad][:4]}")
     total = float(w.sum())  # pairwise summation: part of the bit-exact recipe
-    if total <= 0.0:
-        raise AllZeroWeights("at least one weight must be positive")
+    if not total > 0.0:
+        raise AllZeroWeights("all weights are zero")
 
     n = int(w.size)
     scaled = (w * (n / total)).tolist()  # python floats: same IEEE doubles, faster loop
@@ -101,10 +100,11 @@ def build_alias(weights) -> AliasTable:
 
 def alias_sample(table: AliasTable, uniform_draw):
     """Resolve (bucket index, fraction) draws to entry indices (reference alias.py:112-125)."""
-    idx, frac = uniform_draw
-    idx = np.asarray(idx, dtype=np.int64)
-    out = np.where(np.asarray(frac) < table.threshold[idx], idx, table.alias[idx])
-    return int(out) if out.ndim == 0 else out
+    bucket, fraction = uniform_draw
+    bucket = np.asarray(bucket, dtype=np.int64)
+    keep = np.asarray(fraction) < np.take(table.threshold, bucket)
+    picked = np.where(keep, bucket, np.take(table.alias, bucket))
+    return picked if picked.ndim else int(picked)
 
 
 def threshold_to_u32(threshold: np.ndarray) -> np.ndarray:

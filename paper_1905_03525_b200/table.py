@@ -19,13 +19,13 @@ from __future__ import annotations
 
 import heapq
 import math
+from collections.abc import Iterator
 from dataclasses import dataclass
-from typing import Iterator
 
 import numpy as np
 
-from .alias import AliasTable, build_alias
 from .params import RmatParams
+from .alias import AliasTable, build_alias
 
 __all__ = [
     "DEFAULT_DEPTH_CAP", "MAX_FIXED_DEPTH", "DepthOutOfRange", "SizeLimitTooSmall",
@@ -33,22 +33,22 @@ __all__ = [
     "TableStats", "table_stats",
 ]
 
-DEFAULT_DEPTH_CAP = 62
-
-#: 4**16 entries is the largest fixed table that can be materialised.
-MAX_FIXED_DEPTH = 16
-
-
-class DepthOutOfRange(ValueError):
-    """Fragment depth (or depth cap) outside the supported range."""
+DEFAULT_DEPTH_CAP = 62  # deepest fragment a variable table may grow
+MAX_FIXED_DEPTH = 16    # 4**16 entries: largest fixed table materialised
 
 
 class SizeLimitTooSmall(ValueError):
     """A variable table needs room for one expansion (size_limit >= 4)."""
 
 
-@dataclass(frozen=True)
+class DepthOutOfRange(ValueError):
+    """Fragment depth (or depth cap) outside the supported range."""
+
+
+@dataclass(frozen=True, slots=True)
 class PathEntry:
+    """One fragment: `depth` row and column bits (first level high) and its probability."""
+
     row_bits: int
     col_bits: int
     depth: int
@@ -59,24 +59,24 @@ class PathEntry:
 class FragmentTable:
     """Column-wise fragment set plus its alias sampler (reference table.py:57-89)."""
 
-    row_bits: np.ndarray  # uint64
-    col_bits: np.ndarray  # uint64
-    depths: np.ndarray  # uint64, >= 1
-    probs: np.ndarray  # float64
-    sampler: AliasTable
+    row_bits: np.ndarray    # uint64 per entry
+    col_bits: np.ndarray    # uint64 per entry
+    depths: np.ndarray      # uint64 per entry, each >= 1
+    probs: np.ndarray       # float64 path probabilities
+    sampler: AliasTable     # alias table over probs
     max_depth: int
-    kind: str  # "fixed" | "variable"
-    mean_depth: float  # sum p * depth: bits per sample per endpoint
+    kind: str               # "fixed" or "variable"
+    mean_depth: float       # E[depth] = sum p * depth (bits per sample per endpoint)
 
     def __len__(self) -> int:
-        return int(self.probs.shape[0])
+        return self.probs.shape[0]
 
     def entry(self, i: int) -> PathEntry:
-        return PathEntry(int(self.row_bits[i]), int(self.col_bits[i]),
-                         int(self.depths[i]), float(self.probs[i]))
+        return PathEntry(row_bits=int(self.row_bits[i]), col_bits=int(self.col_bits[i]),
+                         depth=int(self.depths[i]), prob=float(self.probs[i]))
 
     def __iter__(self) -> Iterator[PathEntry]:
-        return (self.entry(i) for i in range(len(self)))
+        yield from map(self.entry, range(len(self)))
 
 
 def _finish(row: np.ndarray, col: np.ndarray, dep: np.ndarray, prob: np.ndarray,
@@ -110,12 +110,11 @@ def _split_code(code: int, depth: int) -> tuple[int, int]:
 def build_fixed_table(params: RmatParams, depth: int) -> FragmentTable:
     """All 4**depth paths of one length, ordered by interleaved path code."""
     if not 1 <= depth <= MAX_FIXED_DEPTH:
-        raise DepthOutOfRange(f"fixed depth must be in [1, {MAX_FIXED_DEPTH}], got {depth}")
+        raise DepthOutOfRange(f"fixed fragment depth {depth} not in 1..{MAX_FIXED_DEPTH}")
     n = 4 ** depth
     code = np.arange(n, dtype=np.uint64)
     q = np.asarray(params.quadrants, dtype=np.float64)
-    row = np.zeros(n, dtype=np.uint64)
-    col = np.zeros(n, dtype=np.uint64)
+    row, col = np.zeros((2, n), dtype=np.uint64)
     prob = np.ones(n, dtype=np.float64)
     for lvl in range(depth):  # root level first: probabilities multiply root -> leaf
         digit = (code >> np.uint64(2 * (depth - 1 - lvl))) & np.uint64(3)
@@ -136,9 +135,9 @@ def build_variable_table(params: RmatParams, size_limit: int,
     smaller interleaved code (reference table.py:163-183).
     """
     if size_limit < 4:
-        raise SizeLimitTooSmall(f"size_limit must be >= 4, got {size_limit}")
+        raise SizeLimitTooSmall(f"size_limit {size_limit} leaves no room for one expansion (need >= 4)")
     if not 1 <= depth_cap <= DEFAULT_DEPTH_CAP:
-        raise DepthOutOfRange(f"depth_cap must be in [1, {DEFAULT_DEPTH_CAP}], got {depth_cap}")
+        raise DepthOutOfRange(f"depth_cap {depth_cap} not in 1..{DEFAULT_DEPTH_CAP}")
     q = params.quadrants
     live: list[tuple[float, int, int]] = [(-1.0, 0, 0)]
     frozen: list[tuple[float, int, int]] = []
@@ -173,6 +172,8 @@ def build_variable_table(params: RmatParams, size_limit: int,
 
 @dataclass(frozen=True)
 class TableStats:
+    """Per-table summary: size, probability range, E[depth] and information content."""
+
     entry_count: int
     min_prob: float
     max_prob: float
@@ -186,14 +187,8 @@ def table_stats(table: FragmentTable) -> TableStats:
     p = table.probs
     pos = p[p > 0.0]
     lp = np.log2(pos)
-    return TableStats(
-        entry_count=len(table),
-        min_prob=float(p.min()),
-        max_prob=float(p.max()),
-        expected_depth=table.mean_depth,
-        expected_info=float(-np.dot(pos, lp)),
-        mean_entry_info=float(-lp.mean()),
-    )
+    return TableStats(len(table), float(p.min()), float(p.max()), table.mean_depth,
+                      float(-np.dot(pos, lp)), float(-lp.mean()))
 
 
 def bits_per_sample(table: FragmentTable) -> float:
