@@ -330,17 +330,24 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
   for (uint32_t i = 0; i < a->n_segments; ++i) aligned = aligned && (a->segments[i].out_row % G) == 0;
   prefix = prefix || !aligned;
   int kernel = a->kernel;
+  // The packed kernels count a stream's edges in 32 bits: the longest stream
+  // actually launched (not E itself: E = m single streams are common) must
+  // stay below 2^31.  Longer streams take the generic kernel (64-bit counts).
+  uint64_t longest = 0;
+  for (uint32_t i = 0; i < a->n_segments; ++i)
+    longest = std::max<uint64_t>(longest, std::min<uint64_t>(E, a->segments[i].edge_count));
+  const bool short_streams = longest < (1ull << 31);
   // one edge per sample at most (dmax <= k), 33-bit accumulators, and a
-  // 32-bit Philox call index: E * k / dmin samples < 2^34.
-  const bool packed_ok = t->fb != 0 && t->dmax <= a->k && a->k <= 33 &&
-                         (double)E * a->k / t->dmin < 17179869184.0;
+  // 32-bit Philox call index: longest * k / dmin samples < 2^34.
+  const bool packed_ok = short_streams && t->fb != 0 && t->dmax <= a->k && a->k <= 33 &&
+                         (double)longest * a->k / t->dmin < 17179869184.0;
   // scheme-G tables (size not a power of two) with 16-bit fragments in shared memory
-  const bool sg = t->gpacked && t->packed_smem && t->dmax <= a->k && a->k <= 33 &&
-                  (double)E * a->k / t->dmin < 8589934592.0;
+  const bool sg = short_streams && t->gpacked && t->packed_smem && t->dmax <= a->k && a->k <= 33 &&
+                  (double)longest * a->k / t->dmin < 8589934592.0;
   // 33 < k <= 48: the shared-memory packed kernel with 64-bit accumulators
-  const bool w64 = !packed_ok && t->fb == 16 && t->packed_smem && t->dmax <= a->k &&
+  const bool w64 = short_streams && !packed_ok && t->fb == 16 && t->packed_smem && t->dmax <= a->k &&
                    a->k > 33 && a->k <= 48 && a->out_width == 8 &&
-                   (double)E * a->k / t->dmin < 17179869184.0;
+                   (double)longest * a->k / t->dmin < 17179869184.0;
   if (kernel == RMAT_KERNEL_AUTO)
     kernel = packed_ok ? (t->packed_smem ? RMAT_KERNEL_PACKED_SMEM : RMAT_KERNEL_PACKED_GLOBAL)
              : (w64 || sg) ? RMAT_KERNEL_PACKED_SMEM
@@ -456,9 +463,11 @@ rmat_status rmat_generate_refstream(const rmat_refstream_args* a, void* cuda_str
   // 64-bit Philox.  Fewer blocks: the CTA-cooperative kernels below.
   const uint64_t E = a->block_size;
   if (a->kernel < RMAT_KERNEL_AUTO || a->kernel > RMAT_KERNEL_GENERIC) return RMAT_ERR_INVALID;
+  // (thread per block: 32-bit edge counts, so blocks shorter than 2^31 edges)
   const bool thread_ok = t->fb == 16 && t->scheme_p && t->packed_smem && t->dmax <= a->k &&
                          a->k <= 33 && a->word_offset == 0 &&
-                         (double)E * a->k / t->dmin < 17179869184.0;
+                         std::min<uint64_t>(E, a->edge_count) < (1ull << 31) &&
+                         (double)std::min<uint64_t>(E, a->edge_count) * a->k / t->dmin < 17179869184.0;
   const bool cta_packed_ok = t->fb == 16 && t->scheme_p;
   if (seg_mode && a->kernel == RMAT_KERNEL_PACKED_SMEM) {
     // segments of one long stream, one thread each (k_packed<..., REF>)

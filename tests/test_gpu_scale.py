@@ -321,3 +321,36 @@ def test_misaligned_output_pointers(cuda, width_k):
         launch_refstream(dt, k, 9, DOMAIN_BLOCK, 1024, 4100, 0, 5, out, kernel=N.KERNEL_PACKED_SMEM)
         launch_refstream(dt, k, 9, DOMAIN_BLOCK, 1024, 4100, 0, 5, ref, kernel=N.KERNEL_PACKED_GLOBAL)
         assert torch.equal(buf[off:], ref.view(wide)) and bool((buf[:off] == -1).all())
+
+
+def test_packed_kernels_refuse_streams_of_2pow31_edges(cuda):
+    """The packed kernels count a stream's edges in 32 bits: a single stream of
+    >= 2^31 edges must not reach them (AUTO routes it to the generic kernel;
+    forcing a packed kernel is refused before any launch).  A huge E whose
+    streams are short (E = m single streams) keeps the fast path."""
+    import ctypes
+
+    dt = device_table(table_for("v1024"), cuda)
+    out = torch.empty((64, 2), dtype=torch.uint32, device=cuda)
+
+    def status(edge_count, out_rows, E, kernel):
+        segs = (N.Segment * 1)(N.Segment(0, edge_count, 0, 0, 0))
+        used = ctypes.c_int(-1)
+        args = N.GenArgs(table=dt.handle, k=16, out_width=4, seed=1, domain=DOMAIN_BLOCK,
+                         edges_per_stream=E, segments=segs, n_segments=1, out=out.data_ptr(),
+                         out_rows=out_rows, kernel=kernel, kernel_used=ctypes.pointer(used))
+        with torch.cuda.device(cuda):
+            st = N.lib().rmat_generate(ctypes.byref(args), torch.cuda.current_stream(cuda).cuda_stream)
+        torch.cuda.synchronize(cuda)
+        return st, used.value
+
+    big = (1 << 31) + 4
+    # rejected at validation, nothing launched (out is far smaller than out_rows claims)
+    assert status(big, big, big, N.KERNEL_PACKED_SMEM)[0] == 4  # RMAT_ERR_UNSUPPORTED
+    assert status(big, big, 1 << 40, N.KERNEL_PACKED_GLOBAL)[0] == 4
+    # short stream, enormous E: still the packed shared-memory kernel, same edges
+    st, used = status(64, 64, 1 << 40, N.KERNEL_AUTO)
+    assert st == 0 and used == N.KERNEL_PACKED_SMEM
+    want = torch.empty_like(out)
+    launch_generate(dt, 16, 1, DOMAIN_BLOCK, 64, [(0, 64, 0, 0, 0)], want, kernel=N.KERNEL_GENERIC)
+    assert torch.equal(out, want)
