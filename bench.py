@@ -181,9 +181,10 @@ def issue_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
 
 
 def lsu_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
-    """The binding ceiling of the fast path: L1 data-pipe (LSU) wavefronts per edge
-    from the committed ncu capture (random bucket gathers from shared memory, ring
-    staging, sector stores) against one wavefront per SM per cycle."""
+    """The L1 data pipe beside the issue bound: LSU wavefronts per edge from the
+    committed ncu capture (random bucket gathers from shared memory, ring staging,
+    sector stores) against one wavefront per SM per cycle.  Busy (~91 %) but
+    measured non-binding."
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as f:
@@ -202,7 +203,7 @@ def lsu_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
     return {"bound": "l1_data_pipe", "wavefronts_per_edge": wpe,
             "wavefronts_per_32_edges_by_role": parts,
             "ceiling_edges_per_s": ceiling, "achieved_edges_per_s": achieved,
-            "frac": achieved / ceiling, "ncu_pct_of_peak": pct,
+            "frac": achieved / ceiling, "ncu_pct_of_peak": pct, "binding": False,
             "source": "profiles/ncu_full_summary.json"}
 
 
