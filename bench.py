@@ -184,7 +184,7 @@ def lsu_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
     """The L1 data pipe beside the issue bound: LSU wavefronts per edge from the
     committed ncu capture (random bucket gathers from shared memory, ring staging,
     sector stores) against one wavefront per SM per cycle.  Busy (~91 %) but
-    measured non-binding."
+    measured non-binding."""
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as f:
