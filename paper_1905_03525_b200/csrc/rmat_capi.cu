@@ -215,7 +215,7 @@ rmat_status rmat_table_create(int device, const rmat_table_desc* d, rmat_table**
     std::vector<uint32_t> B(n), tlo(n);
     for (uint64_t i = 0; i < n; ++i) {
       const uint32_t a = al[i];
-      B[i] = (~T[i] & ~fm) | (uint32_t)dep[i] | ((uint32_t)dep[a] << 8);
+      B[i] = rmat::bucket_word(T[i], fm, (uint32_t)dep[i], (uint32_t)dep[a]);
       tlo[i] = T[i] & fm;
     }
     if ((st = upload(B, &t->pB, &bytes)) || (st = upload(tlo, &t->ptlo, &bytes))) {

@@ -31,6 +31,39 @@ struct SegDev {
 //          FB=32: uint4 {row_self, row_alias, col_self, col_alias}
 //   TLO[i] = T & (4n-1): only read when the fraction's top bits tie T_hi.
 // ---------------------------------------------------------------------------
+// Packed bucket word B (low 16 bits: d_alias << 8 | d_self) and the fraction
+// test against it.  RMAT_B_PLAIN = 1: B carries the threshold's top (32 - F)
+// bits as they are, and `w >= B` (one ISETP) decides frac < thr exactly
+// unless those top bits tie.  RMAT_B_PLAIN = 0: B carries them complemented
+// and the carry of (w | fm) + B (one 64-bit IMAD) decides.  Either way a tie
+// is settled from the low F fraction bits against TLO.
+#ifndef RMAT_B_PLAIN
+#define RMAT_B_PLAIN 0  // measured: 3 % slower on C3 despite 7 % fewer instructions
+#endif
+inline uint32_t bucket_word(uint32_t T, uint32_t fm, uint32_t d_self, uint32_t d_alias) {
+  return ((RMAT_B_PLAIN ? T : ~T) & ~fm) | d_self | (d_alias << 8);
+}
+#if defined(__CUDACC__)
+struct BucketTest {
+  uint32_t ge;  // 1: fraction top bits >= threshold top bits (alias unless a tie says otherwise)
+  bool tie;     // top bits equal: the low F bits decide
+};
+// `one` must be a run-time 1 (PackedTab::one) so the IMAD is not folded into adds.
+__device__ __forceinline__ BucketTest bucket_test(uint32_t w, uint32_t b, uint32_t fm, uint32_t one) {
+  BucketTest r;
+  if (RMAT_B_PLAIN) {
+    r.ge = w >= b ? 1u : 0u;
+    r.tie = (w ^ b) <= fm;
+  } else {
+    uint64_t sum;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(sum) : "r"(w | fm), "r"(one), "l"((uint64_t)b));
+    r.ge = (uint32_t)(sum >> 32);
+    r.tie = (uint32_t)sum <= fm;
+  }
+  return r;
+}
+#endif
+
 struct PackedTab {
   const uint32_t* B;
   const void* A;

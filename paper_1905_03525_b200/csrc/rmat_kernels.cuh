@@ -437,16 +437,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     q.tie = false;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      // B = (~T & ~fm) | d_alias << 8 | d_self: the complemented threshold top
-      // bits above the depth fields.  With X = w | fm, the 64-bit sum X + B
-      // carries out exactly when the fraction's top bits H >= T_hi (alias),
-      // and its low word is < 2^F exactly when H == T_hi (a tie).  One IMAD
-      // on the FMA pipe replaces the compare/select chain on the ALU pipe.
-      const uint64_t sum = mad_wide(q.w[t] | fm, one, q.b[t]);
-      const uint32_t ge = (uint32_t)(sum >> 32);
-      q.tie |= (uint32_t)sum <= fm;
-      q.sel[t] = mad_lo(ge, 0x22u, 0x4410u);   // 0x4410 self / 0x4432 alias
-      q.seld[t] = ge + 0x4440u;                // 0x4440 self / 0x4441 alias
+      // B: threshold top bits above the depth fields (rmat_device.cuh
+      // bucket_test); ge = alias unless the top bits tie.
+      const BucketTest bt = bucket_test(q.w[t], q.b[t], fm, one);
+      q.tie |= bt.tie;
+      q.sel[t] = mad_lo(bt.ge, 0x22u, 0x4410u);  // PRMT selectors: 0x4410 self / 0x4432 alias
+      q.seld[t] = bt.ge + 0x4440u;               // depth byte: 0x4440 self / 0x4441 alias
     }
     return q;
   };
@@ -456,7 +452,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     if constexpr (REF || SG) {  // the word carries its full 32-bit fraction
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if ((uint32_t)mad_wide(cb.w[t] | fm, one, cb.b[t]) <= fm) {
+        if (bucket_test(cb.w[t], cb.b[t], fm, one).tie) {
           const bool lt = (cb.w[t] & fm) < __ldg(tab.tlo + (cb.x[t] >> 2));
           cb.sel[t] = lt ? 0x4410u : 0x4432u;
           cb.seld[t] = lt ? 0x4440u : 0x4441u;
@@ -467,7 +463,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
     for (int t = 0; t < 4; ++t)
-      if ((uint32_t)mad_wide(cb.w[t] | fm, one, cb.b[t]) <= fm) {
+      if (bucket_test(cb.w[t], cb.b[t], fm, one).tie) {
         const bool lt = (zq[t] & fm) < __ldg(tab.tlo + ((cb.w[t] & idxmask4) >> 2));
         cb.sel[t] = lt ? 0x4410u : 0x4432u;
         cb.seld[t] = lt ? 0x4440u : 0x4441u;
@@ -526,7 +522,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           vch = mul_hi(cur_c, pw);
         }
         const bool emit = tt >= k;
-        const uint32_t over = emit ? tt - k : tt;
+#ifndef RMAT_VIADDMIN
+#define RMAT_VIADDMIN 1
+#endif
+        // tt - k wraps above tt when tt < k: over = min(tt - k, tt) in one VIADDMNMX
+        const uint32_t over = RMAT_VIADDMIN ? __viaddmin_u32(tt, 0u - k, tt) : (emit ? tt - k : tt);
         cur_r = vr;
         cur_c = vc;
         f = over;

@@ -338,9 +338,9 @@ k_refstream_packed(const PackedTab tab, const RefLaunch g, uint64_t n_blocks) {
         const uint32_t frac = (uint32_t)w;
         const uint32_t bw = sB[idx];
         const uint2 aw = sA[idx];
-        const uint64_t sum = mad_wide_ref(frac | fm, one, bw);
-        uint32_t ge = (uint32_t)(sum >> 32);
-        if ((uint32_t)sum <= fm) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
+        const BucketTest bt = bucket_test(frac, bw, fm, one);
+        uint32_t ge = bt.ge;
+        if (bt.tie) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
         const uint32_t sel = ge ? 0x4432u : 0x4410u;
         const uint32_t r = prmt_ref(aw.x, sel), c = prmt_ref(aw.y, sel);
         dq[q] = chunk_base + 4 * tid + q < blk.w0 ? 0u : prmt_ref(bw, 0x4440u + ge);
@@ -545,9 +545,9 @@ k_refstream_scatter(const PackedTab tab, const RefLaunch g, uint64_t n_blocks,
         const uint32_t frac = (uint32_t)w;
         const uint32_t bw = sB[idx];
         const uint2 aw = sA[idx];
-        const uint64_t sum = mad_wide_ref(frac | fm, one, bw);
-        uint32_t ge = (uint32_t)(sum >> 32);
-        if ((uint32_t)sum <= fm) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
+        const BucketTest bt = bucket_test(frac, bw, fm, one);
+        uint32_t ge = bt.ge;
+        if (bt.tie) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
         const uint32_t sel = ge ? 0x4432u : 0x4410u;
         rq[q] = prmt_ref(aw.x, sel);
         cq[q] = prmt_ref(aw.y, sel);
@@ -741,9 +741,9 @@ k_ref_segment_depths_packed(const PackedTab tab, uint64_t key0, uint64_t key1, u
         const uint32_t idx = (uint32_t)(w >> 32) & nmask;
         const uint32_t frac = (uint32_t)w;
         const uint32_t bw = sB[idx];
-        const uint64_t sum = mad_wide_ref(frac | fm, one, bw);
-        uint32_t ge = (uint32_t)(sum >> 32);
-        if ((uint32_t)sum <= fm) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
+        const BucketTest bt = bucket_test(frac, bw, fm, one);
+        uint32_t ge = bt.ge;
+        if (bt.tie) ge = (frac & fm) < __ldg(tab.tlo + idx) ? 0u : 1u;  // tie
         if (i >= lo && i < hi) acc += prmt_ref(bw, 0x4440u + ge);
       }
     }
