@@ -48,6 +48,38 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+_XCHECK = os.path.join(_HERE, "_build", "libcurand_xcheck.so")
+
+
+def build_curand_xcheck(force: bool = False) -> str:
+    """nvcc oracle/curand_xcheck.cu (ours vs cuRAND Philox4x32-10 on the GPU) for sm_100a."""
+    src = os.path.join(_HERE, "curand_xcheck.cu")
+    hdr = os.path.join(os.path.dirname(_HERE), "paper_1905_03525_b200", "csrc", "philox.cuh")
+    stale = (not os.path.exists(_XCHECK)
+             or os.path.getmtime(_XCHECK) < max(os.path.getmtime(src), os.path.getmtime(hdr)))
+    if force or stale:
+        os.makedirs(os.path.dirname(_XCHECK), exist_ok=True)
+        subprocess.run(["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
+                        "-shared", "-Xcompiler", "-fPIC", src, "-o", _XCHECK], check=True)
+    return _XCHECK
+
+
+def curand_xcheck(inputs: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """inputs (n, 6) uint32 = (c0, c1, c2, c3, k0, k1) -> (ours, curand), each (n, 3, 4):
+    our three Philox4x32-10 forms and cuRAND's `curand_Philox4x32_10` on cuda:0."""
+    L = ctypes.CDLL(build_curand_xcheck())
+    L.xcheck_philox4x32.argtypes = [_u32p, ctypes.c_uint32, _u32p, _u32p]
+    inp = np.ascontiguousarray(inputs, dtype=np.uint32)
+    n = inp.shape[0]
+    ours = np.zeros((n, 3, 4), dtype=np.uint32)
+    theirs = np.zeros((n, 3, 4), dtype=np.uint32)
+    rc = L.xcheck_philox4x32(inp.ctypes.data_as(_u32p), n, ours.ctypes.data_as(_u32p),
+                             theirs.ctypes.data_as(_u32p))
+    if rc:
+        raise RuntimeError(f"curand cross-check: CUDA error {rc}")
+    return ours, theirs
+
+
 @lru_cache(maxsize=1)
 def lib() -> ctypes.CDLL:
     build()
