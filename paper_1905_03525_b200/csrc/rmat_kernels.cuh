@@ -200,6 +200,10 @@ constexpr int kSmemThreads = RMAT_SMEM_THREADS;     // packed_smem CTA size
 #define RMAT_CLEAN_ACC 0  // measured 1 % slower at C3 (2 ALU masks -> 1 SHF + 2 IMAD)
 #endif
 constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k-bit mask
+#ifndef RMAT_HEADS_CAREFUL
+#define RMAT_HEADS_CAREFUL 1
+#endif
+constexpr bool kHeadsCareful = RMAT_HEADS_CAREFUL != 0;  // PREFIX: unaligned heads off the fast path
 // slot-major ring addressing wants a power-of-two thread stride
 constexpr int kSmemStrideThreads = kSmemThreads <= 256 ? 256 : kSmemThreads <= 512 ? 512 : 1024;
 constexpr int kGlobalThreads = 256;                 // packed_global CTA size
@@ -589,13 +593,14 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         // At most G edges since the last check: the sector at gptr is
         // complete when the next slot has left its ring half.
         const bool full = (roff / (G * STRIDE)) != half;
-        if constexpr (PREFIX) {
+        if constexpr (PREFIX && (CAREFUL || !kHeadsCareful)) {
           flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full && lo == 0);
           // unaligned stream head (rare).  No warp vote here: on the careful
           // path other lanes may be elsewhere in the loop.
           if (full && lo != 0) flush_slots<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, lo, G);
           lo = full ? 0 : lo;
         } else {
+          // (PREFIX fast path: heads are flushed on the careful path, lo == 0 here)
           flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full);
         }
         gptr += full ? kSectorBytes : 0;
@@ -624,7 +629,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
                         : (SMEM && (PREFIX || OUT64)) ? RMAT_WIDE_CPI
                         : REF ? RMAT_REF_CPI
                         : !SMEM ? RMAT_GLOBAL_CPI : RMAT_CALLS_PER_ITER;
-    if (__all_sync(0xFFFFFFFFu, L >= 4 * CPI + R - 1)) {
+    // Tile streams may start mid-sector (lo != 0): such a lane keeps the warp
+    // on the careful path until its partial head sector has been flushed, so
+    // the fast path's flush is one predicated sector store with no call.
+    if (__all_sync(0xFFFFFFFFu, L >= 4 * CPI + R - 1 && (!(PREFIX && kHeadsCareful) || lo == 0))) {
       Batch cb[CPI];
 #pragma unroll
       for (int c = 0; c < CPI; ++c) cb[c] = fetch(j + c);
