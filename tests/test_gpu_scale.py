@@ -93,6 +93,28 @@ def test_c3_full_size_properties(cuda):
         assert (got == want).all(), p
     spe = int(s.item()) / m
     assert abs(spe - k / table.mean_depth) < 0.005  # 3.257 samples per edge
+    # Free mode at full size: the (row bit, col bit) digit of every level over
+    # all 2^32 edges is (a, b, c, d)-distributed (Pearson chi-square, 3 dof,
+    # alpha 1e-3 Bonferroni-corrected over the 28 levels; counts on the GPU).
+    from scipy import stats as sps
+
+    quads = np.asarray(params_for(G500, k).quadrants)
+    n11 = torch.zeros(k, dtype=torch.int64, device=cuda)
+    nr = torch.zeros_like(n11)
+    nc = torch.zeros_like(n11)
+    shifts = torch.arange(k - 1, -1, -1, dtype=torch.int32, device=cuda)  # level 0 = MSB
+    for a in range(0, m, 1 << 26):
+        ch = v[a:a + (1 << 26)]
+        r = (ch[:, 0:1] >> shifts) & 1
+        c = (ch[:, 1:2] >> shifts) & 1
+        n11 += (r & c).sum(0)
+        nr += r.sum(0)
+        nc += c.sum(0)
+    n11, nr, nc = n11.cpu().numpy(), nr.cpu().numpy(), nc.cpu().numpy()
+    counts = np.stack([m - nr - nc + n11, nc - n11, nr - n11, n11], axis=1)  # digits a, b, c, d
+    exp = quads * m
+    pvals = sps.chi2.sf(((counts - exp) ** 2 / exp).sum(axis=1), 3)
+    assert (pvals > 1e-3 / k).all(), pvals
     del out, v
     torch.cuda.empty_cache()
 
