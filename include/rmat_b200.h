@@ -83,6 +83,9 @@ typedef struct {
 
 typedef enum {
   RMAT_KERNEL_AUTO = 0,
+  /* The packed kernels need: a packed layout, max depth <= k <= 33 (48 with
+   * 64-bit accumulators), and every launched stream shorter than 2^31 edges;
+   * forcing one where ineligible returns RMAT_ERR_UNSUPPORTED before any launch. */
   RMAT_KERNEL_PACKED_SMEM = 1,   /* packed buckets staged in shared memory */
   RMAT_KERNEL_PACKED_GLOBAL = 2, /* packed buckets read through L1/L2 */
   RMAT_KERNEL_GENERIC = 3        /* any table, k <= 62, 128-bit accumulators */
