@@ -1,5 +1,8 @@
-import os, sys
-sys.path.insert(0, "/root/repo")
+"""Profiling driver: one 2^30-edge reference stream in thread-per-segment mode (k=28, S=2^14)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1905_03525_b200 import build_variable_table, validate
 from paper_1905_03525_b200.device import device_table, launch_refstream_segments
