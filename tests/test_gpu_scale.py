@@ -376,3 +376,70 @@ def test_packed_kernels_refuse_streams_of_2pow31_edges(cuda):
     want = torch.empty_like(out)
     launch_generate(dt, 16, 1, DOMAIN_BLOCK, 64, [(0, 64, 0, 0, 0)], want, kernel=N.KERNEL_GENERIC)
     assert torch.equal(out, want)
+
+
+@pytest.mark.parametrize("k", [20, 33])
+def test_no_writes_outside_the_output_rows(cuda, k):
+    """Canaries on both sides of the output slice: every kernel variant of both
+    stream modes writes exactly rows [0, m) of `out` -- whole-sector stores,
+    partial heads and tails, ragged stream lengths included."""
+    from paper_1905_03525_b200.device import launch_refstream
+    from paper_1905_03525_b200.generator import edge_dtype
+
+    dt = device_table(table_for("v1024"), cuda)
+    wide = torch.int32 if k <= 32 else torch.int64
+    m, E = 4099, 1000  # ragged: streams of 1000 edges, last one 99
+    kernels = [N.KERNEL_AUTO, N.KERNEL_PACKED_SMEM, N.KERNEL_PACKED_GLOBAL, N.KERNEL_GENERIC]
+    for front in (0, 1, 3):
+        for back in (1, 5):
+            buf = torch.full((front + m + back, 2), -1, dtype=wide, device=cuda)
+            out = buf.view(edge_dtype(k))[front:front + m]
+            want = None
+            for kern in kernels:
+                buf.fill_(-1)
+                launch_generate(dt, k, 5, DOMAIN_BLOCK, E, [(0, m, 0, 0, 0)], out, kernel=kern)
+                torch.cuda.synchronize()
+                assert bool((buf[:front] == -1).all()) and bool((buf[front + m:] == -1).all()), kern
+                got = buf[front:front + m].clone()
+                want = got if want is None else want
+                assert torch.equal(got, want), kern
+            want = None
+            for kern in kernels:
+                buf.fill_(-1)
+                launch_refstream(dt, k, 5, DOMAIN_BLOCK, E, m, 0, (m + E - 1) // E, out, kernel=kern)
+                torch.cuda.synchronize()
+                assert bool((buf[:front] == -1).all()) and bool((buf[front + m:] == -1).all()), kern
+                got = buf[front:front + m].clone()
+                want = got if want is None else want
+                assert torch.equal(got, want), kern
+
+
+@pytest.mark.parametrize("k,t", [(20, 3), (36, 3)])
+def test_tile_segments_leave_gaps_untouched(cuda, k, t):
+    """Tile-style segments (prefixes, key tweaks, unaligned starts) written into
+    one buffer with gaps between them: the gap rows keep their canary and
+    every segment equals the same segment launched alone into its own buffer."""
+    from paper_1905_03525_b200.generator import edge_dtype
+
+    inner = k - t
+    dt = device_table(table_for("v1024"), cuda)
+    wide = torch.int32 if k <= 32 else torch.int64
+    segs, row = [], 3
+    for i, cnt in enumerate((777, 1234, 5, 2050)):
+        segs.append((1000 * i, cnt, row, (i % 8) << inner, ((i * 3) % 8) << inner, 0x9E37 * (i + 1)))
+        row += cnt + 1 + (i % 3)
+    total = row + 2
+    buf = torch.full((total, 2), -1, dtype=wide, device=cuda)
+    out = buf.view(edge_dtype(k))
+    for kern in (N.KERNEL_AUTO, N.KERNEL_GENERIC):
+        buf.fill_(-1)
+        launch_generate(dt, inner, 7, DOMAIN_TILE, 512, segs, out, kernel=kern)
+        torch.cuda.synchronize()
+        covered = torch.zeros(total, dtype=torch.bool, device=cuda)
+        for sid, cnt, r0, rp, cp, tw in segs:
+            covered[r0:r0 + cnt] = True
+            alone = torch.full((cnt, 2), -1, dtype=wide, device=cuda)
+            launch_generate(dt, inner, 7, DOMAIN_TILE, 512, [(sid, cnt, 0, rp, cp, tw)],
+                            alone.view(edge_dtype(k)), kernel=kern)
+            assert torch.equal(buf[r0:r0 + cnt], alone), (kern, sid)
+        assert bool((buf[~covered] == -1).all()), kern
