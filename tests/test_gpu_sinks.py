@@ -120,3 +120,41 @@ def test_generate_from_several_host_threads(cuda):
         got = list(ex.map(generate, cfgs))
     for w, g in zip(want, got):
         assert (w == g).all()
+
+
+@pytest.mark.parametrize("k", [20, 40])
+def test_postprocess_stays_inside_its_rows(cuda, k):
+    """rmat_postprocess on slices with canaries around them: undirected +
+    scramble in place and the mirrored out-of-place form touch exactly their
+    rows, and the in-place result equals the oracle's numpy restatement."""
+    import torch
+
+    import oracle.post as opost
+    from paper_1905_03525_b200.postprocess import make_scramble_key, postprocess_device
+
+    dt = torch.int32 if k <= 32 else torch.int64
+    npdt = np.uint32 if k <= 32 else np.uint64
+    rng = np.random.default_rng(k)
+    key = make_scramble_key(11, k)
+    for rows in (1, 7, 1001):
+        for front in (0, 1, 3):
+            host = rng.integers(0, 1 << k, size=(rows, 2), dtype=np.uint64)
+            buf = torch.full((front + rows + 5, 2), -1, dtype=dt, device=cuda)
+            buf[front:front + rows] = torch.from_numpy(host.astype(npdt).view(
+                np.int32 if k <= 32 else np.int64)).to(cuda)
+            out = postprocess_device(buf[front:front + rows], k=k, undirected=True, key=key)
+            torch.cuda.synchronize()
+            assert bool((buf[:front] == -1).all()) and bool((buf[front + rows:] == -1).all())
+            und = opost.to_undirected(host)
+            want = np.stack([opost.scramble(und[:, 0], k, key.round_keys),
+                             opost.scramble(und[:, 1], k, key.round_keys)], axis=1)
+            got = buf[front:front + rows].cpu().numpy().view(npdt).astype(np.uint64)
+            assert np.array_equal(got, want)
+            big = torch.full((front + 2 * rows + 5, 2), -1, dtype=dt, device=cuda)
+            postprocess_device(buf[front:front + rows], k=k, mirror=True,
+                               out=big[front:front + 2 * rows])
+            torch.cuda.synchronize()
+            assert bool((big[:front] == -1).all()) and bool((big[front + 2 * rows:] == -1).all())
+            gotm = big[front:front + 2 * rows].cpu().numpy().view(npdt).astype(np.uint64)
+            assert np.array_equal(gotm, opost.mirrored(got))
+            del out
