@@ -11,8 +11,9 @@ the ranks; each rank keeps its shard in HBM.  No collective on the data path
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Under torchrun (N > 1) one process per GPU.  `--impl reference` times the
-reference's CPU algorithm (numpy port, oracle/refport.py) on the host cores
-over a bounded sample of the same workload; rank 0 alone runs it.
+stock reference (`rmatgen.generate_result`, installed unmodified into the
+git-ignored baseline/_ref) on all host cores over a bounded sample of the same
+workload; rank 0 alone runs it.
 """
 
 from __future__ import annotations
@@ -110,26 +111,97 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def cpu_reference(steps: int, warmup: int, sample_edges: int) -> dict:
-    """Reference CPU algorithm (numpy port), all host cores, bounded sample."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # the stock reference (pip --target install)
+
+
+def stock_reference():
+    """The unmodified reference package `rmatgen`, installed into baseline/_ref
+    (git-ignored; travels to the GPU box).  None when it is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "rmatgen")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import rmatgen
+
+    return rmatgen
+
+
+def host_cpu() -> dict:
+    """lscpu model / topology of the host the CPU legs ran on."""
+    info = {"os_cpu_count": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            key, _, val = line.partition(":")
+            if key.strip() in ("Model name", "CPU(s)", "Thread(s) per core", "Core(s) per socket",
+                               "Socket(s)"):
+                info[key.strip()] = val.strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return info
+
+
+def _median_rate(run, edges: int, warmup: int, reps: int) -> tuple[float, float, int]:
+    """The reference's own timing convention (cli.py:296-314): warm-up runs, then
+    the median of `reps` timed runs; edges/s, seconds per run, runs timed."""
+    for _ in range(warmup):
+        run()
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run()
+        times.append(max(time.perf_counter() - t0, 1e-9))
+    med = float(np.median(times))
+    return edges / med, med, len(times)
+
+
+def cpu_reference(steps: int, warmup: int, sample_edges: int, threads: int | None = None,
+                  port_fallback: bool = True) -> dict:
+    """The reference's CPU generator on the host cores over a bounded sample of C3:
+    stock `rmatgen.generate_result(GenConfig(..., threads=os.cpu_count()))` with its
+    default 2^16-edge blocks (kind "reference"); the numpy port under oracle/ only
+    when baseline/_ref is missing (kind "port")."""
+    cores = threads or os.cpu_count() or 1
+    rg = stock_reference()
+    if rg is not None:
+        p = rg.validate(*QUADS, K)
+        t = rg.build_variable_table(p, TABLE_SIZE)
+        cfg = rg.GenConfig(params=p, table=t, edge_count=sample_edges, seed=SEED, threads=cores)
+        rate, sec, n = _median_rate(lambda: rg.generate_result(cfg), sample_edges, warmup, steps)
+        return {"value": rate, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"first {sample_edges} edges of C3 through the stock reference "
+                          f"(rmatgen.generate_result, threads={cores}, 2^16-edge blocks), "
+                          f"median of {n} after {warmup} warm-up",
+                "seconds_per_step": sec}
+    if not port_fallback:
+        raise RuntimeError("baseline/_ref/rmatgen is not installed")
     from oracle import refport
     from paper_1905_03525_b200 import build_variable_table, validate
 
     p = validate(*QUADS, K)
     t = refport.PortTable.from_fragment_table(build_variable_table(p, TABLE_SIZE))
-    cores = refport.cpu_count()
-    times = []
-    for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        refport.generate(t, K, sample_edges, SEED, 1 << 16, processes=cores)
-        dt = time.perf_counter() - t0
-        if i >= warmup:
-            times.append(dt)
-    med = float(np.median(times))
-    return {"value": sample_edges / med, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"first {sample_edges} edges of C3 (reference blocks of 2^16, "
-                      f"numpy Philox4x64 streams), median of {len(times)} after {warmup} warm-up",
-            "seconds_per_step": med}
+    rate, sec, n = _median_rate(
+        lambda: refport.generate(t, K, sample_edges, SEED, 1 << 16, processes=cores),
+        sample_edges, warmup, steps)
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"first {sample_edges} edges of C3 (numpy port of the reference, "
+                      f"reference blocks of 2^16), median of {n} after {warmup} warm-up",
+            "seconds_per_step": sec}
+
+
+def cpu_baseline_leg(sample_edges: int, sample_1t: int) -> dict:
+    """cpu_baseline of our arm (rank 0, N=1): the stock reference on every host
+    core (1 warm-up + median of 3, cli.py's convention), its threads=1 rate on a
+    smaller slice, and the host's lscpu."""
+    res = cpu_reference(3, 1, sample_edges)
+    res.pop("seconds_per_step", None)
+    try:
+        one = cpu_reference(3, 1, sample_1t, threads=1)
+        res["threads1"] = {"value": one["value"], "sample": one["sample"], "kind": one["kind"]}
+    except Exception as exc:  # noqa: BLE001 (reported, not fatal)
+        res["threads1"] = {"error": repr(exc)[:200]}
+    res["host"] = host_cpu()
+    return res
 
 
 def run_reference_arm(args) -> None:
@@ -137,12 +209,13 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return
     res = cpu_reference(args.steps, min(args.warmup, 1), args.ref_sample)
+    res["host"] = host_cpu()
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": res["seconds_per_step"] * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": workload_config(args.gpus), "impl": "reference",
-            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample", "host")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -214,9 +287,11 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    # cpu_baseline leg (our arm, rank 0, once): ~11 s of CPU work on 16 cores;
-    # --impl reference: per step, so the whole K-step run stays within minutes
-    ap.add_argument("--cpu-sample", type=int, default=1 << 28)
+    # cpu_baseline leg (our arm, rank 0, once): 4 runs of 2^26 edges on every core
+    # + 4 of 2^22 on one (~25 s of CPU work on 16 cores); --impl reference: per
+    # step, so the whole K-step run stays within minutes
+    ap.add_argument("--cpu-sample", type=int, default=1 << 26)
+    ap.add_argument("--cpu-sample-1t", type=int, default=1 << 22)
     ap.add_argument("--ref-sample", type=int, default=1 << 25)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -331,8 +406,7 @@ def main() -> None:
         traffic = traffic / world
     cpu = None
     if not args.no_cpu and world == 1:  # the CPU leg runs on rank 0 at N=1 only
-        cpu = cpu_reference(1, 1, args.cpu_sample)
-        cpu.pop("seconds_per_step", None)
+        cpu = cpu_baseline_leg(args.cpu_sample, args.cpu_sample_1t)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": step_ms, "higher_is_better": True,

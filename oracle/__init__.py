@@ -321,6 +321,19 @@ def ref_tile(table: OracleTable, k: int, t: int, row: int, col: int, count: int,
 DOMAIN_ORACLE = 0xFF51AFD7ED558CCD  # reference _rng.py:22
 
 
+def naive_edges_from_doubles(quads, r):
+    """The reference's naive_edges digit loop (generator.py:388-394) on given doubles r (count, k)."""
+    a, b, c = quads[0], quads[1], quads[2]
+    k = r.shape[1]
+    digit = ((r >= a).astype(np.uint64) + (r >= a + b).astype(np.uint64)
+             + (r >= a + b + c).astype(np.uint64))
+    w = np.uint64(1) << np.arange(k - 1, -1, -1, dtype=np.uint64)
+    out = np.empty((r.shape[0], 2), dtype=np.uint64)
+    out[:, 0] = ((digit >> np.uint64(1)) * w).sum(axis=1, dtype=np.uint64)
+    out[:, 1] = ((digit & np.uint64(1)) * w).sum(axis=1, dtype=np.uint64)
+    return out
+
+
 def naive_edges(quads, k: int, count: int, key0: int, key1: int = 0, start: int = 0):
     """The reference's naive_edges (generator.py:372-395) on raw words [start, start+count*k):
     r = (w >> 11) * 2^-53, digit = [r >= a] + [r >= a+b] + [r >= a+b+c]."""

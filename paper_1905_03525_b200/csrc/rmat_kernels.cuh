@@ -118,9 +118,22 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t sel) {
   return r;
 }
 
+// PRMT in replicate-byte mode: byte c[1:0] of a copied into all four bytes.
+__device__ __forceinline__ uint32_t prmt_rc8(uint32_t a, uint32_t c) {
+  uint32_t r;
+  asm("prmt.b32.rc8 %0, %1, 0, %2;" : "=r"(r) : "r"(a), "r"(c));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
   return r;
 }
 
@@ -200,6 +213,37 @@ constexpr int kSmemThreads = RMAT_SMEM_THREADS;     // packed_smem CTA size
 #define RMAT_CLEAN_ACC 0  // measured 1 % slower at C3 (2 ALU masks -> 1 SHF + 2 IMAD)
 #endif
 constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k-bit mask
+// RMAT_RC8: bit counts (f, d, tt, over) kept byte-replicated (x * 0x01010101) so
+// the depth byte is picked by PRMT.rc8 with the alias bit itself as selector
+// (no per-sample selector add); wrap-mode shifts only look at the low 5 bits.
+#ifndef RMAT_RC8
+#define RMAT_RC8 0
+#endif
+// RMAT_AADDR_IMAD: fragment-pair address a4 * 2 + base on the FMA pipe.
+#ifndef RMAT_AADDR_IMAD
+#define RMAT_AADDR_IMAD 0
+#endif
+// RMAT_DIRECT: 0 = shared-memory staging ring + whole-sector stores;
+// 1 = uint64 edges stored directly (16-byte stores, L2 merges sector halves);
+// 2 = every width stored directly.
+#ifndef RMAT_DIRECT
+#define RMAT_DIRECT 0
+#endif
+#define RMAT_CALLS_PER_ITER_MAX 4
+// RMAT_XRING: ring slot kept in the top bits of a word (see rp_* in k_packed).
+#ifndef RMAT_XRING
+#define RMAT_XRING 0
+#endif
+// RMAT_EMIT_MUL: emit = hi(tt * ceil(2^32 / k)) (0/1 for tt < 2k) and
+// over = tt - emit * k as IMADs; with RMAT_STS_ALWAYS the fast path stores
+// every sample's edge word into the current slot and advances the slot by
+// `emit` (no predicated stores).
+#ifndef RMAT_EMIT_MUL
+#define RMAT_EMIT_MUL 0
+#endif
+#ifndef RMAT_STS_ALWAYS
+#define RMAT_STS_ALWAYS 0
+#endif
 #ifndef RMAT_HEADS_CAREFUL
 #define RMAT_HEADS_CAREFUL 1
 #endif
@@ -295,6 +339,13 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   constexpr uint32_t G = kSectorBytes / EB;     // edges per sector (4 or 2)
   constexpr uint32_t R = kRingFactor * G;       // ring slots
   constexpr uint32_t STRIDE = STHREADS * EB;    // slot-major ring
+  // stores straight to the edge's row (no ring); not for REF (dropped lead edges)
+  constexpr bool DIRECT = !REF && (RMAT_DIRECT == 2 || (RMAT_DIRECT == 1 && OUT64));
+  // byte-replicated bit counts (see RMAT_RC8); 32-bit accumulator path only
+  constexpr bool RC8 = RMAT_RC8 && !OUT64 && !W64 && !REF && !kCleanAcc;
+  constexpr uint32_t REP = RC8 ? 0x01010101u : 1u;
+  constexpr bool XRING = RMAT_XRING != 0;
+  constexpr bool EMUL = RMAT_EMIT_MUL && !RC8 && !W64;
   extern __shared__ __align__(16) uint8_t smem[];
 
   const uint8_t* baseA;
@@ -328,9 +379,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   }
   // shared-space addresses: ring slot q of this thread = ring_sa + q * STRIDE
   const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint32_t baseA_sa = SMEM ? (uint32_t)__cvta_generic_to_shared(baseA) : 0u;
   const uint32_t ring_sa = stage_sa + threadIdx.x * EB;
 
   const uint32_t k = g.k;
+  const uint32_t kr = k * REP;  // emission threshold in the bit-count representation
+  const uint32_t kmagic = (uint32_t)(0xFFFFFFFFull / k) + 1u;  // ceil(2^32 / k) (EMUL)
   const uint32_t kmask = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
   const uint32_t hmask = k > 32 ? 1u : 0u;  // OUT64: bit 32 of a 33-bit edge
   const uint32_t idxmask4 = tab.idxmask4, fm = tab.fm;
@@ -378,7 +432,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   PhiloxPre pre{};
   if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
   uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
-  uint32_t cur_r = 0, cur_c = 0, f = REF ? p.lead : 0u;
+  uint32_t cur_r = 0, cur_c = 0, f = REF ? p.lead * REP : 0u;
   uint64_t cur_r64 = 0, cur_c64 = 0;  // W64 accumulators
   const uint64_t kmask64 = k >= 64 ? ~0ull : ((1ull << k) - 1);
   uint64_t total_nf = 0;
@@ -390,13 +444,49 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // streams are sector-aligned, checked by the host).  L = edges of the
   // stream not yet flushed; the edges still to produce are L - staged.
   uint32_t L = (uint32_t)p.left;
-  uint32_t roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
-  uint32_t half = roff / (G * STRIDE);
-  uint32_t lo = roff / STRIDE & (G - 1);
+  // Ring position rp: roff (byte offset from stage) or, with XRING, the slot
+  // in the top log2(R) bits of a word (slot << SLOT_SHIFT) -- the slot then
+  // advances by a plain add that wraps by itself, and the slot's byte offset
+  // is one IMAD.HI: both on the FMA pipe.
+  constexpr uint32_t LOGR = R == 8 ? 3 : R == 4 ? 2 : R == 2 ? 1 : 0;
+  constexpr uint32_t LOGSTRIDE = STRIDE == 16384 ? 14 : STRIDE == 8192 ? 13 : STRIDE == 4096 ? 12
+                                 : STRIDE == 2048 ? 11 : 10;
+  static_assert((1u << LOGR) == R && (1u << LOGSTRIDE) == STRIDE, "ring geometry");
+  constexpr uint32_t SLOT_SHIFT = 32 - LOGR;
+  const uint32_t ring_mul = tab.one << (LOGR + LOGSTRIDE);
+  auto rp_init = [&](uint64_t row) -> uint32_t {
+    return XRING ? (uint32_t)(row & (R - 1)) << SLOT_SHIFT
+                 : (uint32_t)(row & (R - 1)) * STRIDE + threadIdx.x * EB;
+  };
+  auto rp_slot = [&](uint32_t rp) -> uint32_t { return XRING ? rp >> SLOT_SHIFT : rp / STRIDE; };
+  auto rp_half = [&](uint32_t rp) -> uint32_t { return XRING ? rp >> 31 : rp / (G * STRIDE); };
+  auto rp_addr = [&](uint32_t rp) -> uint32_t {
+    // (run-time multiplier: a constant power of two would become an ALU LEA.HI)
+    return XRING ? mad_hi(rp, ring_mul, ring_sa) : stage_sa + rp;
+  };
+  auto rp_adv = [&](uint32_t rp, uint32_t n01) -> uint32_t {
+    return XRING ? mad_lo(n01, 1u << SLOT_SHIFT, rp) : (rp + n01 * STRIDE) & (R * STRIDE - 1);
+  };
+  uint32_t roff = rp_init(p.row);
+  uint32_t half = rp_half(roff);
+  uint32_t lo = rp_slot(roff) & (G - 1);
   L += lo;  // count the head's missing slots as already "staged"
   if (REF) lo += p.drop;  // a dropped first edge is staged but never flushed (lo may reach G)
   char* gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
-  auto staged = [&]() { return ((roff / STRIDE) - half * G) & (R - 1); };
+  // DIRECT: gptr = the next edge's row, gfast = last row pointer from which a
+  // whole fast iteration still fits, gend = one past the stream's rows.
+  char* gend = nullptr;
+  char* gfast = nullptr;
+  auto direct_open = [&]() {
+    if constexpr (DIRECT) {
+      gptr = reinterpret_cast<char*>(g.out) + p.row * EB;
+      gend = gptr + p.left * EB;
+      gfast = gend - (uint64_t)EB * 8u * RMAT_CALLS_PER_ITER_MAX;
+      lo = 0;
+    }
+  };
+  direct_open();
+  auto staged = [&]() { return (rp_slot(roff) - half * G) & (R - 1); };
 
   // One call's worth of samples: words, bucket entries, byte selectors.
   struct Batch {
@@ -440,7 +530,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     for (int t = 0; t < 4; ++t) {
       const uint32_t a4 = (REF || SG) ? q.x[t] : (q.w[t] & idxmask4);
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
-      q.a[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
+      if constexpr (RMAT_AADDR_IMAD && SMEM && FB == 16) {
+        const uint32_t sa = mad_lo(a4, 2u, baseA_sa);
+        asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(q.a[t].x), "=r"(q.a[t].y) : "r"(sa));
+      } else {
+        q.a[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
+      }
     }
     q.tie = false;
 #pragma unroll
@@ -450,7 +545,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       const BucketTest bt = bucket_test(q.w[t], q.b[t], fm, one);
       q.tie |= bt.tie;
       q.sel[t] = mad_lo(bt.ge, 0x22u, 0x4410u);  // PRMT selectors: 0x4410 self / 0x4432 alias
-      q.seld[t] = bt.ge + 0x4440u;               // depth byte: 0x4440 self / 0x4441 alias
+      q.seld[t] = RC8 ? bt.ge : bt.ge + 0x4440u; // depth byte: 0x4440 self / 0x4441 alias
     }
     return q;
   };
@@ -463,7 +558,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         if (bucket_test(cb.w[t], cb.b[t], fm, one).tie) {
           const bool lt = (cb.w[t] & fm) < __ldg(tab.tlo + (cb.x[t] >> 2));
           cb.sel[t] = lt ? 0x4410u : 0x4432u;
-          cb.seld[t] = lt ? 0x4440u : 0x4441u;
+          cb.seld[t] = RC8 ? (lt ? 0u : 1u) : (lt ? 0x4440u : 0x4441u);
         }
       return;
     }
@@ -474,7 +569,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       if (bucket_test(cb.w[t], cb.b[t], fm, one).tie) {
         const bool lt = (zq[t] & fm) < __ldg(tab.tlo + ((cb.w[t] & idxmask4) >> 2));
         cb.sel[t] = lt ? 0x4410u : 0x4432u;
-        cb.seld[t] = lt ? 0x4440u : 0x4441u;
+        cb.seld[t] = RC8 ? (lt ? 0u : 1u) : (lt ? 0x4440u : 0x4441u);
       }
   };
   // Fragments of one call appended to the accumulators; stores into the ring
@@ -493,8 +588,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         r = lt ? cb.a[t].x : cb.a[t].y;
         c = lt ? cb.a[t].z : cb.a[t].w;
       }
-      const uint32_t d = prmt(cb.b[t], cb.seld[t]);
+      const uint32_t d = RC8 ? prmt_rc8(cb.b[t], cb.seld[t]) : prmt(cb.b[t], cb.seld[t]);
       bool st;
+      uint32_t e01 = 0;  // EMUL: 1 iff this sample completes an edge
       uint64_t u, v;
       if constexpr (W64) {
         // 64-bit accumulators: V = cur << d | bits, edge = (V >> over) & kmask
@@ -523,18 +619,27 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           vch = __funnelshift_l(cur_c, 0u, d);
         } else {
           // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
-          const uint32_t pw = 1u << d;
+          const uint32_t pw = RC8 ? __funnelshift_l(0u, 1u, d) : 1u << d;
           vr = mad_lo(cur_r, pw, r);
           vrh = mul_hi(cur_r, pw);
           vc = mad_lo(cur_c, pw, c);
           vch = mul_hi(cur_c, pw);
         }
-        const bool emit = tt >= k;
 #ifndef RMAT_VIADDMIN
 #define RMAT_VIADDMIN 1
 #endif
-        // tt - k wraps above tt when tt < k: over = min(tt - k, tt) in one VIADDMNMX
-        const uint32_t over = RMAT_VIADDMIN ? __viaddmin_u32(tt, 0u - k, tt) : (emit ? tt - k : tt);
+        bool emit;
+        uint32_t over;
+        if constexpr (EMUL) {
+          // tt < 2k (max depth <= k): hi(tt * ceil(2^32/k)) is 1 iff tt >= k
+          e01 = mul_hi(tt, kmagic);
+          over = mad_lo(e01, 0u - k, tt);
+          emit = e01 != 0;
+        } else {
+          emit = tt >= kr;
+          // tt - k wraps above tt when tt < k: over = min(tt - k, tt) in one VIADDMNMX
+          over = RMAT_VIADDMIN ? __viaddmin_u32(tt, 0u - kr, tt) : (emit ? tt - kr : tt);
+        }
         cur_r = vr;
         cur_c = vc;
         f = over;
@@ -578,21 +683,40 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           v = min(a, b);
         }
       }
-      if (st) {
+      if constexpr (DIRECT) {
+        if (st) {
+          if constexpr (OUT64) {
+            asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(gptr), "l"(u), "l"(v) : "memory");
+          } else {
+            asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(gptr), "r"((uint32_t)u),
+                         "r"((uint32_t)v) : "memory");
+          }
+          gptr += EB;
+          if (CAREFUL) --left;
+        }
+      } else if (EMUL && RMAT_STS_ALWAYS && !CAREFUL) {
+        // the current slot is not staged yet: a non-edge word there is overwritten later
         if constexpr (OUT64) {
-          sts128(stage_sa + roff, u, v);
+          sts128(rp_addr(roff), u, v);
         } else {
-          sts64(stage_sa + roff, (uint32_t)u, (uint32_t)v);
+          sts64(rp_addr(roff), (uint32_t)u, (uint32_t)v);
+        }
+        roff = rp_adv(roff, e01);
+      } else if (st) {
+        if constexpr (OUT64) {
+          sts128(rp_addr(roff), u, v);
+        } else {
+          sts64(rp_addr(roff), (uint32_t)u, (uint32_t)v);
         }
         // next slot; the mask keeps this thread's column bits (tid * EB < STRIDE)
-        roff = (roff + STRIDE) & (R * STRIDE - 1);
+        roff = rp_adv(roff, 1u);
         if (CAREFUL) --left;
       }
-      if (COUNT) ebits |= (uint32_t)st << t;
-      if ((uint32_t)t % G == G - 1) {
+      if (COUNT) ebits |= (EMUL && !CAREFUL ? e01 : (uint32_t)st) << t;
+      if (!DIRECT && (uint32_t)t % G == G - 1) {
         // At most G edges since the last check: the sector at gptr is
         // complete when the next slot has left its ring half.
-        const bool full = (roff / (G * STRIDE)) != half;
+        const bool full = rp_half(roff) != half;
         if constexpr (PREFIX && (CAREFUL || !kHeadsCareful)) {
           flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full && lo == 0);
           // unaligned stream head (rare).  No warp vote here: on the careful
@@ -632,7 +756,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     // Tile streams may start mid-sector (lo != 0): such a lane keeps the warp
     // on the careful path until its partial head sector has been flushed, so
     // the fast path's flush is one predicated sector store with no call.
-    if (__all_sync(0xFFFFFFFFu, L >= 4 * CPI + R - 1 && (!(PREFIX && kHeadsCareful) || lo == 0))) {
+    static_assert(CPI <= RMAT_CALLS_PER_ITER_MAX, "gfast assumes at most RMAT_CALLS_PER_ITER_MAX calls");
+    const bool fast_ok = DIRECT ? (gptr <= gfast + (uint64_t)EB * 4u * (2 * RMAT_CALLS_PER_ITER_MAX - CPI))
+                                : (L >= 4 * CPI + R - 1 && (!(PREFIX && kHeadsCareful) || lo == 0));
+    if (__all_sync(0xFFFFFFFFu, fast_ok)) {
       Batch cb[CPI];
 #pragma unroll
       for (int c = 0; c < CPI; ++c) cb[c] = fetch(j + c);
@@ -649,11 +776,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       j += CPI;
       continue;
     }
-    uint32_t left = L - staged();
+    uint32_t left = DIRECT ? (uint32_t)((uint64_t)(gend - gptr) / EB) : L - staged();
     if (left == 0) {
       // Stream done: write its partial last sector, account nf, open the next.
-      const uint32_t hi_slot = roff / STRIDE & (G - 1);
-      if (hi_slot > lo) flush_tail<OUT64, STHREADS>(gptr, ring_sa, half, lo, hi_slot);
+      const uint32_t hi_slot = rp_slot(roff) & (G - 1);
+      if (!DIRECT && hi_slot > lo) flush_tail<OUT64, STHREADS>(gptr, ring_sa, half, lo, hi_slot);
       if (COUNT) {
         // nf (generator.py:255-257): the highest sample of call j-1 that
         // produced an edge this stream needed.
@@ -668,15 +795,16 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       if (!p.valid) break;
       stream_keys();
       if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
-      j = 0; cur_r = cur_c = 0; f = REF ? p.lead : 0u;
+      j = 0; cur_r = cur_c = 0; f = REF ? p.lead * REP : 0u;
       cur_r64 = cur_c64 = 0;
       L = (uint32_t)p.left;
-      roff = (uint32_t)(p.row & (R - 1)) * STRIDE + threadIdx.x * EB;
-      half = roff / (G * STRIDE);
-      lo = roff / STRIDE & (G - 1);
+      roff = rp_init(p.row);
+      half = rp_half(roff);
+      lo = rp_slot(roff) & (G - 1);
       L += lo;
       if (REF) lo += p.drop;
       gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+      direct_open();
       continue;
     }
     Batch cb = fetch(j);

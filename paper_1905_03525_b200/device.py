@@ -19,7 +19,7 @@ from . import _native as N
 from .alias import threshold_to_u32
 from .table import FragmentTable
 
-__all__ = ["DeviceTable", "device_table", "launch_generate", "launch_refstream",
+__all__ = ["DeviceTable", "device_table", "launch_generate", "launch_refstream", "launch_ref_block",
            "replay_words", "require_cuda", "Segment", "refstream_depth_sum", "DedupSet"]
 
 Segment = N.Segment
@@ -59,14 +59,18 @@ class DeviceTable:
     def __init__(self, table: FragmentTable, device=None):
         dev = require_cuda(device)
         self.device = dev
-        self.table = table
-        self.thr32 = threshold_to_u32(table.sampler.threshold)
-        self.alias = np.ascontiguousarray(table.sampler.alias, dtype=np.int64)
-        self.row = np.ascontiguousarray(table.row_bits, dtype=np.uint64)
-        self.col = np.ascontiguousarray(table.col_bits, dtype=np.uint64)
-        self.depth = np.ascontiguousarray(table.depths, dtype=np.uint64)
-        desc = N.TableDesc(len(table), self.thr32.ctypes.data, self.alias.ctypes.data,
-                           self.row.ctypes.data, self.col.ctypes.data, self.depth.ctypes.data)
+        # No reference to `table` itself: the upload cache (device_table) drops
+        # this object once the FragmentTable is collected.
+        self.mean_depth = float(table.mean_depth)
+        thr32 = threshold_to_u32(table.sampler.threshold)
+        alias = np.ascontiguousarray(table.sampler.alias, dtype=np.int64)
+        row = np.ascontiguousarray(table.row_bits, dtype=np.uint64)
+        col = np.ascontiguousarray(table.col_bits, dtype=np.uint64)
+        depth = np.ascontiguousarray(table.depths, dtype=np.uint64)
+        #: bytes handed to rmat_table_create (the host -> device table upload)
+        self.upload_bytes = sum(a.nbytes for a in (thr32, alias, row, col, depth))
+        desc = N.TableDesc(len(table), thr32.ctypes.data, alias.ctypes.data,
+                           row.ctypes.data, col.ctypes.data, depth.ctypes.data)
         handle = ctypes.c_void_p()
         L = N.lib()
         N.check(L.rmat_table_create(dev.index, ctypes.byref(desc), ctypes.byref(handle)),
@@ -87,8 +91,14 @@ _cache: dict[tuple[int, int], tuple[weakref.ref, DeviceTable]] = {}
 _cache_lock = threading.Lock()
 
 
+def _evict(key) -> None:
+    with _cache_lock:
+        _cache.pop(key, None)  # the DeviceTable's own finalizer frees the device copy
+
+
 def device_table(table: FragmentTable, device=None) -> DeviceTable:
-    """Upload `table` to `device` once; later calls reuse the handle."""
+    """Upload `table` to `device` once; later calls reuse the handle.  The entry
+    lives as long as `table` does (weakref.finalize on the table evicts it)."""
     dev = require_cuda(device)
     key = (id(table), dev.index)
     with _cache_lock:
@@ -97,7 +107,14 @@ def device_table(table: FragmentTable, device=None) -> DeviceTable:
             return hit[1]
         dt = DeviceTable(table, dev)
         _cache[key] = (weakref.ref(table), dt)
-        return dt
+    weakref.finalize(table, _evict, key)
+    return dt
+
+
+def cached_tables() -> int:
+    """Number of live (table, device) uploads in the cache (tests)."""
+    with _cache_lock:
+        return len(_cache)
 
 
 def _stream_ptr(dev) -> int:
@@ -165,6 +182,26 @@ def launch_refstream(dt: DeviceTable, k: int, seed: int, domain: int, block_size
                 "rmat_generate_refstream")
 
 
+def launch_ref_block(dt: DeviceTable, k: int, seed: int, domain: int, block: int, count: int,
+                     out, *, samples_total=None, row_prefix: int = 0, col_prefix: int = 0,
+                     word_offset: int = 0, post_flags: int = 0) -> None:
+    """ONE reference stream keyed [seed ^ domain, block] with `count` edges into out[0:count].
+
+    rmat_generate_refstream addresses blocks by (first_block, block_size,
+    edge_count); for a lone block that is (block, count, (block + 1) * count),
+    which leaves 64 bits for large block indices (tile payloads of t >= ~25 bits):
+    those go through the segment-table launch, whose jobs carry the stream key
+    and count directly."""
+    if (block + 1) * count < 1 << 64:
+        launch_refstream(dt, k, seed, domain, count, (block + 1) * count, block, 1, out,
+                         samples_total=samples_total, row_prefix=row_prefix,
+                         col_prefix=col_prefix, word_offset=word_offset, post_flags=post_flags)
+    else:
+        launch_refstream_streams(dt, k, (seed ^ domain) & _M64,
+                                 [(block, count, 0, row_prefix, col_prefix, word_offset)], out,
+                                 samples_total=samples_total, post_flags=post_flags)
+
+
 #: a launch of fewer reference blocks than the GPU has SMs (one CTA each would
 #: leave SMs idle), each of at least LONG_STREAM_EDGES edges, runs in segment mode
 LONG_STREAM_MAX_BLOCKS = None  # None: the device's SM count
@@ -216,7 +253,7 @@ def launch_refstream_streams(dt: DeviceTable, k: int, key0: int, streams, out, *
     if mode not in ("auto", "thread", "cta"):
         raise ValueError(f"mode must be auto, thread or cta, got {mode!r}")
     thread = mode == "thread" or (mode == "auto" and eligible)
-    mean = float(dt.table.mean_depth)
+    mean = dt.mean_depth
     total_words = sum(st[1] * k for st in streams) / mean
     if words_per_segment:
         L = int(words_per_segment)
@@ -366,6 +403,11 @@ class DedupSet:
         import torch
 
         rows = edges.shape[0]
+        if (out.device != edges.device or out.dtype != edges.dtype or not out.is_contiguous()
+                or out.dim() != 2 or out.shape[1] != 2 or out.shape[0] < rows
+                or not edges.is_contiguous() or edges.dim() != 2 or edges.shape[1] != 2):
+            raise ValueError(f"edges and out must be contiguous (rows, 2) {edges.dtype} tensors "
+                             f"on {edges.device}, out holding at least {rows} rows")
         need = int(N.lib().rmat_dedup_scratch_bytes(rows))
         if self._scratch is None or self._scratch.numel() * 8 < need:
             self._scratch = torch.empty((need + 7) // 8, dtype=torch.int64, device=self.device)

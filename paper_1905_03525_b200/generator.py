@@ -30,7 +30,8 @@ from typing import NamedTuple
 import numpy as np
 
 from . import _native as N
-from .device import device_table, launch_generate, launch_refstream, replay_words, require_cuda
+from .device import (device_table, launch_generate, launch_ref_block, launch_refstream,
+                     replay_words, require_cuda)
 from .params import RmatParams, check_k
 from .table import FragmentTable
 
@@ -65,6 +66,11 @@ class Edge(NamedTuple):
 class GenConfig:
     """Everything `generate` needs (reference generator.py:62-79).
 
+    rng: "philox4x32" (default) = the north_star fast mode -- Philox4x32-10
+    streams, a different (documented, oracle-checked) word source than the
+    reference, so its bytes differ from `rmatgen.generate` for the same config;
+    "reference" = numpy's Philox4x64-10 block streams, byte-identical to
+    `rmatgen.generate` (use it when the exact reference bytes are needed).
     block_size: edges per random stream; None = the mode's default
     (2^16 for "reference", 2^10 for "philox4x32").  threads: accepted for
     API compatibility; like the reference, it never changes the output.
@@ -291,8 +297,7 @@ def emit_block(table: FragmentTable, k: int, count: int, stream_key: tuple[int, 
     out = torch.empty((count, 2), dtype=edge_dtype(int(k)), device=dev)
     if rng == "reference":
         # one reference block whose index is `block`: run a 1-block launch
-        launch_refstream(dt, int(k), seed, DOMAIN_BLOCK, count, (block + 1) * count, block, 1,
-                         out)
+        launch_ref_block(dt, int(k), seed, DOMAIN_BLOCK, block, count, out)
     else:
         if count >= 1 << 31:
             raise ValueError("fast-mode stream length must be < 2**31")
@@ -315,11 +320,12 @@ def stream_replay_words(table: FragmentTable, seed: int, stream: int, count: int
 # The naive per-level sampler (reference generator.py:359-395): baseline and
 # statistical oracle, on the device (k_naive), same numpy Philox words.
 # ---------------------------------------------------------------------------
-def _philox_word_position(gen) -> tuple[int, int, int]:
-    """(key0, key1, index of the next raw word) of a numpy Philox Generator."""
+def _philox_word_position(gen) -> tuple[int, int, int] | None:
+    """(key0, key1, index of the next raw word) of a numpy Philox Generator; None
+    for any other bit generator."""
     st = gen.bit_generator.state
     if st.get("bit_generator") != "Philox":
-        raise TypeError("naive_edge(s) needs a numpy Philox Generator (e.g. keyed_stream) or a seed")
+        return None
     ctr = [int(x) for x in st["state"]["counter"]]
     key = [int(x) for x in st["state"]["key"]]
     if any(ctr[1:]):
@@ -344,9 +350,11 @@ def naive_edges(params: RmatParams, k: int, count: int, rng, chunk: int = 1 << 1
     """Bulk naive sampler (reference generator.py:372-395): k uniforms per edge.
 
     rng: an int seed (stream keyed (seed, DOMAIN_ORACLE, 0) as the reference)
-    or a numpy Philox Generator, which is advanced by count*k words exactly as
-    `rng.random((count, k))` would.  `chunk` is accepted for API compatibility;
-    it never changes the output (the reference draws consecutive words).
+    or a numpy Generator.  A Philox Generator (e.g. keyed_stream) is replayed on
+    the device and advanced by count*k words exactly as `rng.random((count, k))`
+    would; any other bit generator draws those count*k doubles on the host (the
+    caller's own RNG, in `chunk`-edge pieces) and the per-level digits are cut on
+    the device.  The output never depends on `chunk` (consecutive draws).
     """
     import math
 
@@ -360,7 +368,10 @@ def naive_edges(params: RmatParams, k: int, count: int, rng, chunk: int = 1 << 1
     if isinstance(rng, (int, np.integer)):
         key0, key1, w0, gen = (int(rng) ^ DOMAIN_ORACLE) & _M64, 0, 0, None
     else:
-        key0, key1, w0 = _philox_word_position(rng)
+        pos = _philox_word_position(rng)
+        if pos is None:
+            return _naive_edges_drawn(params, k, count, rng, chunk, device)
+        key0, key1, w0 = pos
         gen = rng
     if count == 0:
         return np.empty((0, 2), dtype=np.uint64)
@@ -380,6 +391,29 @@ def naive_edges(params: RmatParams, k: int, count: int, rng, chunk: int = 1 << 1
     if gen is not None:
         _philox_seek(gen, w0 + count * k)
     return edges
+
+
+def _naive_edges_drawn(params: RmatParams, k: int, count: int, gen, chunk: int,
+                       device) -> np.ndarray:
+    """naive_edges for a non-Philox numpy Generator: the caller's generator draws
+    the k doubles per edge (reference generator.py:388), the digits
+    (r >= a) + (r >= a+b) + (r >= a+b+c) and the bit assembly run on the device."""
+    import torch
+
+    dev = require_cuda(device)
+    a, b, c, _ = params.quadrants
+    t1, t2, t3 = a, a + b, a + b + c
+    w = torch.bitwise_left_shift(torch.ones(k, dtype=torch.int64, device=dev),
+                                 torch.arange(k - 1, -1, -1, dtype=torch.int64, device=dev))
+    out = np.empty((count, 2), dtype=np.uint64)
+    chunk = max(1, int(chunk))
+    for pos in range(0, count, chunk):
+        n = min(chunk, count - pos)
+        r = torch.from_numpy(gen.random((n, k))).to(dev)
+        digit = (r >= t1).to(torch.int64) + (r >= t2).to(torch.int64) + (r >= t3).to(torch.int64)
+        uv = torch.stack([((digit >> 1) * w).sum(1), ((digit & 1) * w).sum(1)], 1)
+        out[pos:pos + n] = uv.cpu().numpy().view(np.uint64)
+    return out
 
 
 def naive_edge(params: RmatParams, k: int, rng) -> Edge:

@@ -56,7 +56,7 @@ def generate_to_host(config: GenConfig, out=None, *, rank: int = 0, world: int =
 
     if fresh_table:
         dt = DeviceTable(config.table, dev)
-        h2d = sum(a.nbytes for a in (dt.thr32, dt.alias, dt.row, dt.col, dt.depth))
+        h2d = dt.upload_bytes
     else:
         dt = device_table(config.table, dev)
         h2d = 0

@@ -41,7 +41,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .device import (DedupSet, device_table, launch_generate, launch_refstream,
+from .device import (DedupSet, device_table, launch_generate, launch_ref_block,
                      launch_refstream_streams, refstream_depth_sum, require_cuda)
 from .generator import DOMAIN_NODE, DOMAIN_TILE, FAST_STREAM_EDGES, RNG_MODES, edge_dtype
 from .params import RmatParams, check_k
@@ -237,9 +237,8 @@ def _emit_tile(dt, inner: int, seed: int, rng: str, row: int, col: int, t: int, 
     payload = (row << t) | col
     rp, cp = row << inner, col << inner
     if rng == "reference":
-        launch_refstream(dt, inner, seed, DOMAIN_TILE, count, (payload + 1) * count, payload, 1,
-                         out, samples_total=samples, row_prefix=rp, col_prefix=cp,
-                         word_offset=word_offset)
+        launch_ref_block(dt, inner, seed, DOMAIN_TILE, payload, count, out, samples_total=samples,
+                         row_prefix=rp, col_prefix=cp, word_offset=word_offset)
     else:
         launch_generate(dt, inner, seed, DOMAIN_TILE, FAST_STREAM_EDGES,
                         [(round_ << RESAMPLE_SID_SHIFT, count, 0, rp, cp, tile_key(payload))], out,

@@ -97,6 +97,11 @@ def postprocess_device(edges, *, k: int, undirected: bool = False, key: Scramble
     if out is None:
         out = (torch.empty((2 * rows, 2), dtype=edges.dtype, device=edges.device) if mirror
                else edges)
+    # the ABI carries no output capacity: the kernel writes exactly this shape
+    want = ((2 if mirror else 1) * rows, 2)
+    if (not hasattr(out, "device") or out.device != edges.device or out.dtype != edges.dtype
+            or not out.is_contiguous() or tuple(out.shape) != want):
+        raise ValueError(f"out must be a contiguous {want} {edges.dtype} tensor on {edges.device}")
     flags = (N.POST_UNDIRECTED if undirected else 0) | (N.POST_SCRAMBLE if key else 0) | \
         (N.POST_MIRROR if mirror else 0)
     args = N.PostArgs(flags=flags, k=k, width=edges.element_size(), rows=rows,
@@ -118,13 +123,22 @@ def _host_roundtrip(edges: np.ndarray, k: int, **kw) -> np.ndarray:
     import torch
 
     dev = require_cuda()
-    arr = np.ascontiguousarray(edges)
-    if arr.dtype != np.uint64:
-        raise ValueError("host edge arrays must be uint64 (rows, 2) like the reference's")
+    arr = _as_u64(edges)
     width32 = k <= 32
     t = torch.from_numpy(arr.astype(np.uint32) if width32 else arr.view(np.int64)).to(dev)
     res = postprocess_device(t, k=k, **kw).cpu().numpy()
-    return res.astype(np.uint64) if width32 else res.view(np.uint64)
+    res = res.astype(np.uint64) if width32 else res.view(np.uint64)
+    return res if edges.dtype == np.uint64 else res.astype(edges.dtype)
+
+
+def _as_u64(edges: np.ndarray) -> np.ndarray:
+    """Any integer (rows, 2) host array as contiguous uint64 (the values must be
+    non-negative node ids); results are cast back to the caller's dtype."""
+    if not np.issubdtype(edges.dtype, np.integer):
+        raise ValueError(f"host edge arrays must hold integer node ids, got {edges.dtype}")
+    if np.issubdtype(edges.dtype, np.signedinteger) and edges.size and int(edges.min()) < 0:
+        raise ValueError("node ids must be non-negative")
+    return np.ascontiguousarray(edges, dtype=np.uint64)
 
 
 def _bits(edges) -> int:
@@ -199,11 +213,12 @@ def dedup_local(edges, row_range: tuple[int, int] | None = None,
         if len(edges) == 0:
             return edges.copy()
         dev = require_cuda()
-        arr = np.ascontiguousarray(edges, dtype=np.uint64)
+        arr = _as_u64(edges)
         t = torch.from_numpy(arr.view(np.int64)).to(dev)
         out = torch.empty_like(t)
         kept = DedupSet(len(arr), dev).append(t, out)
-        return out[:kept].cpu().numpy().view(np.uint64)
+        res = out[:kept].cpu().numpy().view(np.uint64)
+        return res if edges.dtype == np.uint64 else res.astype(edges.dtype)
     if edges.device.type != "cuda" or edges.dim() != 2 or edges.shape[1] != 2:
         raise ValueError("edges must be a (rows, 2) CUDA tensor or a host numpy array")
     edges = edges.contiguous()

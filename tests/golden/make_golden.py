@@ -254,6 +254,12 @@ def main() -> None:
     nxt = int(gen.bit_generator.random_raw(1)[0])
     nv["sequence"] = {"k": 10, "seed": 5, "payload": 2, "singles": singles,
                       "bulk_after": [[int(x) for x in r] for r in bulk], "next_word": nxt}
+    # any other numpy bit generator (PCG64 here): the caller's doubles, chunked
+    pp = rmatgen.validate(*G500, 20)
+    gen = np.random.default_rng(7)
+    e = naive_edges(pp, 20, 3000, gen, chunk=1000)
+    nv["pcg64"] = {"k": 20, "count": 3000, "rng_seed": 7, "chunk": 1000, "edges": sha(e),
+                   "next_double": float(gen.random())}
     out["naive"] = nv
 
     with open(os.path.join(HERE, "golden.json"), "w") as f:

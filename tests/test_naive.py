@@ -67,10 +67,37 @@ def test_gpu_naive_generator_sequence(cuda):
     assert int(gen.bit_generator.random_raw(1)[0]) == s["next_word"]
 
 
-def test_naive_rejects_non_philox_generator_before_cuda():
-    from paper_1905_03525_b200 import naive_edges
+def test_oracle_naive_other_bit_generator_matches_reference():
+    """Any numpy Generator (PCG64 here): the reference draws count*k doubles in order."""
+    c = GOLD["pcg64"]
+    p = validate(0.57, 0.19, 0.19, 0.05, c["k"])
+    gen = np.random.default_rng(c["rng_seed"])
+    r = np.concatenate([gen.random((min(c["chunk"], c["count"] - i), c["k"]))
+                        for i in range(0, c["count"], c["chunk"])])
+    assert sha(oracle.naive_edges_from_doubles(p.quadrants, r)) == c["edges"]
+    assert gen.random() == c["next_double"]
+
+
+def test_naive_non_philox_generator_needs_the_gpu():
+    """No CPU fallback: a PCG64 generator is accepted, but the digits are cut on the device."""
+    import torch
+
+    from paper_1905_03525_b200 import NativeUnavailable, naive_edges
 
     p = validate(0.57, 0.19, 0.19, 0.05, 8)
-    with pytest.raises(TypeError):
-        naive_edges(p, 8, 10, np.random.default_rng(1))  # PCG64
+    if not torch.cuda.is_available():
+        with pytest.raises(NativeUnavailable):
+            naive_edges(p, 8, 10, np.random.default_rng(1))
     assert naive_edges(p, 8, 0, 1).shape == (0, 2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunk", [1000, 7, 1 << 16])
+def test_gpu_naive_other_bit_generator(cuda, chunk):
+    from paper_1905_03525_b200 import naive_edges
+
+    c = GOLD["pcg64"]
+    p = validate(0.57, 0.19, 0.19, 0.05, c["k"])
+    gen = np.random.default_rng(c["rng_seed"])
+    assert sha(naive_edges(p, c["k"], c["count"], gen, chunk=chunk)) == c["edges"]
+    assert gen.random() == c["next_double"]  # advanced exactly as the reference advances it

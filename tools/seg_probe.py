@@ -42,7 +42,7 @@ from paper_1905_03525_b200 import _native as N  # noqa: E402
 
 p = validate(0.57, 0.19, 0.19, 0.05, 28)
 dt = device_table(build_variable_table(p, 1 << 14))
-words = int((1 << 30) * 28 / dt.table.mean_depth)
+words = int((1 << 30) * 28 / dt.mean_depth)
 pre = {}
 for L in (1 << 12, 1 << 16):
     nseg = words // L + 1
