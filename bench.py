@@ -221,6 +221,35 @@ def run_reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def dropin_e2e(steps: int) -> dict:
+    """generate(GenConfig(C2)) -> numpy (m, 2) uint64, the reference's return type
+    (generator.py:472), timed per call (table cached, result array from the pinned
+    caching allocator after the warm-up call; device generation + DMA of every edge)."""
+    import torch
+
+    from paper_1905_03525_b200 import GenConfig, build_variable_table, generate, validate
+
+    k, m = 24, 1 << 28
+    p = validate(*QUADS, k)
+    cfg = GenConfig(params=p, table=build_variable_table(p, 1 << 12), edge_count=m, seed=SEED)
+    edges = generate(cfg)  # warm-up: table upload, pinned result allocation
+    ok = edges.shape == (m, 2) and edges.dtype == np.uint64 and int(edges[:, 0].max()) < 1 << k
+    del edges
+    times = []
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        for _ in range(max(steps, 2)):
+            t0 = time.perf_counter()
+            edges = generate(cfg)
+            times.append(time.perf_counter() - t0)
+            del edges
+    dt = float(np.median(times))
+    return {"value": m / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+            "d2h_bytes_per_step": m * 16, "seconds_per_step": dt, "steps": len(times),
+            "workload": "C2: k=24, m=2^28, variable table 2^12 (fast mode)",
+            "path": "paper_1905_03525_b200.generate -> numpy (m, 2) uint64 (drop-in return type)",
+            "result_ok": bool(ok), "clocks": clocks.summary()}
+
+
 def traffic_from_profile() -> float | None:
     """dram read+write bytes per launch of the main kernel from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
@@ -393,6 +422,12 @@ def main() -> None:
                "steps": args.e2e_steps}
         del host_buf
 
+    # the drop-in call itself: generate() -> the reference's (m, 2) uint64 numpy
+    # array, at C2 (k=24, 2^12 table, m=2^28: 4 GiB of uint64 pairs per call)
+    e2e_dropin = None
+    if not args.no_e2e and world == 1:
+        e2e_dropin = dropin_e2e(args.e2e_steps)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -421,6 +456,7 @@ def main() -> None:
                      "lsu_bound": lsu_bound_from_profile(kernel_ms / 1e3, rows)},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_dropin": e2e_dropin,
         "gpu_launches": args.steps,
         "clocks": clocks.summary(),
         "oracle_check": oracle_ok,

@@ -258,6 +258,31 @@ def ref_depth_sum(table: OracleTable, key0: int, key1: int, start: int, count: i
     return int(lib().oracle_ref_depth_sum(*table.args(), key0 & M64, key1 & M64, start, count))
 
 
+def ref_stream_window(table: OracleTable, k: int, key0: int, key1: int, word: int, n: int,
+                      row_prefix: int = 0, col_prefix: int = 0):
+    """Edges [e0, e0 + n) from the middle of a reference stream -> (e0, edges).
+
+    Restated from the concatenation semantics (generator.py:
+    324-356): the fragments of words [0, word) hold D = sum of their depths bits,
+    so e0 = ceil(D / k) is the first edge starting at or after word `word`; a
+    fresh emission from `word` (ref_stream_from) yields the stream's bits from
+    offset D on, which are re-cut on the global k-bit grid (skip e0*k - D bits).
+    """
+    D = ref_depth_sum(table, key0, key1, 0, word)
+    e0 = -(-D // k)
+    skip = e0 * k - D
+    fresh, _ = ref_stream_from(table, k, n + 1, key0, key1, word)
+    out = np.empty((n, 2), dtype=np.uint64)
+    mask = (1 << k) - 1
+    for side, pre in ((0, row_prefix), (1, col_prefix)):
+        big = 0
+        for x in fresh[:, side].tolist():
+            big = (big << k) | x
+        big = (big >> ((n + 1) * k - skip - n * k)) & ((1 << (n * k)) - 1)
+        out[:, side] = [((big >> ((n - 1 - j) * k)) & mask) | pre for j in range(n)]
+    return e0, out
+
+
 def ref_emit_words(table: OracleTable, k: int, count: int, key0: int, key1: int,
                    start: int) -> int:
     """How many words the reference's `_emit(comp, k, count, gen)` draws (generator.py:293-298).

@@ -24,6 +24,8 @@ function of (table, k, m, seed, block_size, rng) and never of the GPU count.
 from __future__ import annotations
 
 import ctypes
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import NamedTuple
 
@@ -214,47 +216,103 @@ def _to_host_u64(t) -> np.ndarray:
 
 #: generate()/generate_result() stream through HBM in slices of at most this
 #: many bytes of edges per device (whole streams), so m is bounded by host RAM only
-HOST_SLICE_BYTES = 16 << 30
+HOST_SLICE_BYTES = 1 << 29
+#: results up to this many bytes are returned in pinned host memory (torch's
+#: caching host allocator): the device writes uint64 pairs and DMAs them straight
+#: into the returned array; larger results go through pageable memory
+PINNED_RESULT_BYTES = None  # None: half of the host's physical memory
+
+
+def _pinned_limit() -> int:
+    if PINNED_RESULT_BYTES is not None:
+        return PINNED_RESULT_BYTES
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") // 2
+    except (ValueError, OSError, AttributeError):
+        return 8 << 30
+
+
+def _host_result(m: int):
+    """The (m, 2) uint64 result array: a view of pinned memory when it fits."""
+    import torch
+
+    if m * 16 <= _pinned_limit():
+        try:
+            t = torch.empty((m, 2), dtype=torch.int64, pin_memory=True)
+            return t.numpy().view(np.uint64), t
+        except RuntimeError:  # pinning refused: pageable fallback below
+            pass
+    return np.empty((m, 2), dtype=np.uint64), None
 
 
 def _generate_host(config: GenConfig, count_samples: bool):
-    """(m, 2) uint64 host edges (+ samples): per device, slices of whole streams are
-    generated in HBM and gathered into the host array (gather.copy_to_host_u64)."""
+    """(m, 2) uint64 host edges (+ samples), the reference's return type.
+
+    Per device (one host thread each, all concurrently -- the reference runs its
+    blocks in a process pool, generator.py:458-468): slices of whole streams are
+    generated as uint64 pairs in HBM on a compute stream while the previous slice
+    is DMA'd on a copy stream straight into the returned array (pinned), or
+    through the staging path of gather.copy_to_host_u64 (pageable, huge m)."""
     import torch
 
     from .gather import copy_to_host_u64
 
     m = config.edge_count
-    edges = np.empty((m, 2), dtype=np.uint64)
+    edges, pinned = _host_result(m)
     B = config.stream_edges
     k = config.params.k
-    width = 4 if k <= 32 else 8
     devices = config.devices or (None,)
     world = len(devices)
     post = N.POST_UNDIRECTED if config.undirected else 0
-    total = 0
-    for rank, d in enumerate(devices):
+
+    def run(rank: int, d) -> int:
         dev = require_cuda(d)
         s_lo, s_hi, r_lo, r_hi = shard_rows(m, B, rank, world)
         if r_hi == r_lo:
-            continue
-        dt = device_table(config.table, dev)
-        per = max(1, HOST_SLICE_BYTES // (2 * width * B))  # streams per slice
-        buf = torch.empty((min(per * B, r_hi - r_lo), 2), dtype=edge_dtype(k), device=dev)
-        samples = torch.zeros(1, dtype=torch.int64, device=dev) if count_samples else None
-        for s in range(s_lo, s_hi, per):
-            ns = min(per, s_hi - s)
-            a, b = s * B, min((s + ns) * B, m)
-            out = buf[:b - a]
-            if config.rng == "reference":
-                launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, m, s, ns, out,
-                                 samples_total=samples, post_flags=post)
-            else:
-                launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B, [(s, b - a, 0, 0, 0)], out,
-                                samples_total=samples, post_flags=post)
-            copy_to_host_u64(out, edges[a:b])
-        if count_samples:
-            total += int(samples.item())
+            return 0
+        with torch.cuda.device(dev):
+            dt = device_table(config.table, dev)
+            per = max(1, HOST_SLICE_BYTES // (16 * B))  # streams per slice
+            n_slices = (s_hi - s_lo + per - 1) // per
+            bufs = [torch.empty((min(per * B, r_hi - r_lo), 2), dtype=torch.int64, device=dev)
+                    for _ in range(min(2, n_slices))]
+            samples = torch.zeros(1, dtype=torch.int64, device=dev) if count_samples else None
+            comp = torch.cuda.Stream(dev)
+            copy = torch.cuda.Stream(dev)
+            freed = [None, None]  # copy-stream events: slice buffer i % 2 drained
+            comp.wait_stream(torch.cuda.current_stream(dev))
+            for i, s in enumerate(range(s_lo, s_hi, per)):
+                ns = min(per, s_hi - s)
+                a, b = s * B, min((s + ns) * B, m)
+                out = bufs[i % 2][:b - a]
+                with torch.cuda.stream(comp):
+                    if freed[i % 2] is not None:
+                        comp.wait_event(freed[i % 2])
+                    if config.rng == "reference":
+                        launch_refstream(dt, k, config.seed, DOMAIN_BLOCK, B, m, s, ns, out,
+                                         samples_total=samples, post_flags=post)
+                    else:
+                        launch_generate(dt, k, config.seed, DOMAIN_BLOCK, B,
+                                        [(s, b - a, 0, 0, 0)], out, samples_total=samples,
+                                        post_flags=post)
+                if pinned is not None:
+                    copy.wait_stream(comp)
+                    with torch.cuda.stream(copy):
+                        pinned[a:b].copy_(out, non_blocking=True)
+                        freed[i % 2] = torch.cuda.Event()
+                        freed[i % 2].record(copy)
+                else:
+                    with torch.cuda.stream(comp):
+                        copy_to_host_u64(out, edges[a:b])  # synchronous staging path
+            copy.synchronize()
+            comp.synchronize()
+            return int(samples.item()) if count_samples else 0
+
+    if world == 1:
+        total = run(0, devices[0])
+    else:
+        with ThreadPoolExecutor(max_workers=world) as ex:
+            total = sum(ex.map(run, range(world), devices))
     return edges, total
 
 

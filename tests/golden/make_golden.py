@@ -262,6 +262,25 @@ def main() -> None:
                    "next_double": float(gen.random())}
     out["naive"] = nv
 
+    # ---- statistics helpers the free-mode acceptance tests restate (stats.py)
+    from rmatgen import chi_square, exact_cell_probs, pool_small_cells
+    st = {"probs": [], "pool": [], "chi": []}
+    for quads, k in ((G500, 4), (SKEW, 6), (LESS, 3)):
+        pr = exact_cell_probs(rmatgen.validate(*quads, k), k)
+        st["probs"].append({"quads": list(quads), "k": k, "probs": sha(pr)})
+    rs = np.random.default_rng(99)
+    for quads, k, total in ((SKEW, 4, 1000), (G500, 5, 3000), (SKEW, 6, 200000)):
+        pr = exact_cell_probs(rmatgen.validate(*quads, k), k)
+        cnt = rs.multinomial(total, pr)
+        pp, pc = pool_small_cells(pr, cnt)
+        st["pool"].append({"quads": list(quads), "k": k, "total": total, "rng": 99,
+                           "probs": sha(pp), "counts": sha(pc.astype(np.int64)),
+                           "cells": int(len(pp))})
+        res = chi_square(pc, pp)
+        st["chi"].append({"statistic": res.statistic, "threshold": res.threshold,
+                          "passed": bool(res.passed)})
+    out["stats"] = st
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", os.path.join(HERE, "golden.json"))

@@ -1,0 +1,102 @@
+"""The reference's distribution acceptance criteria, run on the fast-mode
+(Philox4x32-10, scheme P / scheme G) word streams the B200 kernels draw.
+
+* Criterion 1 (reference tests/test_acceptance.py:41-43, 64-95): 3 models x
+  {fixed l = 1, 2, 4; variable 4, 253, 1021} x 100 seeds, k = 4, m = 10^6,
+  Pearson with rare-cell pooling at alpha = 1e-3, at least 99/100 seeds pass per
+  combination.  Here every run is `generate()` in fast mode (1024-edge streams:
+  the production k_packed kernel for the power-of-two tables with max depth
+  <= k, the generic kernel for the others), plus the naive sampler on the GPU.
+* The same rule at k = 10 (4^10 cells, pooled) on the packed-kernel tables.
+* Out/in-degree log2-histogram homogeneity (reference stats.py:211-239,
+  tests/test_stats.py:200-222) at C2 and C3 size: fast mode against
+  reference-stream mode (byte-identical to rmatgen.generate), degrees counted
+  on the device, two-sample chi-square at alpha = 1e-3.
+The checker is oracle/stats.py, pinned to the reference's own stats outputs.
+"""
+
+import numpy as np
+import pytest
+import torch
+from scipy import stats as sps
+
+from conftest import G500, SKEWED, UNIFORM, params_for, table_for
+from oracle import stats as ost
+from paper_1905_03525_b200 import GenConfig, generate, generate_shard, naive_edges
+
+pytestmark = pytest.mark.gpu
+MODELS = [("graph500", G500), ("uniform", UNIFORM), ("skewed", SKEWED)]
+TABLES = ["f1", "f2", "f4", "v4", "v253", "v1021"]
+
+
+def passes(quads, k, tag, m, seeds):
+    p = params_for(quads, k)
+    probs = ost.exact_cell_probs(p.quadrants, k)
+    table = table_for(tag, quads)
+    return sum(ost.chi_ok(generate(GenConfig(params=p, table=table, edge_count=m, seed=s)),
+                          probs, k) for s in range(seeds))
+
+
+@pytest.mark.timeout(3600)
+@pytest.mark.parametrize("name,quads", MODELS, ids=[m[0] for m in MODELS])
+@pytest.mark.parametrize("tag", TABLES)
+def test_criterion_01_fast_mode(cuda, name, quads, tag):
+    assert passes(quads, 4, tag, 10 ** 6, 100) >= 99, (name, tag)
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("name,quads", MODELS, ids=[m[0] for m in MODELS])
+def test_criterion_01_naive_oracle(cuda, name, quads):
+    k = 4
+    p = params_for(quads, k)
+    probs = ost.exact_cell_probs(p.quadrants, k)
+    ok = sum(ost.chi_ok(naive_edges(p, k, 10 ** 6, s), probs, k) for s in range(100))
+    assert ok >= 99, name
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("name,quads", MODELS, ids=[m[0] for m in MODELS])
+@pytest.mark.parametrize("tag", ["f2", "f5", "v256", "v1024"])
+def test_cells_k10_fast_mode(cuda, name, quads, tag):
+    # v1024's deepest fragments exceed k = 10 for the skewed models: generic kernel there
+    assert passes(quads, 10, tag, 10 ** 6, 20) >= 19, (name, tag)
+
+
+# ---------------------------------------------------------------- degrees at config size
+def degree_log2_hist(col, n: int, buckets: int = 40) -> np.ndarray:
+    """log2-bucketed histogram of the nonzero degrees of one endpoint column (device)."""
+    deg = torch.zeros(n, dtype=torch.int64, device=col.device)
+    step = 1 << 26
+    for a in range(0, col.shape[0], step):
+        deg += torch.bincount(col[a:a + step].to(torch.int64), minlength=n)
+    d = deg[deg > 0].to(torch.float64)
+    b = torch.floor(torch.log2(d)).to(torch.int64).clamp_(max=buckets - 1)
+    return torch.bincount(b, minlength=buckets).cpu().numpy()
+
+
+def homogeneity_p(h1: np.ndarray, h2: np.ndarray) -> float:
+    keep = (h1 + h2) >= 10  # pool sparse tail buckets
+    tab = np.vstack([np.append(h1[keep], h1[~keep].sum()), np.append(h2[keep], h2[~keep].sum())])
+    tab = tab[:, tab.sum(axis=0) > 0]
+    return float(sps.chi2_contingency(tab)[1])
+
+
+def degree_hists(cfg, k):
+    out, _, _ = generate_shard(cfg)
+    v = out.view(torch.int32)
+    h = [degree_log2_hist(v[:, c], 1 << k) for c in (0, 1)]  # out-, in-degree
+    del out, v
+    torch.cuda.empty_cache()
+    return h
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("k,tag,logm", [(24, "v4096", 28), (28, "v16384", 32)], ids=["C2", "C3"])
+def test_degree_histograms_fast_vs_reference_mode(cuda, k, tag, logm):
+    p = params_for(G500, k)
+    t = table_for(tag)
+    fast = degree_hists(GenConfig(params=p, table=t, edge_count=1 << logm, seed=21), k)
+    ref = degree_hists(GenConfig(params=p, table=t, edge_count=1 << logm, seed=22,
+                                 rng="reference"), k)
+    for side, (h1, h2) in zip(("out", "in"), zip(fast, ref)):
+        assert h1.sum() > 0 and homogeneity_p(h1, h2) > 1e-3, (side, h1, h2)

@@ -90,7 +90,7 @@ def test_generate_streams_through_hbm_slices(cuda, monkeypatch, rng, block):
                     seed=3, block_size=block, rng=rng)
     whole, _, s = G.generate_shard(cfg, count_samples=True)
     want = whole.view(torch.int32).cpu().numpy().view(np.uint32).astype(np.uint64)
-    monkeypatch.setattr(G, "HOST_SLICE_BYTES", 5 * 8 * block)  # 5 streams per slice
+    monkeypatch.setattr(G, "HOST_SLICE_BYTES", 5 * 16 * block)  # 5 streams per slice
     res = generate_result(cfg)
     assert (res.edges == want).all() and res.samples_consumed == int(s.item())
     assert (generate(cfg) == want).all()
@@ -158,3 +158,27 @@ def test_postprocess_stays_inside_its_rows(cuda, k):
             gotm = big[front:front + 2 * rows].cpu().numpy().view(npdt).astype(np.uint64)
             assert np.array_equal(gotm, opost.mirrored(got))
             del out
+
+
+@pytest.mark.parametrize("rng", ["philox4x32", "reference"])
+def test_generate_host_paths_and_device_threads(cuda, monkeypatch, rng):
+    """generate(): pinned result (direct DMA of uint64 pairs) == pageable fallback ==
+    the same job split over several device threads (here all on cuda:0: the
+    per-device host threads run concurrently and fill disjoint rows)."""
+    from paper_1905_03525_b200 import generate_result
+    from paper_1905_03525_b200 import generator as G
+
+    base = dict(params=params_for(G500, 20), table=table_for("v1024"), edge_count=1_234_567,
+                seed=5, rng=rng)
+    monkeypatch.setattr(G, "HOST_SLICE_BYTES", 16 * 4096 * 7)
+    want = generate_result(GenConfig(**base))
+    whole, _, s = G.generate_shard(GenConfig(**base), count_samples=True)
+    assert (want.edges == whole.view(torch.int32).cpu().numpy().view(np.uint32)).all()
+    assert want.samples_consumed == int(s.item())
+    assert isinstance(want.edges, np.ndarray) and want.edges.dtype == np.uint64
+    monkeypatch.setattr(G, "PINNED_RESULT_BYTES", 0)  # pageable result array
+    got = generate_result(GenConfig(**base))
+    assert (got.edges == want.edges).all() and got.samples_consumed == want.samples_consumed
+    monkeypatch.setattr(G, "PINNED_RESULT_BYTES", None)
+    got = generate_result(GenConfig(**base, devices=(0, 0, 0)))
+    assert (got.edges == want.edges).all() and got.samples_consumed == want.samples_consumed

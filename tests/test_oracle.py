@@ -157,3 +157,36 @@ def test_fast_words_scheme_p_fraction_layout():
         z = oracle.philox4x32([i >> 2, 1, 5, 0], [key & 0xFFFFFFFF, key >> 32])[i & 3]
         want = (((int(w) >> 2) & 0x3FFF) << 32) | (int(w) & 0xFFFF0000) | (int(z) & 0xFFFF)
         assert int(words[i]) == want
+
+
+def test_ref_stream_window_equals_the_full_stream():
+    """oracle.ref_stream_window (mid-stream windows for the full-size C4 checks)
+    re-cuts a fresh emission on the stream's k-bit grid: equal to the same rows
+    of the whole stream."""
+    from conftest import LESS_SKEWED, oracle_table
+
+    ot = oracle_table("v16384", LESS_SKEWED)
+    full, _ = oracle.ref_stream(ot, 33, 20000, 77, 9, 5 << 33, 2 << 33)
+    for w in (0, 1, 4, 1001, 5000, 60000):
+        e0, win = oracle.ref_stream_window(ot, 33, 77, 9, w, 300, 5 << 33, 2 << 33)
+        assert (full[e0:e0 + 300] == win).all(), w
+
+
+def test_stats_restatement_matches_reference():
+    """oracle/stats.py (checker of the free-mode acceptance tests) against the
+    reference's own exact_cell_probs / pool_small_cells / chi_square outputs."""
+    from oracle import stats as ost
+
+    st = GOLD["stats"]
+    for c in st["probs"]:
+        assert sha(ost.exact_cell_probs(validate(*c["quads"], c["k"]).quadrants, c["k"])) == c["probs"]
+    rs = np.random.default_rng(st["pool"][0]["rng"])  # one generator across the cases, in order
+    for c, ch in zip(st["pool"], st["chi"]):
+        pr = ost.exact_cell_probs(validate(*c["quads"], c["k"]).quadrants, c["k"])
+        cnt = rs.multinomial(c["total"], pr)
+        pp, pc = ost.pool_small_cells(pr, cnt)
+        assert len(pp) == c["cells"] and sha(pp) == c["probs"]
+        assert sha(pc.astype(np.int64)) == c["counts"]
+        stat, thr, ok = ost.chi_square(pc, pp)
+        assert abs(stat - ch["statistic"]) <= 1e-9 * ch["statistic"]
+        assert abs(thr - ch["threshold"]) <= 1e-6 and ok == ch["passed"]

@@ -66,12 +66,15 @@ def main() -> None:
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    from bench import ClockSampler
+
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(args.steps):
-        run()
-    b.record()
-    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clocks:
+        a.record()
+        for _ in range(args.steps):
+            run()
+        b.record()
+        torch.cuda.synchronize(dev)
     sec = a.elapsed_time(b) / 1e3 / args.steps
     tmax = torch.tensor([sec], dtype=torch.float64, device=dev)
     if world > 1:
@@ -80,7 +83,7 @@ def main() -> None:
         print(json.dumps({
             "metric": "edges/sec", "value": m / float(tmax.item()), "unit": "edges/s",
             "n_gpus": world, "plan": args.plan, "rng": args.rng, "parts_per_rank": len(mine),
-            "rank0_edges": rows, "seconds": float(tmax.item()),
+            "rank0_edges": rows, "seconds": float(tmax.item()), "clocks": clocks.summary(),
             "config": {"workload": f"C4: less-skewed k=36 m=2^33 t={t}, 8 parts, uint64 pairs",
                        "table_size": 1 << 14, "seed": 1}}), flush=True)
     if world > 1:

@@ -43,6 +43,15 @@ def timed(fn, reps=3, warm=2):
 
 
 def main():
+    from bench import ClockSampler
+
+    with ClockSampler(0) as clocks:
+        res = _modes()
+    res["clocks"] = clocks.summary()
+    print(json.dumps(res, indent=1))
+
+
+def _modes():
     dev = torch.device("cuda", 0)
     res = {}
     p = validate(0.57, 0.19, 0.19, 0.05, 28)
@@ -185,7 +194,7 @@ def main():
                               tot / max(x["seconds"] for x in bparts),
                           "note": "same 64 tiles and bytes as c4_partitioned; tiles dealt to "
                                   "parts by LPT on their counts (balanced_tiles)"}
-    print(json.dumps(res, indent=1))
+    return res
 
 
 if __name__ == "__main__":

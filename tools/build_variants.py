@@ -2,7 +2,7 @@
 
 usage: python tools/build_variants.py name=DEF1=1,DEF2=0 [name2=...] ...
 Each variant lands in paper_1905_03525_b200/_build/exp_<name>.so ("base" = no defines);
-tools/exp_variants.sh times them interleaved on the GPU.
+tools/ab.sh checks them (GPU parity + fuzz) and times them interleaved on the GPU.
 """
 import os
 import sys

@@ -27,6 +27,7 @@ from paper_1905_03525_b200 import (GenConfig, build_fixed_table, build_variable_
 from paper_1905_03525_b200 import _native as N  # noqa: E402
 from paper_1905_03525_b200.device import device_table  # noqa: E402
 from paper_1905_03525_b200.generator import generate_shard  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 
 def main():
@@ -41,6 +42,7 @@ def main():
     tables += [("variable", 1 << e, build_variable_table(p, 1 << e)) for e in (8, 10, 12, 14, 16)]
     dev = torch.device("cuda", 0)
     rows = []
+    clocks = ClockSampler(0).__enter__()
     for kind, size, t in tables:
         cfg = GenConfig(params=p, table=t, edge_count=m, seed=1, block_size=1024)
         out, _, s = generate_shard(cfg, device=dev, count_samples=True)
@@ -82,8 +84,10 @@ def main():
         if r["kind"] == "variable":
             l_eq = np.log(r["entries"]) / np.log(4)  # fixed depth of an equal-size fixed table
             r["depth_gain_vs_equal_fixed"] = r["mean_depth"] / l_eq
+    clocks.__exit__(None, None, None)
     print(json.dumps({"config": "C5: G500 k=26 m=2^%d" % a.log2m, "entropy_H": H,
-                      "bound_2_over_H": speedup_bound(p), "rows": rows}, indent=1))
+                      "bound_2_over_H": speedup_bound(p), "rows": rows,
+                      "clocks": clocks.summary()}, indent=1))
 
 
 if __name__ == "__main__":
