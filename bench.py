@@ -221,6 +221,34 @@ def run_reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def rank_plan(rank: int, world: int) -> dict:
+    """What rank `rank` of `world` generates and checks (pure host arithmetic; the
+    CPU gloo test runs it for every rank): its contiguous run of whole streams and
+    rows of the C3 job (shard_rows, concatenation = the one-GPU output) and the 16
+    streams of its shard the oracle check samples (global stream ids)."""
+    from paper_1905_03525_b200 import shard_rows
+
+    s_lo, s_hi, r_lo, r_hi = shard_rows(M, STREAM_EDGES, rank, world)
+    local = np.linspace(0, max(s_hi - s_lo - 1, 0), 16).astype(int) if s_hi > s_lo else []
+    return {"s_lo": s_lo, "s_hi": s_hi, "r_lo": r_lo, "r_hi": r_hi, "rows": r_hi - r_lo,
+            "oracle_streams": [s_lo + int(x) for x in local],
+            "output_bytes": (r_hi - r_lo) * BYTES_PER_EDGE}
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    """Max of x over the ranks (the bench's timing rule).  NCCL needs a device
+    tensor; gloo (the CPU multi-rank tests) a host one."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    on = device if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=on)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dropin_e2e(steps: int) -> dict:
     """generate(GenConfig(C2)) -> numpy (m, 2) uint64, the reference's return type
     (generator.py:472), timed per call (table cached, result array from the pinned
@@ -349,19 +377,14 @@ def main() -> None:
         if world > 1:
             dist.barrier()
 
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     params = validate(*QUADS, K)
     table = build_variable_table(params, TABLE_SIZE)
     cfg = GenConfig(params=params, table=table, edge_count=M, seed=SEED,
                     block_size=STREAM_EDGES)
+    plan = rank_plan(rank, world)
     out, r_lo, _ = generate_shard(cfg, rank, world, device=dev)
     rows = out.shape[0]
+    assert (r_lo, rows) == (plan["r_lo"], plan["rows"])
     for _ in range(max(args.warmup, 3) - 1):
         generate_shard(cfg, rank, world, device=dev, out=out)
     torch.cuda.synchronize(dev)
@@ -379,7 +402,7 @@ def main() -> None:
         barrier()
     per_launch = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
-    step_ms = max_over_ranks(total_ms / args.steps)
+    step_ms = max_over_ranks(total_ms / args.steps, world, dev)
     value = M / (step_ms / 1e3)
 
     # oracle check on sampled streams of this shard (bit-exact, C oracle)
@@ -389,18 +412,16 @@ def main() -> None:
 
         ot = oracle.OracleTable.from_fragment_table(table)
         host_rows = out.view(torch.int32)
-        nstreams = (rows + STREAM_EDGES - 1) // STREAM_EDGES
-        first_stream = r_lo // STREAM_EDGES
         checked = 0
         ok = True
-        for s in np.linspace(0, nstreams - 1, 16).astype(int):
-            lo = s * STREAM_EDGES
+        for sid in plan["oracle_streams"]:  # global stream ids inside this rank's shard
+            lo = sid * STREAM_EDGES - r_lo
             cnt = min(STREAM_EDGES, rows - lo)
             got = host_rows[lo:lo + cnt].cpu().numpy().view(np.uint32).astype(np.uint64)
-            want, _ = oracle.fast_stream(ot, K, cnt, SEED, first_stream + int(s))
+            want, _ = oracle.fast_stream(ot, K, cnt, SEED, sid)
             ok &= bool((got == want).all())
             checked += cnt
-        oracle_ok = {"streams": 16, "edges": checked, "bit_exact": ok}
+        oracle_ok = {"streams": len(plan["oracle_streams"]), "edges": checked, "bit_exact": ok}
     except Exception as exc:  # the bench still reports; tests are the parity gate
         oracle_ok = {"error": repr(exc)[:200]}
 
@@ -414,7 +435,7 @@ def main() -> None:
         for _ in range(args.e2e_steps):
             info = generate_to_host(cfg, host_buf.numpy(), rank=rank, world=world, device=dev,
                                     fresh_table=True)
-        dt = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+        dt = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, world, dev)
         barrier()
         e2e = {"value": M / dt, "unit": UNIT, "h2d_bytes_per_step": info["h2d_bytes"] * world,
                "d2h_bytes_per_step": M * BYTES_PER_EDGE, "seconds_per_step": dt,

@@ -43,16 +43,27 @@ def _worker(rank, world, port, out):
         cnt = torch.tensor([sum(tc.count for tc in mine), len(mine)], dtype=torch.int64)
         counts = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(counts, cnt)
-        # bench timing: max over ranks
-        x = torch.tensor([float(rank + 1)], dtype=torch.float64)
-        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        # bench timing: max over ranks, through bench.py's own helper
+        import bench
+
+        mx = bench.max_over_ranks(float(rank + 1), world)
+        # bench.py's per-rank plan: rows, shard and the streams its oracle check reads
+        bp = bench.rank_plan(rank, world)
+        ok = (bp["r_lo"] == r_lo and bp["r_hi"] == r_hi and bp["s_lo"] == s_lo
+              and len(bp["oracle_streams"]) == 16
+              and all(s_lo <= sid < s_hi for sid in bp["oracle_streams"])
+              and bp["oracle_streams"][0] == s_lo and bp["oracle_streams"][-1] == s_hi - 1
+              and bp["r_lo"] == bp["s_lo"] * block)
+        oks = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(oks, torch.tensor([int(ok)], dtype=torch.int64))
         if rank == 0:
-            out.put(([p.tolist() for p in parts], [c.tolist() for c in counts], float(x.item())))
+            out.put(([p.tolist() for p in parts], [c.tolist() for c in counts], mx,
+                     [int(o.item()) for o in oks]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_two_ranks_shard_without_exchange(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -60,7 +71,7 @@ def test_two_ranks_shard_without_exchange(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    parts, counts, mx = q.get(timeout=120)
+    parts, counts, mx, plan_ok = q.get(timeout=120)
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
@@ -73,3 +84,4 @@ def test_two_ranks_shard_without_exchange(world):
     assert sum(c[0] for c in counts) == 1 << 33  # C4 parts cover every edge exactly once
     assert sum(c[1] for c in counts) == 64       # 8 x 8 tiles, each owned by one part
     assert mx == float(world)
+    assert plan_ok == [1] * world  # bench.rank_plan agrees with shard_rows on every rank

@@ -1,0 +1,155 @@
+// Probe (C5 spill point): random bucket gathers from a table too large for one
+// SM's shared memory.  Per-thread hash-driven indices into a table of n
+// entries of 12 bytes (B: 4 B + A: 8 B per entry, the packed layout), three
+// placements, one 512-thread CTA per SM (1024-thread probes for the global one):
+//   0: local  -- the table's first 2^14 entries in this CTA's shared memory
+//                (the C3 fast path today: LDS + LDS.64 per sample)
+//   1: dsmem  -- a cluster of C CTAs (C = 2, 4, 8) holds C slices of 2^14
+//                entries; entry i lives in CTA (i >> 14) of the cluster and is
+//                read with ld.shared::cluster (mapa) -- 1/C local, (C-1)/C remote
+//   2: global -- the whole table (C * 2^14 entries) in global memory, read with
+//                ld.global.nc (L1 / L2 resident), the packed_global variant today
+// Reports gathers (samples) per SM per cycle and per second.
+// Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/_dsmem_probe tools/dsmem_probe.cu
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+namespace cg = cooperative_groups;
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+constexpr int SLICE = 1 << 14;  // entries per CTA (192 KiB of 12-byte entries)
+constexpr int THREADS = 512;
+
+__device__ __forceinline__ uint32_t mix(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t cta_addr, uint32_t rank) {
+  uint32_t remote, v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(cta_addr), "r"(rank));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote));
+  return v;
+}
+__device__ __forceinline__ uint2 ld_cluster_v2(uint32_t cta_addr, uint32_t rank) {
+  uint32_t remote;
+  uint2 v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(cta_addr), "r"(rank));
+  asm volatile("ld.shared::cluster.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(remote));
+  return v;
+}
+
+template <int MODE, int C>
+__global__ void __launch_bounds__(THREADS, 1)
+probe(const uint32_t* __restrict__ gB, const uint2* __restrict__ gA, int iters, uint32_t* out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint2* sA = reinterpret_cast<uint2*>(smem);
+  uint32_t* sB = reinterpret_cast<uint32_t*>(smem + SLICE * 8);
+  uint32_t rank = 0;
+  if (MODE == 1) rank = cg::this_cluster().block_rank();
+  if (MODE != 2) {
+    for (int i = threadIdx.x; i < SLICE; i += THREADS) {
+      sA[i] = gA[rank * SLICE + i];
+      sB[i] = gB[rank * SLICE + i];
+    }
+  }
+  if (MODE == 1) cg::this_cluster().sync(); else __syncthreads();
+  const uint32_t baseA = (uint32_t)__cvta_generic_to_shared(sA);
+  const uint32_t baseB = (uint32_t)__cvta_generic_to_shared(sB);
+  uint32_t x = mix(blockIdx.x * THREADS + threadIdx.x + 1);
+  uint32_t acc = 0;
+  const int lgn = 14 + (C == 1 ? 0 : C == 2 ? 1 : C == 4 ? 2 : 3);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      x = x * 1664525u + 1013904223u;
+      const uint32_t idx = x >> (32 - (MODE == 0 ? 14 : lgn));
+      if (MODE == 0) {
+        const uint2 a = sA[idx];
+        acc ^= sB[idx] + a.x + a.y;
+      } else if (MODE == 1) {
+        const uint32_t r = idx >> 14, o = idx & (SLICE - 1);
+        const uint2 a = ld_cluster_v2(baseA + o * 8, r);
+        acc ^= ld_cluster_u32(baseB + o * 4, r) + a.x + a.y;
+      } else {
+        const uint2 a = __ldg(gA + idx);
+        acc ^= __ldg(gB + idx) + a.x + a.y;
+      }
+    }
+  }
+  if (MODE == 1) cg::this_cluster().sync();  // remote smem stays alive until every reader is done
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
+template <int MODE, int C>
+int run(const uint32_t* gB, const uint2* gA, uint32_t* out, int sms, int clk_khz) {
+  auto k = probe<MODE, C>;
+  const size_t smem = MODE == 2 ? 0 : (size_t)SLICE * 12;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (MODE == 1) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  int blocks = MODE == 1 ? (sms / C) * C : sms;
+  if (MODE == 1) {  // as many whole clusters as fit at once
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(blocks); cfg.blockDim = dim3(THREADS); cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int nclusters = 0;
+    CK(cudaOccupancyMaxActiveClusters(&nclusters, k, &cfg));
+    blocks = nclusters * C;
+    cfg.gridDim = dim3(blocks);
+    const int iters = 2000;
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a);
+      CK(cudaLaunchKernelEx(&cfg, k, gB, gA, iters, out));
+      cudaEventRecord(b);
+      CK(cudaEventSynchronize(b));
+    }
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double gathers = (double)blocks * THREADS * iters * 8;
+    printf("{\"mode\": \"dsmem\", \"cluster\": %d, \"ctas\": %d, \"table_entries\": %d, "
+           "\"ms\": %.3f, \"samples_per_s\": %.4g, \"samples_per_sm_cycle\": %.3f}\n",
+           C, blocks, C * SLICE, ms, gathers / ms * 1e3,
+           gathers / blocks / (ms * 1e-3 * clk_khz * 1e3));
+    return 0;
+  }
+  const int iters = MODE == 2 ? 500 : 2000;
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaEventRecord(a);
+    k<<<blocks, THREADS, smem>>>(gB, gA, iters, out);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+  }
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  const double gathers = (double)blocks * THREADS * iters * 8;
+  printf("{\"mode\": \"%s\", \"cluster\": %d, \"ctas\": %d, \"table_entries\": %d, \"ms\": %.3f, "
+         "\"samples_per_s\": %.4g, \"samples_per_sm_cycle\": %.3f}\n",
+         MODE == 0 ? "local" : "global", C, blocks, MODE == 0 ? SLICE : C * SLICE, ms,
+         gathers / ms * 1e3, gathers / sms / (ms * 1e-3 * clk_khz * 1e3));
+  return 0;
+}
+
+int main() {
+  int sms = 0, clk = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  const int n = 8 * SLICE;
+  uint32_t* gB; uint2* gA; uint32_t* out;
+  CK(cudaMalloc(&gB, n * 4)); CK(cudaMalloc(&gA, n * 8)); CK(cudaMalloc(&out, 4));
+  CK(cudaMemset(gB, 1, n * 4)); CK(cudaMemset(gA, 2, n * 8));
+  printf("{\"sms\": %d, \"clock_khz\": %d}\n", sms, clk);
+  if (run<0, 1>(gB, gA, out, sms, clk)) return 1;
+  if (run<1, 2>(gB, gA, out, sms, clk)) return 1;
+  if (run<1, 4>(gB, gA, out, sms, clk)) return 1;
+  if (run<1, 8>(gB, gA, out, sms, clk)) return 1;
+  if (run<2, 4>(gB, gA, out, sms, clk)) return 1;
+  if (run<2, 8>(gB, gA, out, sms, clk)) return 1;
+  return 0;
+}
