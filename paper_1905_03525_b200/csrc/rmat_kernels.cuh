@@ -230,6 +230,14 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 #define RMAT_DIRECT 0
 #endif
 #define RMAT_CALLS_PER_ITER_MAX 4
+// RMAT_PROBE (ablation builds for tools/ab.sh; WRONG OUTPUT, never the product):
+// bit 0: no bucket gathers (bucket words derived from the Philox word, depths
+// 1..16), bit 1: no output (edges XOR-ed into a register, no staging / flush),
+// bit 2: Philox only (one edge per call, nothing sampled or emitted).  Only the
+// fast loop changes; it times what the rest of the loop costs without them.
+#ifndef RMAT_PROBE
+#define RMAT_PROBE 0
+#endif
 // RMAT_XRING: ring slot kept in the top bits of a word (see rp_* in k_packed).
 #ifndef RMAT_XRING
 #define RMAT_XRING 0
@@ -437,6 +445,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   const uint64_t kmask64 = k >= 64 ? ~0ull : ((1ull << k) - 1);
   uint64_t total_nf = 0;
   uint32_t ebits = 0;                // COUNT: samples of the current call that produced an edge
+  uint32_t probe_acc = 0;            // RMAT_PROBE builds only
   // Output bookkeeping.  stage + roff = ring slot of the next edge (roff =
   // slot * STRIDE + tid * EB, slot = output row mod R).  The first unflushed
   // sector starts at gptr, occupies ring half `half` and is valid from slot
@@ -529,6 +538,14 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const uint32_t a4 = (REF || SG) ? q.x[t] : (q.w[t] & idxmask4);
+      if constexpr ((RMAT_PROBE & 1) && !REF && !SG) {
+        q.b[t] = (q.w[t] & 0xFFFF0F0Fu) + 0x0101u;
+        if constexpr (FB == 16) {
+          q.a[t].x = q.w[t] ^ 0x9E3779B9u;
+          q.a[t].y = q.w[t] * 3u;
+        }
+        continue;
+      }
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
       if constexpr (RMAT_AADDR_IMAD && SMEM && FB == 16) {
         const uint32_t sa = mad_lo(a4, 2u, baseA_sa);
@@ -683,6 +700,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           v = min(a, b);
         }
       }
+      if constexpr ((RMAT_PROBE & 2) && !CAREFUL && !REF) {
+        probe_acc ^= (uint32_t)u ^ ((uint32_t)v << 1);
+        L -= st ? 1u : 0u;
+        if (COUNT) ebits |= (uint32_t)st << t;
+        continue;
+      }
       if constexpr (DIRECT) {
         if (st) {
           if constexpr (OUT64) {
@@ -771,6 +794,13 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         for (int c = 0; c < CPI; ++c) resolve_ties(cb[c], j + c);
       }
       uint32_t unused = 0;
+      if constexpr ((RMAT_PROBE & 4) && !REF) {
+#pragma unroll
+        for (int c = 0; c < CPI; ++c) probe_acc ^= cb[c].w[0] ^ cb[c].w[1] ^ cb[c].w[2] ^ cb[c].w[3];
+        L -= CPI;
+        j += CPI;
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < CPI; ++c) step(cb[c], std::false_type{}, unused);
       j += CPI;
@@ -814,6 +844,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   }
   if (COUNT && g.samples_total && total_nf)
     atomicAdd((unsigned long long*)g.samples_total, (unsigned long long)total_nf);
+  if (RMAT_PROBE && probe_acc == 0x9E3779B9u && g.samples_total)  // keep the probes' work live
+    atomicAdd((unsigned long long*)g.samples_total, 1ull);
 }
 
 // ---------------------------------------------------------------------------

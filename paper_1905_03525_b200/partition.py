@@ -71,7 +71,9 @@ class TileCount:
 
 @dataclass(frozen=True)
 class PartitionPlan:
-    """Grid geometry plus the shared deterministic inputs (reference partition.py:42-68)."""
+    """The t-bit tile grid, the job (k, m, seed) and which contiguous run of tile
+    rows each part owns (reference partition.py:42-68).  Every part derives the
+    same plan from these fields alone; the runs must partition [0, 2^t)."""
 
     k: int
     t: int
@@ -80,33 +82,38 @@ class PartitionPlan:
     owner_rows: tuple[tuple[int, int], ...]
 
     def __post_init__(self) -> None:
-        if not 0 <= self.t <= min(self.k, MAX_TILE_BITS):
-            raise ValueError(f"t must be in [0, min(k, {MAX_TILE_BITS})], got {self.t}")
-        if self.m < 0:
-            raise ValueError(f"m must be >= 0, got {self.m}")
-        rows = 1 << self.t
-        pos = 0
-        for lo, hi in self.owner_rows:
-            if lo != pos or hi < lo:
-                raise ValueError(f"owner_rows must tile [0, {rows}) contiguously")
-            pos = hi
-        if pos != rows:
-            raise ValueError(f"owner_rows must cover [0, {rows}), stop at {pos}")
+        _check_grid(self.k, self.t, self.m)
+        _check_runs(self.owner_rows, 1 << self.t)
+
+
+def _check_grid(k: int, t: int, m: int) -> None:
+    if t < 0 or t > min(k, MAX_TILE_BITS):
+        raise ValueError(f"tile bits t={t} outside [0, min(k, {MAX_TILE_BITS})]")
+    if m < 0:
+        raise ValueError(f"edge count m={m} is negative")
+
+
+def _check_runs(runs, n_rows: int) -> None:
+    """Half-open [lo, hi) runs, in order, gap-free, covering [0, n_rows)."""
+    expect = 0
+    for lo, hi in runs:
+        if lo != expect or hi < lo:
+            raise ValueError(f"owner_rows: run ({lo}, {hi}) does not continue at row {expect}")
+        expect = hi
+    if expect != n_rows:
+        raise ValueError(f"owner_rows end at row {expect}, the grid has {n_rows} rows")
 
 
 def default_plan(k: int, t: int, m: int, seed: int, parts: int = 1) -> PartitionPlan:
-    """Tile rows dealt to `parts` in near-equal contiguous runs (reference partition.py:71-83)."""
+    """Part i owns tile rows [i*q + min(i, r), (i+1)*q + min(i+1, r)) with
+    (q, r) = divmod(2^t, parts): near-equal contiguous runs, the larger ones
+    first (reference partition.py:71-83)."""
     if parts < 1:
-        raise ValueError(f"parts must be >= 1, got {parts}")
-    rows = 1 << t
-    base, extra = divmod(rows, parts)
-    owner = []
-    lo = 0
-    for i in range(parts):
-        hi = lo + base + (1 if i < extra else 0)
-        owner.append((lo, hi))
-        lo = hi
-    return PartitionPlan(k=k, t=t, m=m, seed=seed, owner_rows=tuple(owner))
+        raise ValueError(f"need at least one part, got parts={parts}")
+    q, r = divmod(1 << t, parts)
+    edge = [i * q + min(i, r) for i in range(parts + 1)]
+    return PartitionPlan(k=k, t=t, m=m, seed=seed,
+                         owner_rows=tuple(zip(edge[:-1], edge[1:])))
 
 
 def _node_stream(seed: int, path: int) -> np.random.Generator:
@@ -116,21 +123,25 @@ def _node_stream(seed: int, path: int) -> np.random.Generator:
 
 def split_quadrant_counts(count: int, params: RmatParams,
                           node_key: tuple[int, int]) -> tuple[int, int, int, int]:
-    """Multinomial split of `count` over (a, b, c, d) as three binomials.
+    """Multinomial split of `count` edges over the quadrants (a, b, c, d).
 
-    Conditional probabilities b/(b+c+d) and c/(c+d) (reference partition.py:86-109).
+    Drawn as a chain of binomials from the node's own stream (seed, path),
+    each over what the previous draws left, with the conditional
+    probabilities a, b/(b+c+d), c/(c+d) in that floating-point form -- the
+    draws and their order are what make every part agree on the node
+    (reference partition.py:86-109).
     """
     if count == 0:
         return (0, 0, 0, 0)
     seed, path = node_key
     gen = _node_stream(seed, path)
     a, b, c, d = params.quadrants
-    na = int(gen.binomial(count, a))
-    rest = count - na
-    nb = int(gen.binomial(rest, b / (b + c + d)))
-    rest -= nb
-    nc = int(gen.binomial(rest, c / (c + d)))
-    return (na, nb, nc, rest - nc)
+    left, out = count, []
+    for q in (a, b / (b + c + d), c / (c + d)):
+        n = int(gen.binomial(left, q))
+        out.append(n)
+        left -= n
+    return (out[0], out[1], out[2], left)
 
 
 def plan_tiles(plan: PartitionPlan, params: RmatParams, part: int = 0) -> list[TileCount]:

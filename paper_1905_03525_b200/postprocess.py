@@ -53,20 +53,28 @@ class ScrambleKey:
     round_keys: tuple[tuple[int, int, int], ...]
 
 
-def make_scramble_key(seed: int, k: int) -> ScrambleKey:
-    """Four (odd multiplier, xor-shift, rotation) rounds from (seed, k) (postprocess.py:61-79)."""
-    if not 1 <= k <= 62:
-        raise ValueError(f"k must be in [1, 62], got {k}")
-    mask = (1 << k) - 1
+def _key_words(seed: int, k: int):
+    """The splitmix64 chain the scramble rounds are cut from: start at
+    mix64(seed ^ mix64(k)), each word = mix64(previous + golden ratio)."""
     state = mix64((seed & _M64) ^ mix64(k))
+    while True:
+        state = mix64((state + _GOLDEN) & _M64)
+        yield state
+
+
+def make_scramble_key(seed: int, k: int) -> ScrambleKey:
+    """Four rounds of (odd multiplier mod 2^k, xor-shift in [1, k), rotation in
+    [0, k)), three consecutive chain words per round (reference
+    postprocess.py:61-76; the key bytes are pinned by the goldens)."""
+    if k < 1 or k > 62:
+        raise ValueError(f"scramble needs 1 <= k <= 62, got k={k}")
+    words = _key_words(seed, k)
     rounds = []
     for _ in range(4):
-        state = mix64((state + _GOLDEN) & _M64)
-        mult = (state & mask) | 1
-        state = mix64((state + _GOLDEN) & _M64)
-        xshift = 1 + state % (k - 1) if k > 1 else 0
-        state = mix64((state + _GOLDEN) & _M64)
-        rounds.append((mult, xshift, state % k))
+        mult = (next(words) & ((1 << k) - 1)) | 1
+        w = next(words)
+        xshift = 1 + w % (k - 1) if k > 1 else 0
+        rounds.append((mult, xshift, next(words) % k))
     return ScrambleKey(seed=seed, k=k, round_keys=tuple(rounds))
 
 
