@@ -66,8 +66,8 @@ def test_dedup_append_rejects_short_out(cuda):
     assert DedupSet(100, cuda).append(e, torch.empty_like(e)) == 1
 
 
-@pytest.mark.parametrize("t,row,col,count", [(25, (1 << 25) - 1, 12345, 1000),
-                                             (28, 3, (1 << 28) - 2, 40000),
+@pytest.mark.parametrize("t,row,col,count", [(25, (1 << 25) - 1, (1 << 25) - 1, 20000),
+                                             (28, (1 << 28) - 3, 3, 1000),
                                              (31, (1 << 31) - 1, (1 << 31) - 1, 17)])
 def test_reference_mode_tile_with_large_payload(cuda, t, row, col, count):
     from paper_1905_03525_b200.partition import generate_tile
@@ -89,7 +89,7 @@ def test_host_postprocess_keeps_caller_dtype(cuda, dtype):
 
     rng = np.random.default_rng(3)
     e = rng.integers(0, 1 << 20, size=(5000, 2)).astype(dtype)
-    e[::7] = e[::13][: len(e[::7])]  # duplicates for dedup
+    e[3000:3500] = e[:500]  # duplicates for dedup
     u = to_undirected(e)
     assert u.dtype == dtype
     assert (u[:, 0] == np.maximum(e[:, 0], e[:, 1])).all()
