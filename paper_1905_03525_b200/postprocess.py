@@ -150,7 +150,8 @@ def _as_u64(edges: np.ndarray) -> np.ndarray:
 
 
 def _bits(edges) -> int:
-    if hasattr(edges, "device"):
+    # (numpy >= 2 arrays also carry a `.device`: test for a torch tensor itself)
+    if not isinstance(edges, np.ndarray) and hasattr(edges, "element_size"):
         return 32 if edges.element_size() == 4 else 62
     return 62
 

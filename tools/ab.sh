@@ -26,3 +26,8 @@ if [ -n "$C4V" ]; then
     done
   done
 fi
+if [ -n "${REFV:-}" ]; then
+  for v in $REFV; do
+    RMAT_LIB=$LIBD/exp_$v.so timeout 300 python tools/ref_c3_time.py 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('ref $v', {k: round(x/1e9, 2) for k, x in d.items()})"
+  done
+fi

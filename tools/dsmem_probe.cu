@@ -31,15 +31,15 @@ __device__ __forceinline__ uint32_t mix(uint32_t x) {
 
 __device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t cta_addr, uint32_t rank) {
   uint32_t remote, v;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(cta_addr), "r"(rank));
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote));
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(cta_addr), "r"(rank));
+  asm("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote));
   return v;
 }
 __device__ __forceinline__ uint2 ld_cluster_v2(uint32_t cta_addr, uint32_t rank) {
   uint32_t remote;
   uint2 v;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(cta_addr), "r"(rank));
-  asm volatile("ld.shared::cluster.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(remote));
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(cta_addr), "r"(rank));
+  asm("ld.shared::cluster.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(remote));
   return v;
 }
 

@@ -59,7 +59,7 @@ def main():
         for i, (a, t) in enumerate(body):
             if not t.startswith("VOTE.ANY"):
                 continue
-            br = next(((b, u) for b, u in body[i + 1:i + 8] if "BRA" in u), None)
+            br = next(((b, u) for b, u in body[i + 1:i + 12] if "BRA" in u), None)
             if br:
                 tgt = int(br[1].split()[-1], 16)
                 skip = {b for b, _ in body if br[0] < b < tgt}
