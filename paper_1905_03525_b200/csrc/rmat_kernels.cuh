@@ -238,6 +238,9 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 #ifndef RMAT_IDP
 #define RMAT_IDP 1  // measured +2.0 % at C3 (1.615 vs 1.583e11), +2.5 % reference mode, C4 unchanged
 #endif
+#ifndef RMAT_HI_SHF
+#define RMAT_HI_SHF 2  // measured: 2 = +1.0 % at C3 (1.633 vs 1.617e11), 1 = +0.7 %
+#endif
 // RMAT_AADDR_IMAD: fragment-pair address a4 * 2 + base on the FMA pipe.
 #ifndef RMAT_AADDR_IMAD
 #define RMAT_AADDR_IMAD 0
@@ -671,9 +674,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
           const uint32_t pw = RC8 ? __funnelshift_l(0u, 1u, d) : 1u << d;
           vr = mad_lo(cur_r, pw, r);
-          vrh = mul_hi(cur_r, pw);
+          // high halves: IMAD.HI (FMA pipe) or a funnel shift (ALU pipe),
+          // cur >> (32 - d) (RMAT_HI_SHF: 1 = both sides, 2 = row side only)
+          vrh = RMAT_HI_SHF ? __funnelshift_l(cur_r, 0u, d) : mul_hi(cur_r, pw);
           vc = mad_lo(cur_c, pw, c);
-          vch = mul_hi(cur_c, pw);
+          vch = RMAT_HI_SHF == 1 ? __funnelshift_l(cur_c, 0u, d) : mul_hi(cur_c, pw);
         }
 #ifndef RMAT_VIADDMIN
 #define RMAT_VIADDMIN 1
