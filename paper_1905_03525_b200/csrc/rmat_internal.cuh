@@ -43,9 +43,9 @@ rmat::PackedTab packed_view(const rmat_table* t);
 rmat::GenericTab generic_view(const rmat_table* t);
 
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
-          bool W64 = false, bool SG = false>
+          bool W64 = false, bool SG = false, bool K32 = false>
 inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG>;
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32>;
   const int sms = num_sms(t->device);
   int threads, blocks;
   size_t smem = 0;

@@ -278,20 +278,45 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 #define RMAT_HEADS_CAREFUL 1
 #endif
 constexpr bool kHeadsCareful = RMAT_HEADS_CAREFUL != 0;  // PREFIX: unaligned heads off the fast path
+// RMAT_SPLIT64: uint64 edges staged as two 8-byte planes (u plane, v plane at
+// +kVPlane) instead of one 16-byte slot: two STS.64 of register pairs need no
+// 4-register-aligned operand group (the STS.128 path costs 3 register moves per
+// sample), and the flush's four LDS.64 land straight in the STG.256 operands.
+#ifndef RMAT_SPLIT64
+#define RMAT_SPLIT64 0
+#endif
+constexpr bool kSplit64 = RMAT_SPLIT64 != 0;
 // slot-major ring addressing wants a power-of-two thread stride
 constexpr int kSmemStrideThreads = kSmemThreads <= 256 ? 256 : kSmemThreads <= 512 ? 512 : 1024;
 constexpr int kGlobalThreads = 256;                 // packed_global CTA size
 
+// Staging-ring geometry per edge width: bytes per slot of one plane, slot
+// stride (slot-major: slot q of thread t at q * stride + t * slot bytes), and
+// the offset of the v plane (split uint64 staging only).
+template <bool OUT64, int THREADS>
+struct RingGeo {
+  static constexpr bool SPLIT = OUT64 && kSplit64;
+  static constexpr uint32_t EB = OUT64 ? 16 : 8;          // bytes per edge
+  static constexpr uint32_t SB = SPLIT ? 8 : EB;          // bytes per slot (one plane)
+  static constexpr uint32_t STRIDE = THREADS * SB;
+  static constexpr uint32_t G = kSectorBytes / EB;        // edges per flushed sector
+  static constexpr uint32_t R = kRingFactor * G;          // slots
+  static constexpr uint32_t VPLANE = R * STRIDE;          // v plane offset (SPLIT)
+};
+
 template <bool OUT64, int THREADS>
 __device__ __noinline__ void flush_slots(char* gptr, uint32_t st, uint32_t lo, uint32_t hi) {
   // Slot-by-slot stores of a partial sector (stream heads / tails; rare).
-  constexpr uint32_t EB = OUT64 ? 16 : 8;
-  constexpr uint32_t STRIDE = THREADS * EB;
+  using Geo = RingGeo<OUT64, THREADS>;
   for (uint32_t q = lo; q < hi; ++q) {
-    if (OUT64)
-      *reinterpret_cast<uint4*>(gptr + q * EB) = lds128(st + q * STRIDE);
-    else
-      *reinterpret_cast<uint2*>(gptr + q * EB) = lds64(st + q * STRIDE);
+    if constexpr (Geo::SPLIT) {
+      const uint2 u = lds64(st + q * Geo::STRIDE), v = lds64(st + q * Geo::STRIDE + Geo::VPLANE);
+      *reinterpret_cast<uint4*>(gptr + q * Geo::EB) = make_uint4(u.x, u.y, v.x, v.y);
+    } else if (OUT64) {
+      *reinterpret_cast<uint4*>(gptr + q * Geo::EB) = lds128(st + q * Geo::STRIDE);
+    } else {
+      *reinterpret_cast<uint2*>(gptr + q * Geo::EB) = lds64(st + q * Geo::STRIDE);
+    }
   }
 }
 
@@ -299,11 +324,21 @@ __device__ __noinline__ void flush_slots(char* gptr, uint32_t st, uint32_t lo, u
 // straight-line predicated code (no branch / reconvergence in the hot loop).
 template <bool OUT64, int THREADS>
 __device__ __forceinline__ void flush_full_pred(char* gptr, uint32_t st, bool pred) {
-  constexpr uint32_t EB = OUT64 ? 16 : 8;
-  constexpr uint32_t STRIDE = THREADS * EB;
-  constexpr uint32_t G = kSectorBytes / EB;
+  using Geo = RingGeo<OUT64, THREADS>;
+  constexpr uint32_t EB = Geo::EB;
+  constexpr uint32_t STRIDE = Geo::STRIDE;
+  constexpr uint32_t G = Geo::G;
   uint32_t v[8];
-  if constexpr (EB == 8) {
+  if constexpr (Geo::SPLIT) {
+    // edge q = (u plane slot q, v plane slot q) -> words 4q..4q+3
+#pragma unroll
+    for (uint32_t q = 0; q < G; ++q)
+#pragma unroll
+      for (uint32_t h = 0; h < 2; ++h)
+        asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p ld.shared.v2.u32 {%0,%1}, [%2];\n}"
+                     : "=r"(v[4 * q + 2 * h]), "=r"(v[4 * q + 2 * h + 1])
+                     : "r"(st + q * STRIDE + h * Geo::VPLANE), "r"((uint32_t)pred));
+  } else if constexpr (EB == 8) {
 #pragma unroll
     for (uint32_t q = 0; q < G; ++q)
       asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p ld.shared.v2.u32 {%0,%1}, [%2];\n}"
@@ -333,10 +368,8 @@ __device__ __forceinline__ void flush_full_pred(char* gptr, uint32_t st, bool pr
 template <bool OUT64, int THREADS>
 __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_t half,
                                            uint32_t lo, uint32_t hi) {
-  constexpr uint32_t EB = OUT64 ? 16 : 8;
-  constexpr uint32_t G = kSectorBytes / EB;
-  constexpr uint32_t STRIDE = THREADS * EB;
-  flush_slots<OUT64, THREADS>(gptr, ring_sa + half * G * STRIDE, lo, hi);  // partial last sector
+  using Geo = RingGeo<OUT64, THREADS>;
+  flush_slots<OUT64, THREADS>(gptr, ring_sa + half * Geo::G * Geo::STRIDE, lo, hi);  // partial last sector
 }
 
 // UND: fused to_undirected (reference postprocess.py:26-35): every edge leaves
@@ -358,8 +391,11 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 // SG: scheme-G tables (size not a power of two): sample i = words (hi, lo) of
 // Philox call i/2 (pairs of the 4 outputs), bucket = hi mod n (exact fastmod),
 // fraction = lo -- a full 32-bit fraction, so ties are settled from the word.
+// K32 (uint64 edges, 32 <= k <= 33 -- the C4 tiles' 33 inner bits): the low
+// word of an edge is the funnel-shifted accumulator as is (all 32 bits are
+// edge bits, and any tile prefix lies above bit 32), no mask / prefix LOP3.
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF,
-          bool W64 = false, bool SG = false>
+          bool W64 = false, bool SG = false, bool K32 = false>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
@@ -368,13 +404,16 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   constexpr uint32_t EB = OUT64 ? 16 : 8;       // bytes per edge
   constexpr uint32_t G = kSectorBytes / EB;     // edges per sector (4 or 2)
   constexpr uint32_t R = kRingFactor * G;       // ring slots
-  constexpr uint32_t STRIDE = STHREADS * EB;    // slot-major ring
+  using Geo = RingGeo<OUT64, STHREADS>;
+  constexpr bool SPLIT = Geo::SPLIT;            // uint64 edges as two 8-byte planes
+  constexpr uint32_t SB = Geo::SB;              // staged bytes per slot (one plane)
+  constexpr uint32_t STRIDE = Geo::STRIDE;      // slot-major ring
   // stores straight to the edge's row (no ring); not for REF (dropped lead edges)
   constexpr bool DIRECT = !REF && (RMAT_DIRECT == 2 || (RMAT_DIRECT == 1 && OUT64));
   // byte-replicated bit counts (see RMAT_RC8); 32-bit accumulator path only
   constexpr bool RC8 = RMAT_RC8 && !OUT64 && !W64 && !REF && !kCleanAcc;
   constexpr uint32_t REP = RC8 ? 0x01010101u : 1u;
-  constexpr bool XRING = RMAT_XRING != 0;
+  constexpr bool XRING = RMAT_XRING == 1 || (RMAT_XRING == 2 && OUT64);
   constexpr bool IDPSEL = RMAT_IDP && FB == 16 && !RC8;
   constexpr bool EMUL = RMAT_EMIT_MUL && !RC8 && !W64;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -411,7 +450,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // shared-space addresses: ring slot q of this thread = ring_sa + q * STRIDE
   const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(stage);
   const uint32_t baseA_sa = SMEM ? (uint32_t)__cvta_generic_to_shared(baseA) : 0u;
-  const uint32_t ring_sa = stage_sa + threadIdx.x * EB;
+  const uint32_t ring_sa = stage_sa + threadIdx.x * SB;
 
   const uint32_t k = g.k;
   const uint32_t kr = k * REP;  // emission threshold in the bit-count representation
@@ -498,7 +537,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   const uint32_t ring_mul = tab.one << (LOGR + LOGSTRIDE);
   auto rp_init = [&](uint64_t row) -> uint32_t {
     return XRING ? (uint32_t)(row & (R - 1)) << SLOT_SHIFT
-                 : (uint32_t)(row & (R - 1)) * STRIDE + threadIdx.x * EB;
+                 : (uint32_t)(row & (R - 1)) * STRIDE + threadIdx.x * SB;
   };
   auto rp_slot = [&](uint32_t rp) -> uint32_t { return XRING ? rp >> SLOT_SHIFT : rp / STRIDE; };
   auto rp_half = [&](uint32_t rp) -> uint32_t { return XRING ? rp >> 31 : rp / (G * STRIDE); };
@@ -580,7 +619,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         continue;
       }
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
-      if constexpr (RMAT_AADDR_IMAD && SMEM && FB == 16) {
+      if constexpr ((RMAT_AADDR_IMAD == 1 || (RMAT_AADDR_IMAD == 2 && OUT64)) && SMEM && FB == 16) {
         const uint32_t sa = mad_lo(a4, 2u, baseA_sa);
         asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(q.a[t].x), "=r"(q.a[t].y) : "r"(sa));
       } else {
@@ -676,9 +715,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           vr = mad_lo(cur_r, pw, r);
           // high halves: IMAD.HI (FMA pipe) or a funnel shift (ALU pipe),
           // cur >> (32 - d) (RMAT_HI_SHF: 1 = both sides, 2 = row side only)
-          vrh = RMAT_HI_SHF ? __funnelshift_l(cur_r, 0u, d) : mul_hi(cur_r, pw);
+          // (uint32 edges only: the uint64 variants are ALU-bound already)
+          vrh = (RMAT_HI_SHF && !OUT64) ? __funnelshift_l(cur_r, 0u, d) : mul_hi(cur_r, pw);
           vc = mad_lo(cur_c, pw, c);
-          vch = RMAT_HI_SHF == 1 ? __funnelshift_l(cur_c, 0u, d) : mul_hi(cur_c, pw);
+          vch = (RMAT_HI_SHF == 1 && !OUT64) ? __funnelshift_l(cur_c, 0u, d) : mul_hi(cur_c, pw);
         }
 #ifndef RMAT_VIADDMIN
 #define RMAT_VIADDMIN 1
@@ -704,10 +744,15 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           // edge comes from the high accumulator word (hmask = 1 iff k = 33)
           const uint32_t rlo = PREFIX ? (uint32_t)p.rpre : 0u, rhi = PREFIX ? (uint32_t)(p.rpre >> 32) : 0u;
           const uint32_t clo = PREFIX ? (uint32_t)p.cpre : 0u, chi = PREFIX ? (uint32_t)(p.cpre >> 32) : 0u;
-          u = ((uint64_t)and_or(vrh >> over, hmask, rhi) << 32) |
-              and_or(__funnelshift_r(vr, vrh, over), kmask, rlo);
-          v = ((uint64_t)and_or(vch >> over, hmask, chi) << 32) |
-              and_or(__funnelshift_r(vc, vch, over), kmask, clo);
+          if constexpr (K32) {
+            u = ((uint64_t)and_or(vrh >> over, hmask, rhi) << 32) | __funnelshift_r(vr, vrh, over);
+            v = ((uint64_t)and_or(vch >> over, hmask, chi) << 32) | __funnelshift_r(vc, vch, over);
+          } else {
+            u = ((uint64_t)and_or(vrh >> over, hmask, rhi) << 32) |
+                and_or(__funnelshift_r(vr, vrh, over), kmask, rlo);
+            v = ((uint64_t)and_or(vch >> over, hmask, chi) << 32) |
+                and_or(__funnelshift_r(vc, vch, over), kmask, clo);
+          }
         } else if constexpr (PREFIX) {
           u = and_or(__funnelshift_r(vr, vrh, over), kmask, (uint32_t)p.rpre);
           v = and_or(__funnelshift_r(vc, vch, over), kmask, (uint32_t)p.cpre);
@@ -758,14 +803,26 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       } else if (EMUL && RMAT_STS_ALWAYS && !CAREFUL) {
         // the current slot is not staged yet: a non-edge word there is overwritten later
         if constexpr (OUT64) {
-          sts128(rp_addr(roff), u, v);
+          if constexpr (SPLIT) {
+            const uint32_t ad = rp_addr(roff);
+            sts64(ad, (uint32_t)u, (uint32_t)(u >> 32));
+            sts64(ad + Geo::VPLANE, (uint32_t)v, (uint32_t)(v >> 32));
+          } else {
+            sts128(rp_addr(roff), u, v);
+          }
         } else {
           sts64(rp_addr(roff), (uint32_t)u, (uint32_t)v);
         }
         roff = rp_adv(roff, e01);
       } else if (st) {
         if constexpr (OUT64) {
-          sts128(rp_addr(roff), u, v);
+          if constexpr (SPLIT) {
+            const uint32_t ad = rp_addr(roff);
+            sts64(ad, (uint32_t)u, (uint32_t)(u >> 32));
+            sts64(ad + Geo::VPLANE, (uint32_t)v, (uint32_t)(v >> 32));
+          } else {
+            sts128(rp_addr(roff), u, v);
+          }
         } else {
           sts64(rp_addr(roff), (uint32_t)u, (uint32_t)v);
         }
