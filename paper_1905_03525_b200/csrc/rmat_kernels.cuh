@@ -252,6 +252,16 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 #define RMAT_DIRECT 0
 #endif
 #define RMAT_CALLS_PER_ITER_MAX 4
+// RMAT_LGPTR: 1 = every kernel, 2 = reference-stream (REF) kernels only.
+// Measured: C3 -2.8 %, reference mode +2.5 %, C4 = (so: REF only).
+#ifndef RMAT_LGPTR
+#define RMAT_LGPTR 2
+#endif
+// RMAT_HALF_RP: after a flush check the open sector's ring half is the next
+// slot's half (no toggle bookkeeping).  Measured +0.45 % at C3.
+#ifndef RMAT_HALF_RP
+#define RMAT_HALF_RP 1
+#endif
 // RMAT_PROBE (ablation builds for tools/ab.sh; WRONG OUTPUT, never the product):
 // bit 0: no bucket gathers (bucket words derived from the Philox word, depths
 // 1..16), bit 1: no output (edges XOR-ed into a register, no staging / flush),
@@ -493,6 +503,28 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   const uint64_t T = (uint64_t)gridDim.x * THREADS;
   uint64_t s = (uint64_t)blockIdx.x * THREADS + threadIdx.x;
 
+  // Philox calls per fast iteration (drawn back to back for ILP).  Two calls
+  // fit the 128-register budget of the 512-thread shared-memory CTA only for
+  // the plain uint32 variant.
+#ifndef RMAT_CALLS_PER_ITER
+#define RMAT_CALLS_PER_ITER 2
+#endif
+  // Philox calls drawn back to back (ILP).  Two calls fit the 128-register
+  // budget of the 512-thread shared-memory CTA only for the plain variant.
+#ifndef RMAT_REF_CPI
+#define RMAT_REF_CPI 2
+#endif
+#ifndef RMAT_WIDE_CPI
+#define RMAT_WIDE_CPI 1
+#endif
+  constexpr int CPI = (SG || (SMEM && FB == 32)) ? 1
+                      : (SMEM && (PREFIX || OUT64)) ? RMAT_WIDE_CPI
+                      : REF ? RMAT_REF_CPI
+                      : !SMEM ? RMAT_GLOBAL_CPI : RMAT_CALLS_PER_ITER;
+  // RMAT_LGPTR: the flushed-edge count L lives in the sector pointer itself --
+  // gLend = the stream's end row address, L = (gLend - gptr) / EB -- so the
+  // flush keeps no counter and the fast-path test is one 64-bit compare.
+  constexpr bool LGPTR = (RMAT_LGPTR == 1 || (RMAT_LGPTR == 2 && REF)) && !DIRECT && !RMAT_PROBE;
   StreamPos p = open_stream<REF>(g, s);
   if (!p.valid) return;
   // Tile segments carry their own key: rebuild the round keys per stream.
@@ -567,6 +599,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
   };
   direct_open();
+  // LGPTR: end of the stream's rows and the last sector pointer from which a
+  // whole fast iteration (4 * CPI edges + the ring's R - 1 staged) still fits
+  char* gLend = gptr + (uint64_t)L * EB;
+  char* gfastL = gLend - (uint64_t)(4 * CPI + R - 1) * EB;
   auto staged = [&]() { return (rp_slot(roff) - half * G) & (R - 1); };
 
   // One call's worth of samples: words, bucket entries, byte selectors.
@@ -846,8 +882,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full);
         }
         gptr += full ? kSectorBytes : 0;
-        half ^= (uint32_t)full;
-        L -= full ? G : 0;
+        if constexpr (RMAT_HALF_RP) {
+          half = rp_half(roff);  // the next slot's half is the open sector's, flushed or not
+        } else {
+          half ^= (uint32_t)full;
+        }
+        if constexpr (!LGPTR) L -= full ? G : 0;
       }
     }
   };
@@ -856,27 +896,13 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     // Warp-uniform fast path: every lane has >= 4 edges still to produce
     // (L - staged >= L - (R - 1)), so no stream ends during this call and
     // stores need no cap.
-#ifndef RMAT_CALLS_PER_ITER
-#define RMAT_CALLS_PER_ITER 2
-#endif
-    // Philox calls drawn back to back (ILP).  Two calls fit the 128-register
-    // budget of the 512-thread shared-memory CTA only for the plain variant.
-#ifndef RMAT_REF_CPI
-#define RMAT_REF_CPI 2
-#endif
-#ifndef RMAT_WIDE_CPI
-#define RMAT_WIDE_CPI 1
-#endif
-    constexpr int CPI = (SG || (SMEM && FB == 32)) ? 1
-                        : (SMEM && (PREFIX || OUT64)) ? RMAT_WIDE_CPI
-                        : REF ? RMAT_REF_CPI
-                        : !SMEM ? RMAT_GLOBAL_CPI : RMAT_CALLS_PER_ITER;
     // Tile streams may start mid-sector (lo != 0): such a lane keeps the warp
     // on the careful path until its partial head sector has been flushed, so
     // the fast path's flush is one predicated sector store with no call.
     static_assert(CPI <= RMAT_CALLS_PER_ITER_MAX, "gfast assumes at most RMAT_CALLS_PER_ITER_MAX calls");
     const bool fast_ok = DIRECT ? (gptr <= gfast + (uint64_t)EB * 4u * (2 * RMAT_CALLS_PER_ITER_MAX - CPI))
-                                : (L >= 4 * CPI + R - 1 && (!(PREFIX && kHeadsCareful) || lo == 0));
+                         : LGPTR ? (gptr <= gfastL && (!(PREFIX && kHeadsCareful) || lo == 0))
+                                 : (L >= 4 * CPI + R - 1 && (!(PREFIX && kHeadsCareful) || lo == 0));
     if (__all_sync(0xFFFFFFFFu, fast_ok)) {
       Batch cb[CPI];
 #pragma unroll
@@ -901,6 +927,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       j += CPI;
       continue;
     }
+    if constexpr (LGPTR) L = (uint32_t)((uint64_t)(gLend - gptr) / EB);
     uint32_t left = DIRECT ? (uint32_t)((uint64_t)(gend - gptr) / EB) : L - staged();
     if (left == 0) {
       // Stream done: write its partial last sector, account nf, open the next.
@@ -930,6 +957,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       if (REF) lo += p.drop;
       gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
       direct_open();
+      gLend = gptr + (uint64_t)L * EB;
+      gfastL = gLend - (uint64_t)(4 * CPI + R - 1) * EB;
       continue;
     }
     Batch cb = fetch(j);
