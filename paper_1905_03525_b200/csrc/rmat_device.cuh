@@ -43,9 +43,6 @@ struct SegDev {
 inline uint32_t bucket_word(uint32_t T, uint32_t fm, uint32_t d_self, uint32_t d_alias) {
   return ((RMAT_B_PLAIN ? T : ~T) & ~fm) | d_self | (d_alias << 8);
 }
-#ifndef RMAT_GE_ADDC
-#define RMAT_GE_ADDC 0
-#endif
 #if defined(__CUDACC__)
 struct BucketTest {
   uint32_t ge;  // 1: fraction top bits >= threshold top bits (alias unless a tie says otherwise)
@@ -57,12 +54,6 @@ __device__ __forceinline__ BucketTest bucket_test(uint32_t w, uint32_t b, uint32
   if (RMAT_B_PLAIN) {
     r.ge = w >= b ? 1u : 0u;
     r.tie = (w ^ b) <= fm;
-  } else if (RMAT_GE_ADDC) {
-    // the same carry as one 32-bit add with carry-out (IADD3 + IADD3.X)
-    uint32_t t, ge;
-    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, 0, 0;" : "=r"(t), "=r"(ge) : "r"(w | fm), "r"(b));
-    r.ge = ge;
-    r.tie = t <= fm;
   } else {
     uint64_t sum;
     asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(sum) : "r"(w | fm), "r"(one), "l"((uint64_t)b));

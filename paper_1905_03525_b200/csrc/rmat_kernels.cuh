@@ -118,13 +118,6 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t sel) {
   return r;
 }
 
-// PRMT in replicate-byte mode: byte c[1:0] of a copied into all four bytes.
-__device__ __forceinline__ uint32_t prmt_rc8(uint32_t a, uint32_t c) {
-  uint32_t r;
-  asm("prmt.b32.rc8 %0, %1, 0, %2;" : "=r"(r) : "r"(a), "r"(c));
-  return r;
-}
-
 // dot products on byte selectors: dp2a.lo = a.h0 * b.b0 + a.h1 * b.b1 + c,
 // dp4a = sum of a.bi * b.bi + c.  With b = 1 + 255 * alias ((1, 0) or (0, 1) in
 // bytes 0/1) they pick the self or alias half / byte of a table word.
@@ -142,18 +135,6 @@ __device__ __forceinline__ uint32_t dp4a_u(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-  return r;
-}
-
-__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t r;
-  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-  return r;
-}
-
-__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint32_t c) {
-  uint64_t r;
-  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"((uint64_t)c));
   return r;
 }
 
@@ -227,12 +208,6 @@ constexpr int kSmemThreads = RMAT_SMEM_THREADS;     // packed_smem CTA size
 #define RMAT_CLEAN_ACC 0  // measured 1 % slower at C3 (2 ALU masks -> 1 SHF + 2 IMAD)
 #endif
 constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k-bit mask
-// RMAT_RC8: bit counts (f, d, tt, over) kept byte-replicated (x * 0x01010101) so
-// the depth byte is picked by PRMT.rc8 with the alias bit itself as selector
-// (no per-sample selector add); wrap-mode shifts only look at the low 5 bits.
-#ifndef RMAT_RC8
-#define RMAT_RC8 0
-#endif
 // RMAT_IDP: fragment and depth selection by dot-product instructions (IDP, FMA
 // pipe) on one byte selector instead of three PRMTs (ALU pipe) on two selectors.
 #ifndef RMAT_IDP
@@ -241,17 +216,6 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 #ifndef RMAT_HI_SHF
 #define RMAT_HI_SHF 2  // measured: 2 = +1.0 % at C3 (1.633 vs 1.617e11), 1 = +0.7 %
 #endif
-// RMAT_AADDR_IMAD: fragment-pair address a4 * 2 + base on the FMA pipe.
-#ifndef RMAT_AADDR_IMAD
-#define RMAT_AADDR_IMAD 0
-#endif
-// RMAT_DIRECT: 0 = shared-memory staging ring + whole-sector stores;
-// 1 = uint64 edges stored directly (16-byte stores, L2 merges sector halves);
-// 2 = every width stored directly.
-#ifndef RMAT_DIRECT
-#define RMAT_DIRECT 0
-#endif
-#define RMAT_CALLS_PER_ITER_MAX 4
 // RMAT_LGPTR: 1 = every kernel, 2 = reference-stream (REF) kernels only.
 // Measured: C3 -2.8 %, reference mode +2.5 %, C4 = (so: REF only).
 #ifndef RMAT_LGPTR
@@ -270,48 +234,22 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 #ifndef RMAT_PROBE
 #define RMAT_PROBE 0
 #endif
-// RMAT_XRING: ring slot kept in the top bits of a word (see rp_* in k_packed).
-#ifndef RMAT_XRING
-#define RMAT_XRING 0
-#endif
-// RMAT_EMIT_MUL: emit = hi(tt * ceil(2^32 / k)) (0/1 for tt < 2k) and
-// over = tt - emit * k as IMADs; with RMAT_STS_ALWAYS the fast path stores
-// every sample's edge word into the current slot and advances the slot by
-// `emit` (no predicated stores).
-#ifndef RMAT_EMIT_MUL
-#define RMAT_EMIT_MUL 0
-#endif
-#ifndef RMAT_STS_ALWAYS
-#define RMAT_STS_ALWAYS 0
-#endif
 #ifndef RMAT_HEADS_CAREFUL
 #define RMAT_HEADS_CAREFUL 1
 #endif
 constexpr bool kHeadsCareful = RMAT_HEADS_CAREFUL != 0;  // PREFIX: unaligned heads off the fast path
-// RMAT_SPLIT64: uint64 edges staged as two 8-byte planes (u plane, v plane at
-// +kVPlane) instead of one 16-byte slot: two STS.64 of register pairs need no
-// 4-register-aligned operand group (the STS.128 path costs 3 register moves per
-// sample), and the flush's four LDS.64 land straight in the STG.256 operands.
-#ifndef RMAT_SPLIT64
-#define RMAT_SPLIT64 0
-#endif
-constexpr bool kSplit64 = RMAT_SPLIT64 != 0;
 // slot-major ring addressing wants a power-of-two thread stride
 constexpr int kSmemStrideThreads = kSmemThreads <= 256 ? 256 : kSmemThreads <= 512 ? 512 : 1024;
 constexpr int kGlobalThreads = 256;                 // packed_global CTA size
 
-// Staging-ring geometry per edge width: bytes per slot of one plane, slot
-// stride (slot-major: slot q of thread t at q * stride + t * slot bytes), and
-// the offset of the v plane (split uint64 staging only).
+// Staging-ring geometry per edge width: slot-major, slot q of thread t at
+// q * STRIDE + t * EB (a warp's staging stores hit distinct banks).
 template <bool OUT64, int THREADS>
 struct RingGeo {
-  static constexpr bool SPLIT = OUT64 && kSplit64;
-  static constexpr uint32_t EB = OUT64 ? 16 : 8;          // bytes per edge
-  static constexpr uint32_t SB = SPLIT ? 8 : EB;          // bytes per slot (one plane)
-  static constexpr uint32_t STRIDE = THREADS * SB;
+  static constexpr uint32_t EB = OUT64 ? 16 : 8;          // bytes per edge (= per slot)
+  static constexpr uint32_t STRIDE = THREADS * EB;
   static constexpr uint32_t G = kSectorBytes / EB;        // edges per flushed sector
   static constexpr uint32_t R = kRingFactor * G;          // slots
-  static constexpr uint32_t VPLANE = R * STRIDE;          // v plane offset (SPLIT)
 };
 
 template <bool OUT64, int THREADS>
@@ -319,10 +257,7 @@ __device__ __noinline__ void flush_slots(char* gptr, uint32_t st, uint32_t lo, u
   // Slot-by-slot stores of a partial sector (stream heads / tails; rare).
   using Geo = RingGeo<OUT64, THREADS>;
   for (uint32_t q = lo; q < hi; ++q) {
-    if constexpr (Geo::SPLIT) {
-      const uint2 u = lds64(st + q * Geo::STRIDE), v = lds64(st + q * Geo::STRIDE + Geo::VPLANE);
-      *reinterpret_cast<uint4*>(gptr + q * Geo::EB) = make_uint4(u.x, u.y, v.x, v.y);
-    } else if (OUT64) {
+    if (OUT64) {
       *reinterpret_cast<uint4*>(gptr + q * Geo::EB) = lds128(st + q * Geo::STRIDE);
     } else {
       *reinterpret_cast<uint2*>(gptr + q * Geo::EB) = lds64(st + q * Geo::STRIDE);
@@ -339,16 +274,7 @@ __device__ __forceinline__ void flush_full_pred(char* gptr, uint32_t st, bool pr
   constexpr uint32_t STRIDE = Geo::STRIDE;
   constexpr uint32_t G = Geo::G;
   uint32_t v[8];
-  if constexpr (Geo::SPLIT) {
-    // edge q = (u plane slot q, v plane slot q) -> words 4q..4q+3
-#pragma unroll
-    for (uint32_t q = 0; q < G; ++q)
-#pragma unroll
-      for (uint32_t h = 0; h < 2; ++h)
-        asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p ld.shared.v2.u32 {%0,%1}, [%2];\n}"
-                     : "=r"(v[4 * q + 2 * h]), "=r"(v[4 * q + 2 * h + 1])
-                     : "r"(st + q * STRIDE + h * Geo::VPLANE), "r"((uint32_t)pred));
-  } else if constexpr (EB == 8) {
+  if constexpr (EB == 8) {
 #pragma unroll
     for (uint32_t q = 0; q < G; ++q)
       asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p ld.shared.v2.u32 {%0,%1}, [%2];\n}"
@@ -414,18 +340,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   constexpr uint32_t EB = OUT64 ? 16 : 8;       // bytes per edge
   constexpr uint32_t G = kSectorBytes / EB;     // edges per sector (4 or 2)
   constexpr uint32_t R = kRingFactor * G;       // ring slots
-  using Geo = RingGeo<OUT64, STHREADS>;
-  constexpr bool SPLIT = Geo::SPLIT;            // uint64 edges as two 8-byte planes
-  constexpr uint32_t SB = Geo::SB;              // staged bytes per slot (one plane)
-  constexpr uint32_t STRIDE = Geo::STRIDE;      // slot-major ring
-  // stores straight to the edge's row (no ring); not for REF (dropped lead edges)
-  constexpr bool DIRECT = !REF && (RMAT_DIRECT == 2 || (RMAT_DIRECT == 1 && OUT64));
-  // byte-replicated bit counts (see RMAT_RC8); 32-bit accumulator path only
-  constexpr bool RC8 = RMAT_RC8 && !OUT64 && !W64 && !REF && !kCleanAcc;
-  constexpr uint32_t REP = RC8 ? 0x01010101u : 1u;
-  constexpr bool XRING = RMAT_XRING == 1 || (RMAT_XRING == 2 && OUT64);
-  constexpr bool IDPSEL = RMAT_IDP && FB == 16 && !RC8;
-  constexpr bool EMUL = RMAT_EMIT_MUL && !RC8 && !W64;
+  constexpr uint32_t STRIDE = RingGeo<OUT64, STHREADS>::STRIDE;  // slot-major ring
+  // fragment / depth selection by dot products on one byte selector (RMAT_IDP)
+  constexpr bool IDPSEL = RMAT_IDP && FB == 16;
   extern __shared__ __align__(16) uint8_t smem[];
 
   const uint8_t* baseA;
@@ -459,12 +376,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   }
   // shared-space addresses: ring slot q of this thread = ring_sa + q * STRIDE
   const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(stage);
-  const uint32_t baseA_sa = SMEM ? (uint32_t)__cvta_generic_to_shared(baseA) : 0u;
-  const uint32_t ring_sa = stage_sa + threadIdx.x * SB;
+  const uint32_t ring_sa = stage_sa + threadIdx.x * EB;
 
   const uint32_t k = g.k;
-  const uint32_t kr = k * REP;  // emission threshold in the bit-count representation
-  const uint32_t kmagic = (uint32_t)(0xFFFFFFFFull / k) + 1u;  // ceil(2^32 / k) (EMUL)
   const uint32_t kmask = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
   const uint32_t hmask = k > 32 ? 1u : 0u;  // OUT64: bit 32 of a 33-bit edge
   const uint32_t idxmask4 = tab.idxmask4, fm = tab.fm;
@@ -480,16 +394,6 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   } else if (RMAT_RK_REGS == 0) {
 #pragma unroll
     for (int i = 0; i < 20; ++i) rk[i] = g.rk[i];
-  } else if (RMAT_RK_REGS == 2) {
-    // warp-uniform arithmetic on the launch key: the uniform datapath (URs)
-    uint32_t k0 = g.k0, k1 = g.k1;
-#pragma unroll
-    for (int i = 0; i < 10; ++i) {
-      rk[2 * i] = k0;
-      rk[2 * i + 1] = k1;
-      k0 += 0x9E3779B9u;
-      k1 += 0xBB67AE85u;
-    }
   } else {
     uint32_t k0 = g.k0 + (threadIdx.x & tab.zero), k1 = g.k1 + (threadIdx.x & tab.zero);
 #pragma unroll
@@ -524,7 +428,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // RMAT_LGPTR: the flushed-edge count L lives in the sector pointer itself --
   // gLend = the stream's end row address, L = (gLend - gptr) / EB -- so the
   // flush keeps no counter and the fast-path test is one 64-bit compare.
-  constexpr bool LGPTR = (RMAT_LGPTR == 1 || (RMAT_LGPTR == 2 && REF)) && !DIRECT && !RMAT_PROBE;
+  constexpr bool LGPTR = (RMAT_LGPTR == 1 || (RMAT_LGPTR == 2 && REF)) && !RMAT_PROBE;
   StreamPos p = open_stream<REF>(g, s);
   if (!p.valid) return;
   // Tile segments carry their own key: rebuild the round keys per stream.
@@ -544,7 +448,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   PhiloxPre pre{};
   if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
   uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
-  uint32_t cur_r = 0, cur_c = 0, f = REF ? p.lead * REP : 0u;
+  uint32_t cur_r = 0, cur_c = 0, f = REF ? p.lead : 0u;
   uint64_t cur_r64 = 0, cur_c64 = 0;  // W64 accumulators
   const uint64_t kmask64 = k >= 64 ? ~0ull : ((1ull << k) - 1);
   uint64_t total_nf = 0;
@@ -557,48 +461,21 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // streams are sector-aligned, checked by the host).  L = edges of the
   // stream not yet flushed; the edges still to produce are L - staged.
   uint32_t L = (uint32_t)p.left;
-  // Ring position rp: roff (byte offset from stage) or, with XRING, the slot
-  // in the top log2(R) bits of a word (slot << SLOT_SHIFT) -- the slot then
-  // advances by a plain add that wraps by itself, and the slot's byte offset
-  // is one IMAD.HI: both on the FMA pipe.
-  constexpr uint32_t LOGR = R == 8 ? 3 : R == 4 ? 2 : R == 2 ? 1 : 0;
-  constexpr uint32_t LOGSTRIDE = STRIDE == 16384 ? 14 : STRIDE == 8192 ? 13 : STRIDE == 4096 ? 12
-                                 : STRIDE == 2048 ? 11 : 10;
-  static_assert((1u << LOGR) == R && (1u << LOGSTRIDE) == STRIDE, "ring geometry");
-  constexpr uint32_t SLOT_SHIFT = 32 - LOGR;
-  const uint32_t ring_mul = tab.one << (LOGR + LOGSTRIDE);
+  // Ring position: roff = byte offset of the next edge's slot from `stage`
+  // (slot * STRIDE + tid * EB, slot = output row mod R).
   auto rp_init = [&](uint64_t row) -> uint32_t {
-    return XRING ? (uint32_t)(row & (R - 1)) << SLOT_SHIFT
-                 : (uint32_t)(row & (R - 1)) * STRIDE + threadIdx.x * SB;
+    return (uint32_t)(row & (R - 1)) * STRIDE + threadIdx.x * EB;
   };
-  auto rp_slot = [&](uint32_t rp) -> uint32_t { return XRING ? rp >> SLOT_SHIFT : rp / STRIDE; };
-  auto rp_half = [&](uint32_t rp) -> uint32_t { return XRING ? rp >> 31 : rp / (G * STRIDE); };
-  auto rp_addr = [&](uint32_t rp) -> uint32_t {
-    // (run-time multiplier: a constant power of two would become an ALU LEA.HI)
-    return XRING ? mad_hi(rp, ring_mul, ring_sa) : stage_sa + rp;
-  };
-  auto rp_adv = [&](uint32_t rp, uint32_t n01) -> uint32_t {
-    return XRING ? mad_lo(n01, 1u << SLOT_SHIFT, rp) : (rp + n01 * STRIDE) & (R * STRIDE - 1);
-  };
+  auto rp_slot = [&](uint32_t rp) -> uint32_t { return rp / STRIDE; };
+  auto rp_half = [&](uint32_t rp) -> uint32_t { return rp / (G * STRIDE); };
+  auto rp_addr = [&](uint32_t rp) -> uint32_t { return stage_sa + rp; };
+  auto rp_next = [&](uint32_t rp) -> uint32_t { return (rp + STRIDE) & (R * STRIDE - 1); };
   uint32_t roff = rp_init(p.row);
   uint32_t half = rp_half(roff);
   uint32_t lo = rp_slot(roff) & (G - 1);
   L += lo;  // count the head's missing slots as already "staged"
   if (REF) lo += p.drop;  // a dropped first edge is staged but never flushed (lo may reach G)
   char* gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
-  // DIRECT: gptr = the next edge's row, gfast = last row pointer from which a
-  // whole fast iteration still fits, gend = one past the stream's rows.
-  char* gend = nullptr;
-  char* gfast = nullptr;
-  auto direct_open = [&]() {
-    if constexpr (DIRECT) {
-      gptr = reinterpret_cast<char*>(g.out) + p.row * EB;
-      gend = gptr + p.left * EB;
-      gfast = gend - (uint64_t)EB * 8u * RMAT_CALLS_PER_ITER_MAX;
-      lo = 0;
-    }
-  };
-  direct_open();
   // LGPTR: end of the stream's rows and the last sector pointer from which a
   // whole fast iteration (4 * CPI edges + the ring's R - 1 staged) still fits
   char* gLend = gptr + (uint64_t)L * EB;
@@ -655,12 +532,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         continue;
       }
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
-      if constexpr ((RMAT_AADDR_IMAD == 1 || (RMAT_AADDR_IMAD == 2 && OUT64)) && SMEM && FB == 16) {
-        const uint32_t sa = mad_lo(a4, 2u, baseA_sa);
-        asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(q.a[t].x), "=r"(q.a[t].y) : "r"(sa));
-      } else {
-        q.a[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
-      }
+      q.a[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
     }
     q.tie = false;
 #pragma unroll
@@ -671,7 +543,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       q.tie |= bt.tie;
       q.sel[t] = IDPSEL ? mad_lo(bt.ge, 255u, 1u)      // IDP byte selector: 1 self / 256 alias
                         : mad_lo(bt.ge, 0x22u, 0x4410u);  // PRMT selectors: 0x4410 self / 0x4432 alias
-      q.seld[t] = RC8 ? bt.ge : bt.ge + 0x4440u; // depth byte: 0x4440 self / 0x4441 alias
+      q.seld[t] = bt.ge + 0x4440u;               // depth byte: 0x4440 self / 0x4441 alias
     }
     return q;
   };
@@ -684,7 +556,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         if (bucket_test(cb.w[t], cb.b[t], fm, one).tie) {
           const bool lt = (cb.w[t] & fm) < __ldg(tab.tlo + (cb.x[t] >> 2));
           cb.sel[t] = IDPSEL ? (lt ? 1u : 256u) : lt ? 0x4410u : 0x4432u;
-          cb.seld[t] = RC8 ? (lt ? 0u : 1u) : (lt ? 0x4440u : 0x4441u);
+          cb.seld[t] = lt ? 0x4440u : 0x4441u;
         }
       return;
     }
@@ -695,7 +567,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       if (bucket_test(cb.w[t], cb.b[t], fm, one).tie) {
         const bool lt = (zq[t] & fm) < __ldg(tab.tlo + ((cb.w[t] & idxmask4) >> 2));
         cb.sel[t] = IDPSEL ? (lt ? 1u : 256u) : lt ? 0x4410u : 0x4432u;
-        cb.seld[t] = RC8 ? (lt ? 0u : 1u) : (lt ? 0x4440u : 0x4441u);
+        cb.seld[t] = lt ? 0x4440u : 0x4441u;
       }
   };
   // Fragments of one call appended to the accumulators; stores into the ring
@@ -716,9 +588,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       }
       // (IDP: bytes 2-3 of the selector are 0, so B's threshold bytes drop out)
       const uint32_t d = IDPSEL ? dp4a_u(cb.b[t], cb.sel[t])
-                         : RC8 ? prmt_rc8(cb.b[t], cb.seld[t]) : prmt(cb.b[t], cb.seld[t]);
+                                : prmt(cb.b[t], cb.seld[t]);
       bool st;
-      uint32_t e01 = 0;  // EMUL: 1 iff this sample completes an edge
       uint64_t u, v;
       if constexpr (W64) {
         // 64-bit accumulators: V = cur << d | bits, edge = (V >> over) & kmask
@@ -747,7 +618,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           vch = __funnelshift_l(cur_c, 0u, d);
         } else {
           // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
-          const uint32_t pw = RC8 ? __funnelshift_l(0u, 1u, d) : 1u << d;
+          const uint32_t pw = 1u << d;
           vr = mad_lo(cur_r, pw, r);
           // high halves: IMAD.HI (FMA pipe) or a funnel shift (ALU pipe),
           // cur >> (32 - d) (RMAT_HI_SHF: 1 = both sides, 2 = row side only)
@@ -759,18 +630,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #ifndef RMAT_VIADDMIN
 #define RMAT_VIADDMIN 1
 #endif
-        bool emit;
-        uint32_t over;
-        if constexpr (EMUL) {
-          // tt < 2k (max depth <= k): hi(tt * ceil(2^32/k)) is 1 iff tt >= k
-          e01 = mul_hi(tt, kmagic);
-          over = mad_lo(e01, 0u - k, tt);
-          emit = e01 != 0;
-        } else {
-          emit = tt >= kr;
-          // tt - k wraps above tt when tt < k: over = min(tt - k, tt) in one VIADDMNMX
-          over = RMAT_VIADDMIN ? __viaddmin_u32(tt, 0u - kr, tt) : (emit ? tt - kr : tt);
-        }
+        const bool emit = tt >= k;
+        // tt - k wraps above tt when tt < k: over = min(tt - k, tt) in one VIADDMNMX
+        const uint32_t over = RMAT_VIADDMIN ? __viaddmin_u32(tt, 0u - k, tt) : (emit ? tt - k : tt);
         cur_r = vr;
         cur_c = vc;
         f = over;
@@ -825,49 +687,18 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         if (COUNT) ebits |= (uint32_t)st << t;
         continue;
       }
-      if constexpr (DIRECT) {
-        if (st) {
-          if constexpr (OUT64) {
-            asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(gptr), "l"(u), "l"(v) : "memory");
-          } else {
-            asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(gptr), "r"((uint32_t)u),
-                         "r"((uint32_t)v) : "memory");
-          }
-          gptr += EB;
-          if (CAREFUL) --left;
-        }
-      } else if (EMUL && RMAT_STS_ALWAYS && !CAREFUL) {
-        // the current slot is not staged yet: a non-edge word there is overwritten later
+      if (st) {
         if constexpr (OUT64) {
-          if constexpr (SPLIT) {
-            const uint32_t ad = rp_addr(roff);
-            sts64(ad, (uint32_t)u, (uint32_t)(u >> 32));
-            sts64(ad + Geo::VPLANE, (uint32_t)v, (uint32_t)(v >> 32));
-          } else {
-            sts128(rp_addr(roff), u, v);
-          }
-        } else {
-          sts64(rp_addr(roff), (uint32_t)u, (uint32_t)v);
-        }
-        roff = rp_adv(roff, e01);
-      } else if (st) {
-        if constexpr (OUT64) {
-          if constexpr (SPLIT) {
-            const uint32_t ad = rp_addr(roff);
-            sts64(ad, (uint32_t)u, (uint32_t)(u >> 32));
-            sts64(ad + Geo::VPLANE, (uint32_t)v, (uint32_t)(v >> 32));
-          } else {
-            sts128(rp_addr(roff), u, v);
-          }
+          sts128(rp_addr(roff), u, v);
         } else {
           sts64(rp_addr(roff), (uint32_t)u, (uint32_t)v);
         }
         // next slot; the mask keeps this thread's column bits (tid * EB < STRIDE)
-        roff = rp_adv(roff, 1u);
+        roff = rp_next(roff);
         if (CAREFUL) --left;
       }
-      if (COUNT) ebits |= (EMUL && !CAREFUL ? e01 : (uint32_t)st) << t;
-      if (!DIRECT && (uint32_t)t % G == G - 1) {
+      if (COUNT) ebits |= (uint32_t)st << t;
+      if ((uint32_t)t % G == G - 1) {
         // At most G edges since the last check: the sector at gptr is
         // complete when the next slot has left its ring half.
         const bool full = rp_half(roff) != half;
@@ -882,7 +713,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full);
         }
         gptr += full ? kSectorBytes : 0;
-        if constexpr (RMAT_HALF_RP) {
+        if constexpr (RMAT_HALF_RP && !OUT64) {  // (uint64 edges: 3 more instructions there)
           half = rp_half(roff);  // the next slot's half is the open sector's, flushed or not
         } else {
           half ^= (uint32_t)full;
@@ -899,10 +730,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     // Tile streams may start mid-sector (lo != 0): such a lane keeps the warp
     // on the careful path until its partial head sector has been flushed, so
     // the fast path's flush is one predicated sector store with no call.
-    static_assert(CPI <= RMAT_CALLS_PER_ITER_MAX, "gfast assumes at most RMAT_CALLS_PER_ITER_MAX calls");
-    const bool fast_ok = DIRECT ? (gptr <= gfast + (uint64_t)EB * 4u * (2 * RMAT_CALLS_PER_ITER_MAX - CPI))
-                         : LGPTR ? (gptr <= gfastL && (!(PREFIX && kHeadsCareful) || lo == 0))
-                                 : (L >= 4 * CPI + R - 1 && (!(PREFIX && kHeadsCareful) || lo == 0));
+    const bool fast_ok = (LGPTR ? gptr <= gfastL : L >= 4 * CPI + R - 1) &&
+                         (!(PREFIX && kHeadsCareful) || lo == 0);
     if (__all_sync(0xFFFFFFFFu, fast_ok)) {
       Batch cb[CPI];
 #pragma unroll
@@ -928,11 +757,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       continue;
     }
     if constexpr (LGPTR) L = (uint32_t)((uint64_t)(gLend - gptr) / EB);
-    uint32_t left = DIRECT ? (uint32_t)((uint64_t)(gend - gptr) / EB) : L - staged();
+    uint32_t left = L - staged();
     if (left == 0) {
       // Stream done: write its partial last sector, account nf, open the next.
       const uint32_t hi_slot = rp_slot(roff) & (G - 1);
-      if (!DIRECT && hi_slot > lo) flush_tail<OUT64, STHREADS>(gptr, ring_sa, half, lo, hi_slot);
+      if (hi_slot > lo) flush_tail<OUT64, STHREADS>(gptr, ring_sa, half, lo, hi_slot);
       if (COUNT) {
         // nf (generator.py:255-257): the highest sample of call j-1 that
         // produced an edge this stream needed.
@@ -947,7 +776,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       if (!p.valid) break;
       stream_keys();
       if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
-      j = 0; cur_r = cur_c = 0; f = REF ? p.lead * REP : 0u;
+      j = 0; cur_r = cur_c = 0; f = REF ? p.lead : 0u;
       cur_r64 = cur_c64 = 0;
       L = (uint32_t)p.left;
       roff = rp_init(p.row);
@@ -956,7 +785,6 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       L += lo;
       if (REF) lo += p.drop;
       gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
-      direct_open();
       gLend = gptr + (uint64_t)L * EB;
       gfastL = gLend - (uint64_t)(4 * CPI + R - 1) * EB;
       continue;
