@@ -368,10 +368,19 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RMAT_BENCH_SHARED_GPU=1 (functional test of the torchrun path only, never a
+    # measurement): every rank on cuda:0, gloo for the timing reduction.  The
+    # ranks' kernels are independent (no collective on the data path).
+    shared = os.environ.get("RMAT_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
@@ -483,6 +492,8 @@ def main() -> None:
         "oracle_check": oracle_ok,
         "per_gpu_edges_per_s": rows / (kernel_ms / 1e3),
     }
+    if shared:
+        line["data"] += "; RMAT_BENCH_SHARED_GPU=1: all ranks on one GPU (functional test, not a measurement)"
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
