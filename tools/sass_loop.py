@@ -73,8 +73,9 @@ def main():
               f"(tie block {len(skip)} excluded) = {len(hot)/spi:.2f} per sample")
         print("  per sample by pipe: " + ", ".join(f"{p} {n/spi:.2f}" for p, n in pipes.most_common()))
         # issue-slot model: ALU and FMA-heavy accept a warp instruction every 2
-        # cycles, IMAD.WIDE occupies FMA-heavy for 2 issues (ncu fmaheavy %)
-        wide = sum(n for op, n in ops.items() if op.startswith("IMAD.WIDE"))
+        # cycles; IMAD.WIDE and IMAD.HI occupy FMA-heavy for 4 (measured on the
+        # B200: tools/pipe_rate_probe.cu, profiles/r02_pipe_rate_probe.json)
+        wide = sum(n for op, n in ops.items() if op.startswith(("IMAD.WIDE", "IMAD.HI")))
         alu_c, fma_c = 2 * pipes["alu"], 2 * pipes["fma"] + 2 * wide
         print(f"  cycles per sample per SMSP: alu {alu_c/spi:.1f}, fma-heavy {fma_c/spi:.1f}, "
               f"issue {len(hot)/spi:.1f} -> bound {max(alu_c, fma_c, len(hot))/spi:.1f}")
