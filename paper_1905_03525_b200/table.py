@@ -107,21 +107,28 @@ def _split_code(code: int, depth: int) -> tuple[int, int]:
     return row, col
 
 
+def _even_bits(x: np.ndarray) -> np.ndarray:
+    """Bits 0, 2, 4, ... of each uint64 packed into the low 32 (Morton decode)."""
+    x = x & np.uint64(0x5555555555555555)
+    for shift, mask in ((1, 0x3333333333333333), (2, 0x0F0F0F0F0F0F0F0F),
+                        (4, 0x00FF00FF00FF00FF), (8, 0x0000FFFF0000FFFF), (16, 0x00000000FFFFFFFF)):
+        x = (x | (x >> np.uint64(shift))) & np.uint64(mask)
+    return x
+
+
 def build_fixed_table(params: RmatParams, depth: int) -> FragmentTable:
-    """All 4**depth paths of one length, ordered by interleaved path code."""
+    """Every length-`depth` recursion path, in increasing order of its base-4 path
+    code (root decision most significant) (reference table.py:114-136).  The path
+    code interleaves the row bits (odd positions) with the column bits (even)."""
     if not 1 <= depth <= MAX_FIXED_DEPTH:
         raise DepthOutOfRange(f"fixed fragment depth {depth} not in 1..{MAX_FIXED_DEPTH}")
-    n = 4 ** depth
-    code = np.arange(n, dtype=np.uint64)
+    codes = np.arange(4 ** depth, dtype=np.uint64)
+    row, col = _even_bits(codes >> np.uint64(1)), _even_bits(codes)
     q = np.asarray(params.quadrants, dtype=np.float64)
-    row, col = np.zeros((2, n), dtype=np.uint64)
-    prob = np.ones(n, dtype=np.float64)
-    for lvl in range(depth):  # root level first: probabilities multiply root -> leaf
-        digit = (code >> np.uint64(2 * (depth - 1 - lvl))) & np.uint64(3)
-        row = (row << np.uint64(1)) | (digit >> np.uint64(1))
-        col = (col << np.uint64(1)) | (digit & np.uint64(1))
-        prob *= q[digit]
-    return _finish(row, col, np.full(n, depth, dtype=np.uint64), prob, "fixed")
+    prob = np.ones(codes.size, dtype=np.float64)
+    for lvl in range(depth - 1, -1, -1):  # multiplied root -> leaf: the reference's rounding order
+        prob *= q[(codes >> np.uint64(2 * lvl)) & np.uint64(3)]
+    return _finish(row, col, np.full(codes.size, depth, dtype=np.uint64), prob, "fixed")
 
 
 def build_variable_table(params: RmatParams, size_limit: int,
