@@ -211,14 +211,13 @@ def dedup_local(edges, row_range: tuple[int, int] | None = None,
     from .device import DedupSet
 
     if isinstance(edges, np.ndarray):
-        if row_range is not None and len(edges):
-            lo, hi = row_range
-            if int(edges[:, 0].min()) < lo or int(edges[:, 0].max()) >= hi:
-                raise EdgeOutsideDeclaredTile(f"row outside [{lo}, {hi})")
-        if col_range is not None and len(edges):
-            lo, hi = col_range
-            if int(edges[:, 1].min()) < lo or int(edges[:, 1].max()) >= hi:
-                raise EdgeOutsideDeclaredTile(f"col outside [{lo}, {hi})")
+        for side, name, bounds in ((0, "row", row_range), (1, "col", col_range)):
+            if bounds is not None and len(edges):
+                span = (int(edges[:, side].min()), int(edges[:, side].max()))
+                if span[0] < bounds[0] or span[1] >= bounds[1]:
+                    raise EdgeOutsideDeclaredTile(
+                        f"{name} ids span [{span[0]}, {span[1]}], outside the declared "
+                        f"[{bounds[0]}, {bounds[1]})")
         if len(edges) == 0:
             return edges.copy()
         dev = require_cuda()
