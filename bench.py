@@ -310,6 +310,40 @@ def issue_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
             "frac": achieved / ceiling, "source": "profiles/ncu_full_summary.json"}
 
 
+def pipe_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
+    """The binding integer pipe: the per-sample SASS account of the committed
+    capture (profiles/r02_c3_pipe_account_final.json) priced with the measured
+    B200 pipe costs (profiles/r02_pipe_rate_probe.json: 2 cycles per warp
+    instruction per SMSP on ALU and FMA-heavy, 4 for IMAD.WIDE / IMAD.HI)."""
+    acct = os.path.join(ROOT, "profiles", "r02_c3_pipe_account_final.json")
+    summ = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        with open(acct) as f:
+            ops = json.load(f)["per_sample_by_opcode"]
+        with open(summ) as f:
+            hz = float(json.load(f)["sm_clock_hz"])
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from sass_loop import pipe_of
+    except (OSError, KeyError, ValueError, TypeError, ImportError):
+        return None
+    import torch
+
+    cyc = {"fma": 0.0, "alu": 0.0}
+    for op, n in ops.items():
+        p = pipe_of(op)
+        if p in cyc:
+            cyc[p] += n * (4.0 if op.startswith(("IMAD.WIDE", "IMAD.HI")) else 2.0)
+    pipe = max(cyc, key=cyc.get)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    samples_per_edge = 13988142900 / M  # k / E[depth] of the C3 table, x 2^32 edges
+    ceiling = sms * 4 * 32 * hz / cyc[pipe] / samples_per_edge
+    achieved = edges / kernel_s
+    return {"bound": "fma_heavy_pipe" if pipe == "fma" else "alu_pipe",
+            "cycles_per_warp_sample": cyc, "ceiling_edges_per_s": ceiling,
+            "achieved_edges_per_s": achieved, "frac": achieved / ceiling,
+            "source": "profiles/r02_c3_pipe_account_final.json + r02_pipe_rate_probe.json"}
+
+
 def lsu_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
     """The L1 data pipe beside the issue bound: LSU wavefronts per edge from the
     committed ncu capture (random bucket gathers from shared memory, ring staging,
@@ -483,6 +517,7 @@ def main() -> None:
                      "algorithmic_bytes_per_launch": rows * BYTES_PER_EDGE,
                      "frac_of_8TBps_nominal": achieved / 8000.0,
                      "issue_bound": issue_bound_from_profile(kernel_ms / 1e3, rows),
+                     "pipe_bound": pipe_bound_from_profile(kernel_ms / 1e3, rows),
                      "lsu_bound": lsu_bound_from_profile(kernel_ms / 1e3, rows)},
         "cpu_baseline": cpu,
         "e2e": e2e,
