@@ -14,10 +14,12 @@
   printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
 
 enum Op { IMADWIDE, IMADLO, IMADHI, LOP3, IADD3, SHF, PRMT, IDP4A, IDP2A, LOP3_IMADWIDE, LOP3_IMADLO,
-          SHF_IMADLO, N_OPS };
+          SHF_IMADLO, IMADLO_IMM, IMADHI_IMM, LOHI_IMM_LOP3, N_OPS };
 static const char* kName[N_OPS] = {"IMAD.WIDE.U32(+LOP3)", "IMAD", "IMAD.HI.U32", "LOP3", "IADD3",
                                    "SHF", "PRMT", "IDP.4A", "IDP.2A", "philox half-round (IMAD.WIDE+LOP3)",
-                                   "LOP3+IMAD", "SHF+IMAD"};
+                                   "LOP3+IMAD", "SHF+IMAD", "IMAD (immediate multiplier)",
+                                   "IMAD.HI (immediate multiplier)",
+                                   "philox half-round as IMAD + IMAD.HI (immediates) + LOP3"};
 
 template <int OP>
 __device__ __forceinline__ void step(uint32_t& x, uint32_t& y, uint32_t a, uint32_t b) {
@@ -52,6 +54,16 @@ __device__ __forceinline__ void step(uint32_t& x, uint32_t& y, uint32_t a, uint3
   } else if constexpr (OP == LOP3_IMADLO) {
     step<LOP3>(x, y, a, b);
     step<IMADLO>(y, x, a, b);
+  } else if constexpr (OP == IMADLO_IMM) {
+    asm volatile("mad.lo.u32 %0, %0, 0xD2511F53, %1;" : "+r"(x) : "r"(b));
+  } else if constexpr (OP == IMADHI_IMM) {
+    asm volatile("mad.hi.u32 %0, %0, 0xD2511F53, %1;" : "+r"(x) : "r"(b));
+  } else if constexpr (OP == LOHI_IMM_LOP3) {
+    uint32_t lo, hi;
+    asm volatile("mul.lo.u32 %0, %1, 0xD2511F53;" : "=r"(lo) : "r"(x));
+    asm volatile("mul.hi.u32 %0, %1, 0xD2511F53;" : "=r"(hi) : "r"(x));
+    asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(x) : "r"(hi), "r"(y), "r"(a));
+    y = lo;
   } else if constexpr (OP == SHF_IMADLO) {
     step<SHF>(x, y, a, b);
     step<IMADLO>(y, x, a, b);
@@ -59,7 +71,7 @@ __device__ __forceinline__ void step(uint32_t& x, uint32_t& y, uint32_t a, uint3
 }
 
 template <int OP>
-__global__ void __launch_bounds__(256, OP == LOP3_IMADWIDE ? 4 : 8) probe(uint32_t a, uint32_t b, int iters, uint32_t* out) {
+__global__ void __launch_bounds__(256, (OP == LOP3_IMADWIDE || OP == LOHI_IMM_LOP3) ? 4 : 8) probe(uint32_t a, uint32_t b, int iters, uint32_t* out) {
   uint32_t x[8], y[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) { x[c] = threadIdx.x + c; y[c] = blockIdx.x * 7 + c; }
@@ -77,10 +89,11 @@ __global__ void __launch_bounds__(256, OP == LOP3_IMADWIDE ? 4 : 8) probe(uint32
 
 template <int OP>
 int run(int sms, int clk, uint32_t* out) {
-  const int blocks = sms * (OP == LOP3_IMADWIDE ? 4 : 8), iters = 2000;
+  const int blocks = sms * ((OP == LOP3_IMADWIDE || OP == LOHI_IMM_LOP3) ? 4 : 8), iters = 2000;
   // warp instructions per step (IMAD.WIDE probe: one IMAD.WIDE + half a LOP3 --
   // ptxas merges two XORs into one three-input LOP3)
-  const double per_step = OP == IMADWIDE ? 1.5 : OP >= LOP3_IMADWIDE ? 2.0 : 1.0;
+  const double per_step = OP == IMADWIDE ? 1.5 : OP == LOHI_IMM_LOP3 ? 3.0
+                          : (OP >= LOP3_IMADWIDE && OP <= SHF_IMADLO) ? 2.0 : 1.0;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int rep = 0; rep < 2; ++rep) {
@@ -109,7 +122,8 @@ int main() {
       run<LOP3>(sms, clk, out) || run<SHF>(sms, clk, out) ||
       run<PRMT>(sms, clk, out) || run<IDP4A>(sms, clk, out) || run<IDP2A>(sms, clk, out) ||
       run<LOP3_IMADWIDE>(sms, clk, out) || run<LOP3_IMADLO>(sms, clk, out) ||
-      run<SHF_IMADLO>(sms, clk, out))
+      run<SHF_IMADLO>(sms, clk, out) || run<IMADLO_IMM>(sms, clk, out) ||
+      run<IMADHI_IMM>(sms, clk, out) || run<LOHI_IMM_LOP3>(sms, clk, out))
     return 1;
   return 0;
 }
