@@ -310,6 +310,17 @@ def issue_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
             "frac": achieved / ceiling, "source": "profiles/ncu_full_summary.json"}
 
 
+# SASS opcode families of the two integer issue pipes (the rest: LSU, branch, uniform)
+_ALU_OPS = ("LOP3", "SHF", "PRMT", "IADD3", "ISETP", "SEL", "VIMNMX", "VIADDMNMX", "FLO", "BMSK",
+            "LEA", "POPC", "FSETP", "FMNMX", "PLOP3", "P2R", "R2P")
+_FMA_OPS = ("IMAD", "VIADD", "FFMA", "FADD", "FMUL", "IDP")
+
+
+def pipe_of(op: str) -> str:
+    base = op.split(".")[0]
+    return "alu" if base in _ALU_OPS else "fma" if base in _FMA_OPS else "other"
+
+
 def pipe_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
     """The binding integer pipe: the per-sample SASS account of the committed
     capture (profiles/r02_c3_pipe_account_final.json) priced with the measured
@@ -322,9 +333,7 @@ def pipe_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
             ops = json.load(f)["per_sample_by_opcode"]
         with open(summ) as f:
             hz = float(json.load(f)["sm_clock_hz"])
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        from sass_loop import pipe_of
-    except (OSError, KeyError, ValueError, TypeError, ImportError):
+    except (OSError, KeyError, ValueError, TypeError):
         return None
     import torch
 
