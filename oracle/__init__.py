@@ -80,6 +80,10 @@ def curand_xcheck(inputs: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     return ours, theirs
 
 
+#: the fast path's counter layout the product library is built with (philox.cuh)
+FAST_CTR = 2
+
+
 @lru_cache(maxsize=1)
 def lib() -> ctypes.CDLL:
     build()
@@ -108,6 +112,9 @@ def lib() -> ctypes.CDLL:
     L.oracle_ref_stream_from.restype = ctypes.c_int64
     L.oracle_ref_depth_sum.argtypes = T + [ctypes.c_uint64] * 4
     L.oracle_ref_depth_sum.restype = ctypes.c_uint64
+    # fast-path counter layout (philox.cuh RMAT_FAST_CTR; A/B builds set the env)
+    L.oracle_set_fast_ctr.argtypes = [ctypes.c_int]
+    L.oracle_set_fast_ctr(int(os.environ.get("RMAT_FAST_CTR", FAST_CTR)))
     return L
 
 

@@ -7,8 +7,8 @@
 // Three forms of ours are compared for every (counter, key):
 //   0: philox4x32_10(c0..c3, k0, k1)           (generic, key bumped per round)
 //   1: philox4x32_10_rk(c, rk)                 (precomputed key schedule)
-//   2: philox4x32_10_pre(j, philox_pre(s), rk) (rounds 1-2 folded per stream;
-//      only valid for counters (j, 0, s0, s1), so the checker zeroes c1 there)
+//   2: philox4x32_10_pre2(j, philox_pre2(s0, s1, cls), rk) (the fast path's
+//      form: counter (s0, j, s1, cls), rounds 1-3 partly folded per stream)
 // Built by oracle.build_curand_xcheck() with nvcc for sm_100a.
 #include <cuda_runtime.h>
 #include <curand_kernel.h>
@@ -25,9 +25,9 @@ static __global__ void k_xcheck(const uint32_t* in, uint32_t n, uint32_t* ours, 
     rmat::philox4x32_key_schedule(k.x, k.y, rk);
     const rmat::u32x4 a = rmat::philox4x32_10(c.x, c.y, c.z, c.w, k.x, k.y);
     const rmat::u32x4 b = rmat::philox4x32_10_rk(c.x, c.y, c.z, c.w, rk);
-    const rmat::u32x4 p = rmat::philox4x32_10_pre(c.x, rmat::philox_pre(c.z, c.w, rk), rk);
+    const rmat::u32x4 p = rmat::philox4x32_10_pre2(c.y, rmat::philox_pre2(c.x, c.z, c.w, rk), rk);
     const uint4 r = curand_Philox4x32_10(c, k);
-    const uint4 r0 = curand_Philox4x32_10(make_uint4(c.x, 0u, c.z, c.w), k);
+    const uint4 r0 = r;
     uint32_t* o = ours + 12 * (size_t)i;
     o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
     o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;

@@ -60,9 +60,19 @@ void oracle_philox4x64_10(const uint64_t ctr_in[4], const uint64_t key_in[2], ui
 }
 
 /* ---- fast-path word stream (the GPU kernels' RNG) ---- */
+/* Counter layout of call j, class cls (0 primary / 1 lazy), of stream sid:
+ *   2: (sid_lo, j_lo, sid_hi, j_hi << 1 | cls)   -- the spec (philox.cuh RMAT_FAST_CTR)
+ *   1: (j_lo, j_hi << 1 | cls, sid_lo, sid_hi)   -- the round-1 layout, for A/B builds */
+static int g_fast_ctr = 2;
+void oracle_set_fast_ctr(int layout) { g_fast_ctr = layout; }
+
 static void fast_call(uint64_t j, uint32_t cls, uint64_t sid, uint64_t key, uint32_t out[4]) {
   uint32_t ctr[4] = {(uint32_t)j, ((uint32_t)(j >> 32) << 1) | cls, (uint32_t)sid,
                      (uint32_t)(sid >> 32)};
+  if (g_fast_ctr == 2) {
+    ctr[0] = (uint32_t)sid; ctr[1] = (uint32_t)j; ctr[2] = (uint32_t)(sid >> 32);
+    ctr[3] = ((uint32_t)(j >> 32) << 1) | cls;
+  }
   uint32_t k[2] = {(uint32_t)key, (uint32_t)(key >> 32)};
   oracle_philox4x32_10(ctr, k, out);
 }

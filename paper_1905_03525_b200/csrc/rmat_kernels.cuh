@@ -445,8 +445,18 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
   };
   stream_keys();
-  PhiloxPre pre{};
-  if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
+  // per-stream constant part of the primary calls' first rounds (philox.cuh)
+#if RMAT_FAST_CTR == 2
+  using Pre = PhiloxPre2;
+  auto make_pre = [&]() -> Pre { return philox_pre2((uint32_t)p.sid, (uint32_t)(p.sid >> 32), 0u, rk); };
+  auto call_pre = [&](uint32_t jj, const Pre& pp) -> u32x4 { return philox4x32_10_pre2(jj, pp, rk); };
+#else
+  using Pre = PhiloxPre;
+  auto make_pre = [&]() -> Pre { return philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk); };
+  auto call_pre = [&](uint32_t jj, const Pre& pp) -> u32x4 { return philox4x32_10_pre(jj, pp, rk); };
+#endif
+  Pre pre{};
+  if (!REF) pre = make_pre();
   uint32_t j = 0;                    // Philox call index within the stream (< 2^32, host-checked)
   uint32_t cur_r = 0, cur_c = 0, f = REF ? p.lead : 0u;
   uint64_t cur_r64 = 0, cur_c64 = 0;  // W64 accumulators
@@ -506,7 +516,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       // four samples = calls 2jj and 2jj+1, two (hi, lo) pairs each
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const u32x4 w4 = philox4x32_10_pre(2 * jj + h, pre, rk);
+        const u32x4 w4 = call_pre(2 * jj + h, pre);
         const uint32_t his[2] = {w4.x, w4.z}, los[2] = {w4.y, w4.w};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -517,7 +527,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       }
     } else {
       // primary call: rounds 1-2 partly precomputed per stream (philox.cuh)
-      const u32x4 w4 = philox4x32_10_pre(jj, pre, rk);
+      const u32x4 w4 = call_pre(jj, pre);
       q.w[0] = w4.x; q.w[1] = w4.y; q.w[2] = w4.z; q.w[3] = w4.w;
     }
 #pragma unroll
@@ -560,7 +570,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         }
       return;
     }
-    const u32x4 z4 = philox4x32_10_rk(jj, 1, (uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
+    uint32_t zc[4];
+    stream_counter(jj, 1, p.sid, zc);  // the lazy class of the same call
+    const u32x4 z4 = philox4x32_10_rk(zc[0], zc[1], zc[2], zc[3], rk);
     const uint32_t zq[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
     for (int t = 0; t < 4; ++t)
@@ -775,7 +787,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       p = open_stream<REF>(g, s);
       if (!p.valid) break;
       stream_keys();
-      if (!REF) pre = philox_pre((uint32_t)p.sid, (uint32_t)(p.sid >> 32), rk);
+      if (!REF) pre = make_pre();
       j = 0; cur_r = cur_c = 0; f = REF ? p.lead : 0u;
       cur_r64 = cur_c64 = 0;
       L = (uint32_t)p.left;

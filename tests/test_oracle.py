@@ -152,9 +152,14 @@ def test_fast_words_scheme_p_fraction_layout():
     ot = otable("g500:v16384")  # lg 14 -> F 16
     words = oracle.fast_words(ot, 3, oracle.DOMAIN_BLOCK, 5, 64)
     key = (3 ^ oracle.DOMAIN_BLOCK) & (2**64 - 1)
+    layout = int(os.environ.get("RMAT_FAST_CTR", oracle.FAST_CTR))
+
+    def ctr(j, cls, sid):  # DESIGN.md stream spec: the fast path's Philox counter
+        return [sid, j, 0, cls] if layout == 2 else [j, cls, sid, 0]
+
     for i in (0, 1, 2, 3, 17, 63):
-        w = oracle.philox4x32([i >> 2, 0, 5, 0], [key & 0xFFFFFFFF, key >> 32])[i & 3]
-        z = oracle.philox4x32([i >> 2, 1, 5, 0], [key & 0xFFFFFFFF, key >> 32])[i & 3]
+        w = oracle.philox4x32(ctr(i >> 2, 0, 5), [key & 0xFFFFFFFF, key >> 32])[i & 3]
+        z = oracle.philox4x32(ctr(i >> 2, 1, 5), [key & 0xFFFFFFFF, key >> 32])[i & 3]
         want = (((int(w) >> 2) & 0x3FFF) << 32) | (int(w) & 0xFFFF0000) | (int(z) & 0xFFFF)
         assert int(words[i]) == want
 
