@@ -9,6 +9,8 @@
 //                read with ld.shared::cluster (mapa) -- 1/C local, (C-1)/C remote
 //   2: global -- the whole table (C * 2^14 entries) in global memory, read with
 //                ld.global.nc (L1 / L2 resident), the packed_global variant today
+//   3: global, interleaved 16-byte records {A, B, pad}: one LDG.128 per sample
+//   4: global, interleaved 32-byte records (FB = 32 tables: 16 + 4 bytes): one sector
 // Reports gathers (samples) per SM per cycle and per second.
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/_dsmem_probe tools/dsmem_probe.cu
 #include <cooperative_groups.h>
@@ -51,7 +53,7 @@ probe(const uint32_t* __restrict__ gB, const uint2* __restrict__ gA, int iters, 
   uint32_t* sB = reinterpret_cast<uint32_t*>(smem + SLICE * 8);
   uint32_t rank = 0;
   if (MODE == 1) rank = cg::this_cluster().block_rank();
-  if (MODE != 2) {
+  if (MODE < 2) {
     for (int i = threadIdx.x; i < SLICE; i += THREADS) {
       sA[i] = gA[rank * SLICE + i];
       sB[i] = gB[rank * SLICE + i];
@@ -75,9 +77,16 @@ probe(const uint32_t* __restrict__ gB, const uint2* __restrict__ gA, int iters, 
         const uint32_t r = idx >> 14, o = idx & (SLICE - 1);
         const uint2 a = ld_cluster_v2(baseA + o * 8, r);
         acc ^= ld_cluster_u32(baseB + o * 4, r) + a.x + a.y;
-      } else {
+      } else if (MODE == 2) {
         const uint2 a = __ldg(gA + idx);
         acc ^= __ldg(gB + idx) + a.x + a.y;
+      } else if (MODE == 3) {  // interleaved 16-byte records {A.x, A.y, B, pad}: one LDG.128
+        const uint4 r = __ldg(reinterpret_cast<const uint4*>(gA) + idx);
+        acc ^= r.z + r.x + r.y;
+      } else {                 // interleaved 32-byte records (20 bytes used): two LDG.128, one sector
+        const uint4* rec = reinterpret_cast<const uint4*>(gA) + 2 * (size_t)idx;
+        const uint4 r0 = __ldg(rec), r1 = __ldg(rec + 1);
+        acc ^= r0.x + r0.y + r0.z + r0.w + r1.x;
       }
     }
   }
@@ -88,7 +97,7 @@ probe(const uint32_t* __restrict__ gB, const uint2* __restrict__ gA, int iters, 
 template <int MODE, int C>
 int run(const uint32_t* gB, const uint2* gA, uint32_t* out, int sms, int clk_khz) {
   auto k = probe<MODE, C>;
-  const size_t smem = MODE == 2 ? 0 : (size_t)SLICE * 12;
+  const size_t smem = MODE >= 2 ? 0 : (size_t)SLICE * 12;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (MODE == 1) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   int blocks = MODE == 1 ? (sms / C) * C : sms;
@@ -119,7 +128,7 @@ int run(const uint32_t* gB, const uint2* gA, uint32_t* out, int sms, int clk_khz
            gathers / blocks / (ms * 1e-3 * clk_khz * 1e3));
     return 0;
   }
-  const int iters = MODE == 2 ? 500 : 2000;
+  const int iters = MODE >= 2 ? 500 : 2000;
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   for (int rep = 0; rep < 2; ++rep) {
     cudaEventRecord(a);
@@ -131,7 +140,8 @@ int run(const uint32_t* gB, const uint2* gA, uint32_t* out, int sms, int clk_khz
   const double gathers = (double)blocks * THREADS * iters * 8;
   printf("{\"mode\": \"%s\", \"cluster\": %d, \"ctas\": %d, \"table_entries\": %d, \"ms\": %.3f, "
          "\"samples_per_s\": %.4g, \"samples_per_sm_cycle\": %.3f}\n",
-         MODE == 0 ? "local" : "global", C, blocks, MODE == 0 ? SLICE : C * SLICE, ms,
+         MODE == 0 ? "local" : MODE == 2 ? "global" : MODE == 3 ? "global_rec16" : "global_rec32",
+         C, blocks, MODE == 0 ? SLICE : C * SLICE, ms,
          gathers / ms * 1e3, gathers / sms / (ms * 1e-3 * clk_khz * 1e3));
   return 0;
 }
@@ -142,8 +152,8 @@ int main() {
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const int n = 8 * SLICE;
   uint32_t* gB; uint2* gA; uint32_t* out;
-  CK(cudaMalloc(&gB, n * 4)); CK(cudaMalloc(&gA, n * 8)); CK(cudaMalloc(&out, 4));
-  CK(cudaMemset(gB, 1, n * 4)); CK(cudaMemset(gA, 2, n * 8));
+  CK(cudaMalloc(&gB, n * 4)); CK(cudaMalloc(&gA, n * 32)); CK(cudaMalloc(&out, 4));
+  CK(cudaMemset(gB, 1, n * 4)); CK(cudaMemset(gA, 2, n * 32));
   printf("{\"sms\": %d, \"clock_khz\": %d}\n", sms, clk);
   if (run<0, 1>(gB, gA, out, sms, clk)) return 1;
   if (run<1, 2>(gB, gA, out, sms, clk)) return 1;
@@ -151,5 +161,7 @@ int main() {
   if (run<1, 8>(gB, gA, out, sms, clk)) return 1;
   if (run<2, 4>(gB, gA, out, sms, clk)) return 1;
   if (run<2, 8>(gB, gA, out, sms, clk)) return 1;
+  if (run<3, 4>(gB, gA, out, sms, clk)) return 1;
+  if (run<4, 4>(gB, gA, out, sms, clk)) return 1;
   return 0;
 }
