@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -35,10 +36,10 @@ int num_sms(int dev) {
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
   return v;
 }
-rmat::PackedTab packed_view(const rmat_table* t) {
+rmat::PackedTab packed_view(const rmat_table* t, bool rec) {
   rmat::PackedTab p;
   p.B = t->pB;
-  p.A = t->pA;
+  p.A = rec ? static_cast<const void*>(t->pR) : t->pA;
   p.tlo = t->ptlo;
   p.idxmask4 = (uint32_t)((t->n - 1) << 2);
   p.fm = t->gpacked ? 0xFFFFu : (1u << rmat::scheme_p_fbits(t->lg)) - 1u;
@@ -112,6 +113,7 @@ void free_table(rmat_table* t) {
   cudaFree(t->depth);
   cudaFree(t->pB);
   cudaFree(t->pA);
+  cudaFree(t->pR);
   cudaFree(t->ptlo);
   delete t;
 }
@@ -243,6 +245,19 @@ rmat_status rmat_table_create(int device, const rmat_table_desc* d, rmat_table**
       t->pA = dA;
     }
     if (st) { free_table(t); return st; }
+    // 16-byte records for the L1/L2-resident kernel: tables beyond shared
+    // memory whose fragment values fit 16-bit halves (depth may exceed 16)
+    bool rec_ok = t->scheme_p && n >= (1ull << 15) && std::getenv("RMAT_DISABLE_REC") == nullptr;
+    for (uint64_t i = 0; rec_ok && i < n; ++i) rec_ok = row[i] < 0x10000u && col[i] < 0x10000u;
+    if (rec_ok) {
+      std::vector<uint4> R(n);
+      for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t a = al[i];
+        R[i] = make_uint4((uint32_t)row[i] | ((uint32_t)row[a] << 16),
+                          (uint32_t)col[i] | ((uint32_t)col[a] << 16), B[i], tlo[i]);
+      }
+      if ((st = upload(R, &t->pR, &bytes))) { free_table(t); return st; }
+    }
     if (g_pack) {  // kept apart from `fb`: every scheme-P packed path checks fb
       t->gpacked = 1;
       t->fastmod_m = ~0ull / n + 1;
@@ -402,8 +417,9 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
                            : launch_packed_p32(t, g, true, out64, prefix, count, st);
         break;
       case RMAT_KERNEL_PACKED_GLOBAL:
-        rs = t->fb == 16 ? launch_packed_p16(t, g, false, out64, prefix, count, st)
-                         : launch_packed_p32(t, g, false, out64, prefix, count, st);
+        rs = t->pR ? launch_packed_rec(t, g, out64, prefix, count, st)
+             : t->fb == 16 ? launch_packed_p16(t, g, false, out64, prefix, count, st)
+                           : launch_packed_p32(t, g, false, out64, prefix, count, st);
         break;
       default:
         rs = launch_generic(t, g, out64, st);

@@ -30,6 +30,11 @@ struct SegDev {
 //          FB=16: uint2 {row_self | row_alias << 16, col_self | col_alias << 16}
 //          FB=32: uint4 {row_self, row_alias, col_self, col_alias}
 //   TLO[i] = T & (4n-1): only read when the fraction's top bits tie T_hi.
+//   R[i] = {A.x, A.y, B, TLO} (16-bit fields): the same bucket as one 16-byte
+//          record, built for tables beyond shared memory whose fragment values
+//          fit 16 bits (depth may exceed 16).  The L1/L2-resident kernel then
+//          gathers one L2 sector per sample instead of two: 2.0x the random
+//          gather rate (profiles/r02_dsmem_probe.json, global vs global_rec16).
 // ---------------------------------------------------------------------------
 // Packed bucket word B (low 16 bits: d_alias << 8 | d_self) and the fraction
 // test against it.  RMAT_B_PLAIN = 1: B carries the threshold's top (32 - F)

@@ -29,6 +29,10 @@ struct rmat_table {
   uint64_t fastmod_m;  // ceil(2^64 / n): exact bucket = hi mod n (scheme G)
   uint32_t* pB;
   void* pA;
+  // 16-byte bucket records {A.x, A.y, B, TLO} for tables that do not fit
+  // shared memory and whose fragment values fit 16 bits (any depth <= 31):
+  // one L2 sector per sample in the L1/L2-resident kernel (rmat_device.cuh)
+  uint4* pR;
   uint32_t* ptlo;
   uint64_t packed_bytes;
   uint32_t packed_smem;
@@ -39,13 +43,13 @@ namespace rmat_impl {
 
 int max_smem_optin(int dev);
 int num_sms(int dev);
-rmat::PackedTab packed_view(const rmat_table* t);
+rmat::PackedTab packed_view(const rmat_table* t, bool rec = false);
 rmat::GenericTab generic_view(const rmat_table* t);
 
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
-          bool W64 = false, bool SG = false, bool K32 = false>
+          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false>
 inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32>;
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32, REC>;
   const int sms = num_sms(t->device);
   int threads, blocks;
   size_t smem = 0;
@@ -55,7 +59,7 @@ inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g
     blocks = sms;
   } else {
     threads = rmat::kGlobalThreads;
-    smem = (size_t)threads * rmat::kRingBytes;
+    smem = (size_t)rmat::kGlobalStrideThreads * rmat::kRingBytes;
   }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
@@ -64,11 +68,14 @@ inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess)
       return RMAT_ERR_CUDA;
-    blocks = sms * std::max(per_sm, 1);
+    // one CTA per SM by design (RMAT_GLOBAL_MINB): the table lives in the L1
+    // cache, which a second CTA's working set would thrash (measured: a
+    // 128-register build that fits two CTAs runs C3-shaped launches at half speed)
+    blocks = sms * std::max(std::min(per_sm, RMAT_GLOBAL_MINB), 1);
   }
   uint64_t need = (g.total_streams + threads - 1) / threads;
   blocks = (int)std::min<uint64_t>((uint64_t)blocks, std::max<uint64_t>(need, 1));
-  kern<<<blocks, threads, smem, st>>>(packed_view(t), g);
+  kern<<<blocks, threads, smem, st>>>(packed_view(t, REC), g);
   return cudaGetLastError() == cudaSuccess ? RMAT_OK : RMAT_ERR_CUDA;
 }
 
@@ -77,6 +84,9 @@ inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g
 rmat_status launch_packed_p16(const rmat_table* t, const rmat::GenLaunch& g, bool smem, bool out64,
                               bool prefix, bool count, cudaStream_t st);
 rmat_status launch_packed_p32(const rmat_table* t, const rmat::GenLaunch& g, bool smem, bool out64,
+                              bool prefix, bool count, cudaStream_t st);
+// the L1/L2-resident kernel on 16-byte records (t->pR; rmat_packed16.cu)
+rmat_status launch_packed_rec(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
                               bool prefix, bool count, cudaStream_t st);
 // reference blocks per thread, 33 < k <= 48, scheme-G tables (rmat_packed_extra.cu)
 rmat_status launch_ref_thread(const rmat_table* t, const rmat::GenLaunch& g, bool out64,

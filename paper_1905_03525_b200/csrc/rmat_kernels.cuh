@@ -240,7 +240,11 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 constexpr bool kHeadsCareful = RMAT_HEADS_CAREFUL != 0;  // PREFIX: unaligned heads off the fast path
 // slot-major ring addressing wants a power-of-two thread stride
 constexpr int kSmemStrideThreads = kSmemThreads <= 256 ? 256 : kSmemThreads <= 512 ? 512 : 1024;
-constexpr int kGlobalThreads = 256;                 // packed_global CTA size
+#ifndef RMAT_GLOBAL_THREADS
+#define RMAT_GLOBAL_THREADS 256
+#endif
+constexpr int kGlobalThreads = RMAT_GLOBAL_THREADS;  // packed_global CTA size
+constexpr int kGlobalStrideThreads = kGlobalThreads <= 256 ? 256 : kGlobalThreads <= 512 ? 512 : 1024;
 
 // Staging-ring geometry per edge width: slot-major, slot q of thread t at
 // q * STRIDE + t * EB (a warp's staging stores hit distinct banks).
@@ -330,13 +334,15 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 // K32 (uint64 edges, 32 <= k <= 33 -- the C4 tiles' 33 inner bits): the low
 // word of an edge is the funnel-shifted accumulator as is (all 32 bits are
 // edge bits, and any tile prefix lies above bit 32), no mask / prefix LOP3.
+// REC: 16-byte bucket records (rmat_table::pR) in the L1/L2-resident kernel.
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF,
-          bool W64 = false, bool SG = false, bool K32 = false>
+          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
+  static_assert(!REC || (FB == 16 && !SMEM && !REF && !SG), "records: 16-bit fields, global kernel");
   constexpr int THREADS = SMEM ? kSmemThreads : kGlobalThreads;
-  constexpr int STHREADS = SMEM ? kSmemStrideThreads : kGlobalThreads;  // ring stride
+  constexpr int STHREADS = SMEM ? kSmemStrideThreads : kGlobalStrideThreads;  // ring stride
   constexpr uint32_t EB = OUT64 ? 16 : 8;       // bytes per edge
   constexpr uint32_t G = kSectorBytes / EB;     // edges per sector (4 or 2)
   constexpr uint32_t R = kRingFactor * G;       // ring slots
@@ -539,6 +545,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           q.a[t].x = q.w[t] ^ 0x9E3779B9u;
           q.a[t].y = q.w[t] * 3u;
         }
+        continue;
+      }
+      if constexpr (REC) {  // one 16-byte record {A.x, A.y, B, TLO}: one L2 sector
+        const uint4 rr = __ldg(reinterpret_cast<const uint4*>(baseA + a4 * 4));
+        q.a[t] = make_uint2(rr.x, rr.y);
+        q.b[t] = rr.z;
         continue;
       }
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);

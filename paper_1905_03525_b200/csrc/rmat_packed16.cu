@@ -48,4 +48,29 @@ rmat_status launch_packed_p16(const rmat_table* t, const rmat::GenLaunch& g, boo
               : launch_packed_fb<16, false>(t, g, out64, prefix, count, st);
 }
 
+// 16-byte bucket records, L1/L2-resident (tables beyond shared memory)
+template <bool UND>
+rmat_status launch_packed_rec_u(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
+                                bool prefix, bool count, cudaStream_t st) {
+  constexpr bool F = false;
+  if (out64) {
+    if (prefix)
+      return count ? launch_packed_t<16, F, true, true, true, UND, F, F, F, F, true>(t, g, st)
+                   : launch_packed_t<16, F, true, true, false, UND, F, F, F, F, true>(t, g, st);
+    return count ? launch_packed_t<16, F, true, false, true, UND, F, F, F, F, true>(t, g, st)
+                 : launch_packed_t<16, F, true, false, false, UND, F, F, F, F, true>(t, g, st);
+  }
+  if (prefix)
+    return count ? launch_packed_t<16, F, false, true, true, UND, F, F, F, F, true>(t, g, st)
+                 : launch_packed_t<16, F, false, true, false, UND, F, F, F, F, true>(t, g, st);
+  return count ? launch_packed_t<16, F, false, false, true, UND, F, F, F, F, true>(t, g, st)
+               : launch_packed_t<16, F, false, false, false, UND, F, F, F, F, true>(t, g, st);
+}
+
+rmat_status launch_packed_rec(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
+                              bool prefix, bool count, cudaStream_t st) {
+  return (g.post & RMAT_POST_UNDIRECTED) ? launch_packed_rec_u<true>(t, g, out64, prefix, count, st)
+                                         : launch_packed_rec_u<false>(t, g, out64, prefix, count, st);
+}
+
 }  // namespace rmat_impl

@@ -313,3 +313,40 @@ def test_packed_scheme_g_tables(cuda, tag, k, block):
     assert launch_generate(dt, k, 21, DOMAIN_BLOCK, block, [(0, 64, 0, 0, 0)],
                            torch.empty((64, 2), dtype=edge_dtype(k), device=cuda)) == \
         N.KERNEL_PACKED_SMEM
+
+
+@pytest.mark.parametrize("tag,k,undirected", [("v65536", 26, False), ("v65536", 30, True),
+                                              ("f8", 26, False), ("f8", 33, False)])
+def test_bucket_records_match_separate_arrays(cuda, monkeypatch, tag, k, undirected):
+    """Tables beyond shared memory whose fragment values fit 16 bits get 16-byte
+    bucket records (csrc/rmat_device.cuh R[i]) for the L1/L2-resident kernel;
+    RMAT_DISABLE_REC=1 at table creation keeps the separate A / B arrays.  Both
+    must give the oracle's edges and per-stream sample counts."""
+    from paper_1905_03525_b200.device import DeviceTable
+
+    table = table_for(tag)
+    rec = DeviceTable(table, cuda)
+    monkeypatch.setenv("RMAT_DISABLE_REC", "1")
+    plain = DeviceTable(table, cuda)
+    monkeypatch.delenv("RMAT_DISABLE_REC")
+    assert rec.info.device_bytes - plain.info.device_bytes == 16 * rec.info.n  # records present
+    m, E = 40_000, 999  # E not a multiple of the sector: the PREFIX (unaligned) variants too
+    nstreams = (m + E - 1) // E
+    outs = []
+    for dt in (rec, plain):
+        out = torch.empty((m, 2), dtype=torch.uint32 if k <= 32 else torch.uint64, device=cuda)
+        per = torch.zeros(nstreams, dtype=torch.int64, device=cuda)
+        used = launch_generate(dt, k, 7, DOMAIN_BLOCK, E, [(0, m, 0, 0, 0)], out,
+                               samples_per_stream=per, kernel=N.KERNEL_PACKED_GLOBAL,
+                               post_flags=N.POST_UNDIRECTED if undirected else 0)
+        assert used == N.KERNEL_PACKED_GLOBAL
+        outs.append((host(out), per.cpu().numpy()))
+    assert (outs[0][0] == outs[1][0]).all() and (outs[0][1] == outs[1][1]).all()
+    ot = oracle_table(tag)
+    for s in (0, nstreams // 2, nstreams - 1):
+        cnt = min(E, m - s * E)
+        e, nf = oracle.fast_stream(ot, k, cnt, 7, s)
+        if undirected:
+            e = np.stack([e.max(axis=1), e.min(axis=1)], axis=1)
+        assert (outs[0][0][s * E: s * E + cnt] == e).all()
+        assert outs[0][1][s] == nf

@@ -1,4 +1,4 @@
-"""Time the L1/L2-resident bucket variant (packed_global): C5 S=2^16 and C3 forced."""
+"""Time the L1/L2-resident bucket variant (packed_global): C5 S=2^16, fixed l=8 and C3 forced."""
 import json
 import os
 import sys
@@ -6,7 +6,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_1905_03525_b200 import GenConfig, build_variable_table, validate  # noqa: E402
+from paper_1905_03525_b200 import (GenConfig, build_fixed_table, build_variable_table,  # noqa: E402
+                                   validate)
 from paper_1905_03525_b200 import _native as N  # noqa: E402
 from paper_1905_03525_b200.generator import generate_shard  # noqa: E402
 
@@ -29,6 +30,8 @@ p = validate(0.57, 0.19, 0.19, 0.05, 26)
 cfg = GenConfig(params=p, table=build_variable_table(p, 1 << 16), edge_count=1 << 30, seed=1,
                 block_size=1024)
 res["c5_s65536_auto"] = t(cfg, N.KERNEL_AUTO)
+cfg = GenConfig(params=p, table=build_fixed_table(p, 8), edge_count=1 << 30, seed=1, block_size=1024)
+res["c5_fixed8_auto"] = t(cfg, N.KERNEL_AUTO)
 p = validate(0.57, 0.19, 0.19, 0.05, 28)
 cfg = GenConfig(params=p, table=build_variable_table(p, 1 << 14), edge_count=1 << 30, seed=1,
                 block_size=1024)
