@@ -214,7 +214,7 @@ def _long_stream_max_blocks(dt) -> int:
         return LONG_STREAM_MAX_BLOCKS
     return torch.cuda.get_device_properties(dt.device).multi_processor_count
 LONG_STREAM_EDGES = 1 << 15
-SEGMENT_WORDS = 1 << 18         # CTA per segment (tools/seg_probe2.py)
+SEGMENT_WORDS = 1 << 18         # CTA per segment (tools/seg_length_probe.py)
 THREAD_SEGMENT_WORDS = 1 << 14  # thread per segment
 _M64 = (1 << 64) - 1
 
