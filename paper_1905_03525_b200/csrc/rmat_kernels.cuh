@@ -195,13 +195,11 @@ template <> struct AEntry<32> { using T = uint4; };
 #ifndef RMAT_SMEM_THREADS
 #define RMAT_SMEM_THREADS 512
 #endif
-#ifndef RMAT_RING_FACTOR
-#define RMAT_RING_FACTOR 2
-#endif
-constexpr uint32_t kSectorBytes = RMAT_FLUSH_BYTES;  // bytes per flush store (16 or 32)
-// Ring = kRingFactor sectors per thread: 2 -> sector checks once per G
-// samples; 1 -> a check after every stored edge (half the shared memory).
-constexpr uint32_t kRingFactor = RMAT_RING_FACTOR;
+// Ring = 2 sectors per thread: the sector check runs once per G samples (at
+// most G edges arrive between checks, so the open sector cannot be
+// overwritten before it leaves).  A one-sector ring would need a check after
+// every stored edge; that variant is not implemented.
+constexpr uint32_t kRingFactor = 2;
 constexpr uint32_t kRingBytes = kRingFactor * kSectorBytes;  // staging bytes per thread
 constexpr int kSmemThreads = RMAT_SMEM_THREADS;     // packed_smem CTA size
 #ifndef RMAT_CLEAN_ACC
