@@ -195,6 +195,7 @@ template <> struct AEntry<32> { using T = uint4; };
 #ifndef RMAT_SMEM_THREADS
 #define RMAT_SMEM_THREADS 512
 #endif
+constexpr uint32_t kSectorBytes = RMAT_FLUSH_BYTES;  // bytes per flush store (16 or 32)
 // Ring = 2 sectors per thread: the sector check runs once per G samples (at
 // most G edges arrive between checks, so the open sector cannot be
 // overwritten before it leaves).  A one-sector ring would need a check after
