@@ -48,6 +48,7 @@ rmat::PackedTab packed_view(const rmat_table* t, bool rec) {
   p.fastmod_m = t->fastmod_m;
   p.one = 1;
   p.zero = 0;
+  p.dfix = t->dmin == t->dmax ? t->dmin : 0;
   return p;
 }
 rmat::GenericTab generic_view(const rmat_table* t) {
@@ -373,6 +374,13 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
   if (a->kernel_used) *a->kernel_used = kernel;
 
   const uint64_t key = a->seed ^ a->domain;
+  // fixed-depth tables: units of GRP fragments on the fast path (uint32 edges,
+  // block streams; RMAT_DISABLE_GRP=1 keeps the per-sample kernels)
+#ifndef RMAT_GRP
+#define RMAT_GRP 1
+#endif
+  const int grp = (RMAT_GRP && t->fb == 16 && !out64 && !prefix &&
+                   std::getenv("RMAT_DISABLE_GRP") == nullptr) ? fixed_group(t, a->k) : 1;
   uint64_t stream_begin = 0;
   for (uint32_t s0 = 0; s0 < a->n_segments; s0 += rmat::kMaxSegsPerLaunch) {
     rmat::GenLaunch g;
@@ -411,12 +419,15 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
     rmat_status rs;
     switch (kernel) {
       case RMAT_KERNEL_PACKED_SMEM:
-        rs = sg            ? launch_sg(t, g, out64, prefix, count, st)
+        rs = (grp > 1 && !sg && !w64) ? launch_packed_grp(t, g, true, grp, count, st)
+             : sg            ? launch_sg(t, g, out64, prefix, count, st)
              : w64         ? launch_w64(t, g, prefix, count, st)
              : t->fb == 16 ? launch_packed_p16(t, g, true, out64, prefix, count, st)
                            : launch_packed_p32(t, g, true, out64, prefix, count, st);
         break;
       case RMAT_KERNEL_PACKED_GLOBAL:
+        // (no units on the record kernel: it is L1TEX-bound and they measured
+        // -4 % there, fixed l = 8; +11-13 % in shared memory, l = 4 / 6)
         rs = t->pR ? launch_packed_rec(t, g, out64, prefix, count, st)
              : t->fb == 16 ? launch_packed_p16(t, g, false, out64, prefix, count, st)
                            : launch_packed_p32(t, g, false, out64, prefix, count, st);

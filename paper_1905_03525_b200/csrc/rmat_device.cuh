@@ -79,6 +79,7 @@ struct PackedTab {
   uint32_t fb;        // 16 or 32
   uint32_t one;       // 1 (a launch parameter so the IMAD-based compare is not folded)
   uint32_t zero;      // 0 (ditto: keeps the Philox round keys in per-thread registers)
+  uint32_t dfix;      // fixed-depth tables: the depth of every fragment (GRP kernels), else 0
   uint64_t fastmod_m; // scheme G: ceil(2^64 / n), bucket = hi mod n (Lemire's exact fastmod)
 };
 

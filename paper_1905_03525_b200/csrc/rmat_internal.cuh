@@ -47,9 +47,9 @@ rmat::PackedTab packed_view(const rmat_table* t, bool rec = false);
 rmat::GenericTab generic_view(const rmat_table* t);
 
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
-          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false>
+          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1>
 inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32, REC>;
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32, REC, GRP>;
   const int sms = num_sms(t->device);
   int threads, blocks;
   size_t smem = 0;
@@ -85,6 +85,16 @@ rmat_status launch_packed_p16(const rmat_table* t, const rmat::GenLaunch& g, boo
                               bool prefix, bool count, cudaStream_t st);
 rmat_status launch_packed_p32(const rmat_table* t, const rmat::GenLaunch& g, bool smem, bool out64,
                               bool prefix, bool count, cudaStream_t st);
+// fixed-depth tables whose units of GRP fragments fit (rmat_packed16.cu): the
+// GRP to use for k (4, 2, or 1 = none)
+inline int fixed_group(const rmat_table* t, uint32_t k) {
+  if (t->dmin != t->dmax) return 1;
+  const uint32_t lim = std::min<uint32_t>(k, 31);
+  return 4 * t->dmin <= lim ? 4 : 2 * t->dmin <= lim ? 2 : 1;
+}
+// uint32 edges, no tile prefixes, fixed-depth table (GRP > 1)
+rmat_status launch_packed_grp(const rmat_table* t, const rmat::GenLaunch& g, bool smem, int grp,
+                              bool count, cudaStream_t st);
 // the L1/L2-resident kernel on 16-byte records (t->pR; rmat_packed16.cu)
 rmat_status launch_packed_rec(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
                               bool prefix, bool count, cudaStream_t st);

@@ -334,8 +334,14 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 // word of an edge is the funnel-shifted accumulator as is (all 32 bits are
 // edge bits, and any tile prefix lies above bit 32), no mask / prefix LOP3.
 // REC: 16-byte bucket records (rmat_table::pR) in the L1/L2-resident kernel.
+// GRP (fixed-depth tables, every fragment tab.dfix levels): the fast path
+// appends GRP consecutive fragments as one GRP * dfix-bit unit (host-checked
+// GRP * dfix <= min(k, 31): at most one edge boundary per unit), so the
+// append / cut / store work runs once per unit instead of once per sample.
+// Concatenation is associative, so the edges are the per-sample ones; the
+// careful path (stream ends, sample counts) stays per sample.
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF,
-          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false>
+          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
@@ -595,13 +601,27 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   };
   // Fragments of one call appended to the accumulators; stores into the ring
   // and completed sectors flushed.  CAREFUL caps stores at `left`.
+  // GRP units: fragment width P = 2^dfix, unit depth and its power of two
+  const uint32_t gP = 1u << tab.dfix, gD = GRP * tab.dfix, gPW = 1u << (GRP * tab.dfix);
   auto step = [&](Batch& cb, auto careful_tag, uint32_t& left) {
     constexpr bool CAREFUL = decltype(careful_tag)::value;
+    constexpr int UG = (GRP > 1 && !CAREFUL) ? GRP : 1;  // samples per unit
     if (COUNT) ebits = 0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int un = 0; un < 4 / UG; ++un) {
+      const int t = un * UG + UG - 1;  // the unit's last sample
       uint32_t r, c;
-      if constexpr (FB == 16) {
+      if constexpr (UG > 1) {
+        // GRP fragments of dfix bits each, concatenated: r = r0 * P^(GRP-1) + ...
+#pragma unroll
+        for (int s2 = 0; s2 < UG; ++s2) {
+          const int ts = un * UG + s2;
+          const uint32_t rs = dp2a_lo(cb.a[ts].x, cb.sel[ts]);
+          const uint32_t cs = dp2a_lo(cb.a[ts].y, cb.sel[ts]);
+          r = s2 ? mad_lo(r, gP, rs) : rs;
+          c = s2 ? mad_lo(c, gP, cs) : cs;
+        }
+      } else if constexpr (FB == 16) {
         r = IDPSEL ? dp2a_lo(cb.a[t].x, cb.sel[t]) : prmt(cb.a[t].x, cb.sel[t]);
         c = IDPSEL ? dp2a_lo(cb.a[t].y, cb.sel[t]) : prmt(cb.a[t].y, cb.sel[t]);
       } else {
@@ -610,8 +630,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         c = lt ? cb.a[t].z : cb.a[t].w;
       }
       // (IDP: bytes 2-3 of the selector are 0, so B's threshold bytes drop out)
-      const uint32_t d = IDPSEL ? dp4a_u(cb.b[t], cb.sel[t])
-                                : prmt(cb.b[t], cb.seld[t]);
+      const uint32_t d = UG > 1 ? gD
+                         : IDPSEL ? dp4a_u(cb.b[t], cb.sel[t])
+                                  : prmt(cb.b[t], cb.seld[t]);
       bool st;
       uint64_t u, v;
       if constexpr (W64) {
@@ -641,7 +662,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           vch = __funnelshift_l(cur_c, 0u, d);
         } else {
           // IMADs (FMA pipe) rather than shifts: the ALU pipe is the busier one.
-          const uint32_t pw = 1u << d;
+          const uint32_t pw = UG > 1 ? gPW : 1u << d;
           vr = mad_lo(cur_r, pw, r);
           // high halves: IMAD.HI (FMA pipe) or a funnel shift (ALU pipe),
           // cur >> (32 - d) (RMAT_HI_SHF: 1 = both sides, 2 = row side only)
@@ -722,7 +743,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       }
       if (COUNT) ebits |= (uint32_t)st << t;
       if ((uint32_t)t % G == G - 1) {
-        // At most G edges since the last check: the sector at gptr is
+        // At most G edges since the last check (at most one per unit): the sector at gptr is
         // complete when the next slot has left its ring half.
         const bool full = rp_half(roff) != half;
         if constexpr (PREFIX && (CAREFUL || !kHeadsCareful)) {

@@ -48,6 +48,26 @@ rmat_status launch_packed_p16(const rmat_table* t, const rmat::GenLaunch& g, boo
               : launch_packed_fb<16, false>(t, g, out64, prefix, count, st);
 }
 
+// Fixed-depth tables, units of GRP fragments (uint32 edges, no prefixes)
+template <int GRP, bool UND>
+rmat_status launch_packed_grp_u(const rmat_table* t, const rmat::GenLaunch& g, bool smem, bool count,
+                                cudaStream_t st) {
+  constexpr bool F = false;
+  if (!smem) return RMAT_ERR_UNSUPPORTED;  // shared-memory tables only
+  return count ? launch_packed_t<16, true, F, F, true, UND, F, F, F, F, F, GRP>(t, g, st)
+               : launch_packed_t<16, true, F, F, false, UND, F, F, F, F, F, GRP>(t, g, st);
+}
+
+rmat_status launch_packed_grp(const rmat_table* t, const rmat::GenLaunch& g, bool smem, int grp,
+                              bool count, cudaStream_t st) {
+  const bool und = g.post & RMAT_POST_UNDIRECTED;
+  if (grp == 4)
+    return und ? launch_packed_grp_u<4, true>(t, g, smem, count, st)
+               : launch_packed_grp_u<4, false>(t, g, smem, count, st);
+  return und ? launch_packed_grp_u<2, true>(t, g, smem, count, st)
+             : launch_packed_grp_u<2, false>(t, g, smem, count, st);
+}
+
 // 16-byte bucket records, L1/L2-resident (tables beyond shared memory)
 template <bool UND>
 rmat_status launch_packed_rec_u(const rmat_table* t, const rmat::GenLaunch& g, bool out64,

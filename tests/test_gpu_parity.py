@@ -350,3 +350,35 @@ def test_bucket_records_match_separate_arrays(cuda, monkeypatch, tag, k, undirec
             e = np.stack([e.max(axis=1), e.min(axis=1)], axis=1)
         assert (outs[0][0][s * E: s * E + cnt] == e).all()
         assert outs[0][1][s] == nf
+
+
+@pytest.mark.parametrize("tag,k", [("f1", 5), ("f4", 26), ("f4", 16), ("f5", 13), ("f6", 26),
+                                   ("f6", 12), ("f4", 4)])
+def test_fixed_depth_units_match_per_sample(cuda, monkeypatch, tag, k):
+    """Fixed-depth tables: the shared-memory fast path appends GRP fragments as
+    one unit (GRP * depth <= min(k, 31)); RMAT_DISABLE_GRP=1 keeps the
+    per-sample kernel.  Same edges, same per-stream sample counts, the oracle's."""
+    dt = device_table(table_for(tag), cuda)
+    m, E = 50_000, 1024
+    nstreams = (m + E - 1) // E
+    outs = []
+    for disable in (False, True):
+        if disable:
+            monkeypatch.setenv("RMAT_DISABLE_GRP", "1")
+        out = torch.empty((m, 2), dtype=torch.uint32, device=cuda)
+        tot = torch.zeros(1, dtype=torch.int64, device=cuda)
+        per = torch.zeros(nstreams, dtype=torch.int64, device=cuda)
+        used = launch_generate(dt, k, 11, DOMAIN_BLOCK, E, [(0, m, 0, 0, 0)], out,
+                               samples_total=tot, samples_per_stream=per,
+                               kernel=N.KERNEL_PACKED_SMEM)
+        assert used == N.KERNEL_PACKED_SMEM
+        outs.append((host(out), per.cpu().numpy(), int(tot.item())))
+    monkeypatch.delenv("RMAT_DISABLE_GRP")
+    assert (outs[0][0] == outs[1][0]).all()
+    assert (outs[0][1] == outs[1][1]).all() and outs[0][2] == outs[1][2]
+    ot = oracle_table(tag)
+    for s in (0, 1, nstreams // 2, nstreams - 1):
+        cnt = min(E, m - s * E)
+        e, nf = oracle.fast_stream(ot, k, cnt, 11, s)
+        assert (outs[0][0][s * E: s * E + cnt] == e).all()
+        assert outs[0][1][s] == nf
