@@ -47,15 +47,17 @@ rmat::PackedTab packed_view(const rmat_table* t, bool rec = false);
 rmat::GenericTab generic_view(const rmat_table* t);
 
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
-          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1>
+          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1,
+          bool BANK = false>
 inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
-  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32, REC, GRP>;
+  auto kern = rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32, REC, GRP, BANK>;
   const int sms = num_sms(t->device);
   int threads, blocks;
   size_t smem = 0;
   if (SMEM) {
     threads = rmat::kSmemThreads;
-    smem = t->packed_bytes + (size_t)rmat::kSmemStrideThreads * rmat::kRingBytes;
+    smem = (BANK ? (size_t)t->n * 256 : t->packed_bytes) +
+           (size_t)rmat::kSmemStrideThreads * rmat::kRingBytes;
     blocks = sms;
   } else {
     threads = rmat::kGlobalThreads;
@@ -95,6 +97,15 @@ inline int fixed_group(const rmat_table* t, uint32_t k) {
 // uint32 edges, no tile prefixes, fixed-depth table (GRP > 1)
 rmat_status launch_packed_grp(const rmat_table* t, const rmat::GenLaunch& g, bool smem, int grp,
                               bool count, cudaStream_t st);
+// small scheme-P fixed-depth tables (n <= 512): bank-spread copies in shared
+// memory (uint32 edges, no tile prefixes), fragments in units of grp (2 or 4)
+inline bool bank_spread_ok(const rmat_table* t) {
+  return t->fb == 16 && t->scheme_p && t->n <= 512 &&
+         t->n * 256 + (uint64_t)rmat::kSmemStrideThreads * rmat::kRingBytes <=
+             (uint64_t)max_smem_optin(t->device);
+}
+rmat_status launch_packed_bank(const rmat_table* t, const rmat::GenLaunch& g, int grp, bool count,
+                               cudaStream_t st);
 // the L1/L2-resident kernel on 16-byte records (t->pR; rmat_packed16.cu)
 rmat_status launch_packed_rec(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
                               bool prefix, bool count, cudaStream_t st);

@@ -341,11 +341,13 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 // Concatenation is associative, so the edges are the per-sample ones; the
 // careful path (stream ends, sample counts) stays per sample.
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF,
-          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1>
+          bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1,
+          bool BANK = false>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
   static_assert(!REC || (FB == 16 && !SMEM && !REF && !SG), "records: 16-bit fields, global kernel");
+  static_assert(!BANK || (FB == 16 && SMEM && !REF && !SG), "bank-spread copies: 16-bit fields, shared memory");
   constexpr int THREADS = SMEM ? kSmemThreads : kGlobalThreads;
   constexpr int STHREADS = SMEM ? kSmemStrideThreads : kGlobalStrideThreads;  // ring stride
   constexpr uint32_t EB = OUT64 ? 16 : 8;       // bytes per edge
@@ -359,7 +361,22 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   const uint8_t* baseA;
   const uint8_t* baseB;
   uint8_t* stage;
-  if (SMEM) {
+  if (SMEM && BANK) {
+    // Bank-spread copies of a small table (n <= 512): A entry i of copy c at
+    // (16 i + c) * 8, B entry i of copy c at (32 i + c) * 4, lane l reads copy
+    // l & 15 of A and copy l of B -- random gathers without bank conflicts.
+    const uint32_t n = tab.n;
+    uint2* dA = reinterpret_cast<uint2*>(smem);
+    uint32_t* dB = reinterpret_cast<uint32_t*>(smem + (size_t)n * 128);
+    const uint2* sA = reinterpret_cast<const uint2*>(tab.A);
+    for (uint32_t i = threadIdx.x; i < n * 16; i += THREADS) dA[i] = __ldg(sA + (i >> 4));
+    for (uint32_t i = threadIdx.x; i < n * 32; i += THREADS) dB[i] = __ldg(tab.B + (i >> 5));
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    baseA = smem + (lane & 15) * 8;
+    baseB = smem + (size_t)n * 128 + lane * 4;
+    stage = smem + (size_t)n * 256;
+  } else if (SMEM) {
     // Stage the bucket arrays: A first (16B aligned), then B.
     const uint32_t n = tab.n;
     const size_t abytes = (size_t)n * sizeof(AE);
@@ -556,6 +573,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         const uint4 rr = __ldg(reinterpret_cast<const uint4*>(baseA + a4 * 4));
         q.a[t] = make_uint2(rr.x, rr.y);
         q.b[t] = rr.z;
+        continue;
+      }
+      if constexpr (BANK) {  // this lane's copy: entry i at base + 128 i = base + 32 a4
+        q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + (a4 << 5));
+        q.a[t] = *reinterpret_cast<const AE*>(baseA + (a4 << 5));
         continue;
       }
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);

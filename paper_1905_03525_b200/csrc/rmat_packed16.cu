@@ -68,6 +68,27 @@ rmat_status launch_packed_grp(const rmat_table* t, const rmat::GenLaunch& g, boo
              : launch_packed_grp_u<2, false>(t, g, smem, count, st);
 }
 
+// Small fixed-depth tables as bank-spread copies, units of GRP fragments
+// (uint32 edges, no prefixes).  Per sample the copies measured +-0 (the
+// integer pipes bind together with L1); with the units, +15 % (l = 4).
+template <int GRP, bool UND>
+rmat_status launch_packed_bank_u(const rmat_table* t, const rmat::GenLaunch& g, bool count,
+                                 cudaStream_t st) {
+  constexpr bool F = false;
+  return count ? launch_packed_t<16, true, F, F, true, UND, F, F, F, F, F, GRP, true>(t, g, st)
+               : launch_packed_t<16, true, F, F, false, UND, F, F, F, F, F, GRP, true>(t, g, st);
+}
+
+rmat_status launch_packed_bank(const rmat_table* t, const rmat::GenLaunch& g, int grp, bool count,
+                               cudaStream_t st) {
+  const bool und = g.post & RMAT_POST_UNDIRECTED;
+  if (grp == 4)
+    return und ? launch_packed_bank_u<4, true>(t, g, count, st)
+               : launch_packed_bank_u<4, false>(t, g, count, st);
+  return und ? launch_packed_bank_u<2, true>(t, g, count, st)
+             : launch_packed_bank_u<2, false>(t, g, count, st);
+}
+
 // 16-byte bucket records, L1/L2-resident (tables beyond shared memory)
 template <bool UND>
 rmat_status launch_packed_rec_u(const rmat_table* t, const rmat::GenLaunch& g, bool out64,

@@ -382,3 +382,35 @@ def test_fixed_depth_units_match_per_sample(cuda, monkeypatch, tag, k):
         e, nf = oracle.fast_stream(ot, k, cnt, 11, s)
         assert (outs[0][0][s * E: s * E + cnt] == e).all()
         assert outs[0][1][s] == nf
+
+
+@pytest.mark.parametrize("tag,k,undirected", [("f4", 26, False), ("f4", 16, True), ("f1", 7, False),
+                                              ("f4", 9, False)])
+def test_bank_spread_copies_match_one_copy(cuda, monkeypatch, tag, k, undirected):
+    """Small fixed-depth tables (n <= 512) on fragment units read bank-spread
+    copies (lane l: copy l of B, l & 15 of A); RMAT_DISABLE_BANK=1 keeps one
+    copy.  Same edges and sample counts, the oracle's."""
+    dt = device_table(table_for(tag), cuda)
+    m, E = 30_000, 1024
+    nstreams = (m + E - 1) // E
+    outs = []
+    for disable in (False, True):
+        if disable:
+            monkeypatch.setenv("RMAT_DISABLE_BANK", "1")
+        out = torch.empty((m, 2), dtype=torch.uint32, device=cuda)
+        per = torch.zeros(nstreams, dtype=torch.int64, device=cuda)
+        used = launch_generate(dt, k, 3, DOMAIN_BLOCK, E, [(0, m, 0, 0, 0)], out,
+                               samples_per_stream=per, kernel=N.KERNEL_PACKED_SMEM,
+                               post_flags=N.POST_UNDIRECTED if undirected else 0)
+        assert used == N.KERNEL_PACKED_SMEM
+        outs.append((host(out), per.cpu().numpy()))
+    monkeypatch.delenv("RMAT_DISABLE_BANK")
+    assert (outs[0][0] == outs[1][0]).all() and (outs[0][1] == outs[1][1]).all()
+    ot = oracle_table(tag)
+    for s in (0, nstreams // 2, nstreams - 1):
+        cnt = min(E, m - s * E)
+        e, nf = oracle.fast_stream(ot, k, cnt, 3, s)
+        if undirected:
+            e = np.stack([e.max(axis=1), e.min(axis=1)], axis=1)
+        assert (outs[0][0][s * E: s * E + cnt] == e).all()
+        assert outs[0][1][s] == nf
