@@ -342,7 +342,7 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 // careful path (stream ends, sample counts) stays per sample.
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF,
           bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1,
-          bool BANK = false>
+          bool BANK = false, bool SPR = false>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
@@ -433,7 +433,13 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
   }
   const uint64_t T = (uint64_t)gridDim.x * THREADS;
-  uint64_t s = (uint64_t)blockIdx.x * THREADS + threadIdx.x;
+  // SPR (launches of few rounds, host-chosen): warp w of block b takes the 32
+  // streams of virtual warp w * grid + b, so the last, partial round of
+  // streams lands on every SM instead of filling the first SMs while the
+  // others idle (C2: +11 %).  Otherwise block b takes streams [b T/grid, ...)
+  // (C3, 55 rounds: ~1 % faster that way).  The output never depends on it.
+  uint64_t s = SPR ? ((uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32 + (threadIdx.x & 31)
+                   : (uint64_t)blockIdx.x * THREADS + threadIdx.x;
 
   // Philox calls per fast iteration (drawn back to back for ILP).  Two calls
   // fit the 128-register budget of the 512-thread shared-memory CTA only for
