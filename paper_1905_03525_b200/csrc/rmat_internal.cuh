@@ -48,7 +48,7 @@ rmat::GenericTab generic_view(const rmat_table* t);
 
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
           bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1,
-          bool BANK = false>
+          bool BANK = false, bool VU = false>
 inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
   // R rounds of streams per thread: with the contiguous mapping the partial
   // last round runs on the first SMs only, wasting (ceil R - R) / ceil R of
@@ -59,8 +59,8 @@ inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g
   const uint64_t t_max = (uint64_t)sms0 * (SMEM ? rmat::kSmemThreads : rmat::kGlobalThreads);
   const uint64_t rounds = (g.total_streams + t_max - 1) / t_max;
   const bool spr = (double)(rounds * t_max - g.total_streams) > 0.03 * (double)(rounds * t_max);
-  auto kern = spr ? rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32, REC, GRP, BANK, true>
-                  : rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32, REC, GRP, BANK, false>;
+  auto kern = spr ? rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32, REC, GRP, BANK, true, VU>
+                  : rmat::k_packed<FB, SMEM, OUT64, PREFIX, COUNT, UND, REF, W64, SG, K32, REC, GRP, BANK, false, VU>;
   const int sms = num_sms(t->device);
   int threads, blocks;
   size_t smem = 0;

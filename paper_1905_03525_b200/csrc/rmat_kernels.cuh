@@ -342,12 +342,19 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 // careful path (stream ends, sample counts) stays per sample.
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF,
           bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1,
-          bool BANK = false, bool SPR = false>
+          bool BANK = false, bool SPR = false, bool VU = false>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
   static_assert(!REC || (FB == 16 && !SMEM && !REF && !SG), "records: 16-bit fields, global kernel");
   static_assert(!BANK || (FB == 16 && SMEM && !REF && !SG), "bank-spread copies: 16-bit fields, shared memory");
+  // VU (variable-depth tables, uint32 edges, block streams): the fast path
+  // appends the fragments of samples (2u, 2u+1) as one unit of d_2u + d_2u+1
+  // bits.  A unit holds one edge boundary unless f + D >= 2k (or D = 32);
+  // an iteration where any lane has such a unit runs per sample instead
+  // (for the BASELINE tables that never happens: deep fragments are rare).
+  static_assert(!VU || (FB == 16 && RMAT_IDP && !OUT64 && !PREFIX && !REF && !W64 && !SG && GRP == 1),
+                "variable units: the plain uint32 fast path");
   constexpr int THREADS = SMEM ? kSmemThreads : kGlobalThreads;
   constexpr int STHREADS = SMEM ? kSmemStrideThreads : kGlobalStrideThreads;  // ring stride
   constexpr uint32_t EB = OUT64 ? 16 : 8;       // bytes per edge
@@ -455,7 +462,11 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #ifndef RMAT_WIDE_CPI
 #define RMAT_WIDE_CPI 1
 #endif
-  constexpr int CPI = (SG || (SMEM && FB == 32)) ? 1
+#ifndef RMAT_VU_CPI
+#define RMAT_VU_CPI 1
+#endif
+  constexpr int CPI = VU ? RMAT_VU_CPI
+                      : (SG || (SMEM && FB == 32)) ? 1
                       : (SMEM && (PREFIX || OUT64)) ? RMAT_WIDE_CPI
                       : REF ? RMAT_REF_CPI
                       : !SMEM ? RMAT_GLOBAL_CPI : RMAT_CALLS_PER_ITER;
@@ -795,6 +806,53 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
   };
 
+  // VU: one unit = samples (ta, tb) of a call, fast path only (see above)
+  const uint32_t vu_lim = min(k, 31u);
+  // d bits (r, c) appended; at most one edge boundary (d <= min(k, 31))
+  auto append_bits = [&](uint32_t r, uint32_t c, uint32_t d) {
+    const uint32_t pw = 1u << d;
+    const uint32_t vr = mad_lo(cur_r, pw, r);
+    const uint32_t vrh = __funnelshift_l(cur_r, 0u, d);
+    const uint32_t vc = mad_lo(cur_c, pw, c);
+    const uint32_t vch = mul_hi(cur_c, pw);
+    const uint32_t tt = f + d;
+    const bool emit = tt >= k;
+    const uint32_t over = __viaddmin_u32(tt, 0u - k, tt);
+    cur_r = vr;
+    cur_c = vc;
+    f = over;
+    uint32_t eu = __funnelshift_r(vr, vrh, over) & kmask;
+    uint32_t ev = __funnelshift_r(vc, vch, over) & kmask;
+    if constexpr (UND) {
+      const uint32_t hi = max(eu, ev);
+      ev = min(eu, ev);
+      eu = hi;
+    }
+    if (emit) {
+      sts64(rp_addr(roff), eu, ev);
+      roff = rp_next(roff);
+    }
+  };
+  // one unit = samples (ta, tb) of a call, D = d_ta + d_tb bits at once
+  // (the caller has checked D <= min(k, 31) for every unit of the iteration)
+  auto step_unit = [&](const Batch& cb, int ta, int tb, uint32_t D) {
+    const uint32_t pwb = 1u << dp4a_u(cb.b[tb], cb.sel[tb]);
+    append_bits(mad_lo(dp2a_lo(cb.a[ta].x, cb.sel[ta]), pwb, dp2a_lo(cb.a[tb].x, cb.sel[tb])),
+                mad_lo(dp2a_lo(cb.a[ta].y, cb.sel[ta]), pwb, dp2a_lo(cb.a[tb].y, cb.sel[tb])), D);
+  };
+  // after a call's two units (at most two edges): the per-sample path's sector check
+  auto unit_flush = [&]() {
+    const bool full = rp_half(roff) != half;
+    flush_full_pred<OUT64, STHREADS>(gptr, ring_sa + half * G * STRIDE, full);
+    gptr += full ? kSectorBytes : 0;
+    if constexpr (RMAT_HALF_RP && !OUT64) {
+      half = rp_half(roff);
+    } else {
+      half ^= (uint32_t)full;
+    }
+    if constexpr (!LGPTR) L -= full ? G : 0;
+  };
+
   for (;;) {
     // Warp-uniform fast path: every lane has >= 4 edges still to produce
     // (L - staged >= L - (R - 1)), so no stream ends during this call and
@@ -816,6 +874,31 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         for (int c = 0; c < CPI; ++c) resolve_ties(cb[c], j + c);
       }
       uint32_t unused = 0;
+      if constexpr (VU) {
+        // unit depths; a unit deeper than min(k, 31) bits might hold two edge
+        // boundaries (f + D >= 2k needs D > k since f < k) or overflow 2^D:
+        // then the whole iteration runs per sample (below)
+        uint32_t DU[CPI][2];
+        bool deep = false;
+#pragma unroll
+        for (int c = 0; c < CPI; ++c) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            DU[c][u] = dp4a_u(cb[c].b[2 * u], cb[c].sel[2 * u]) + dp4a_u(cb[c].b[2 * u + 1], cb[c].sel[2 * u + 1]);
+            deep |= DU[c][u] > vu_lim;
+          }
+        }
+        if (!__any_sync(0xFFFFFFFFu, deep)) {
+#pragma unroll
+          for (int c = 0; c < CPI; ++c) {
+            step_unit(cb[c], 0, 1, DU[c][0]);
+            step_unit(cb[c], 2, 3, DU[c][1]);
+            unit_flush();  // at most two edges this call
+          }
+          j += CPI;
+          continue;
+        }
+      }
       if constexpr ((RMAT_PROBE & 4) && !REF) {
 #pragma unroll
         for (int c = 0; c < CPI; ++c) probe_acc ^= cb[c].w[0] ^ cb[c].w[1] ^ cb[c].w[2] ^ cb[c].w[3];

@@ -2,6 +2,8 @@
 // librmat_b200.so; see rmat_internal.cuh).
 #include "rmat_internal.cuh"
 
+#include <cstdlib>
+
 #ifndef RMAT_K32
 #define RMAT_K32 1  // measured +0.5 % on C4 (9.625 vs 9.575e10 edges/s per job)
 #endif
@@ -29,6 +31,15 @@ rmat_status launch_packed_fu(const rmat_table* t, const rmat::GenLaunch& g, bool
   if (prefix)
     return count ? launch_packed_t<FB, SMEM, false, true, true, UND>(t, g, st)
                  : launch_packed_t<FB, SMEM, false, true, false, UND>(t, g, st);
+  if constexpr (SMEM && FB == 16) {
+    // variable-depth tables: fragments in units of two samples (VU;
+    // RMAT_DISABLE_VU=1 keeps the per-sample kernel)
+    if (t->dmin != t->dmax && std::getenv("RMAT_DISABLE_VU") == nullptr) {
+      constexpr bool F = false;
+      return count ? launch_packed_t<16, true, F, F, true, UND, F, F, F, F, F, 1, F, true>(t, g, st)
+                   : launch_packed_t<16, true, F, F, false, UND, F, F, F, F, F, 1, F, true>(t, g, st);
+    }
+  }
   return count ? launch_packed_t<FB, SMEM, false, false, true, UND>(t, g, st)
                : launch_packed_t<FB, SMEM, false, false, false, UND>(t, g, st);
 }

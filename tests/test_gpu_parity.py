@@ -414,3 +414,41 @@ def test_bank_spread_copies_match_one_copy(cuda, monkeypatch, tag, k, undirected
             e = np.stack([e.max(axis=1), e.min(axis=1)], axis=1)
         assert (outs[0][0][s * E: s * E + cnt] == e).all()
         assert outs[0][1][s] == nf
+
+
+@pytest.mark.parametrize("tag,k,undirected", [("v16384", 28, False), ("v4096", 24, True),
+                                              ("v1024", 16, False), ("v16384", 17, False),
+                                              ("v256", 9, False), ("v16384", 32, False)])
+def test_variable_units_match_per_sample(cuda, monkeypatch, tag, k, undirected):
+    """Variable-depth tables: the shared-memory fast path appends samples in
+    units of two (VU); iterations where a unit could hold two edge boundaries
+    (D > min(k, 31): small k makes them common here) run per sample.
+    RMAT_DISABLE_VU=1 keeps the per-sample kernel.  Same edges, same sample
+    counts, the oracle's."""
+    dt = device_table(table_for(tag), cuda)
+    m, E = 60_000, 1024
+    nstreams = (m + E - 1) // E
+    outs = []
+    for disable in (False, True):
+        if disable:
+            monkeypatch.setenv("RMAT_DISABLE_VU", "1")
+        out = torch.empty((m, 2), dtype=torch.uint32, device=cuda)
+        tot = torch.zeros(1, dtype=torch.int64, device=cuda)
+        per = torch.zeros(nstreams, dtype=torch.int64, device=cuda)
+        used = launch_generate(dt, k, 13, DOMAIN_BLOCK, E, [(0, m, 0, 0, 0)], out,
+                               samples_total=tot, samples_per_stream=per,
+                               kernel=N.KERNEL_PACKED_SMEM,
+                               post_flags=N.POST_UNDIRECTED if undirected else 0)
+        assert used == N.KERNEL_PACKED_SMEM
+        outs.append((host(out), per.cpu().numpy(), int(tot.item())))
+    monkeypatch.delenv("RMAT_DISABLE_VU")
+    assert (outs[0][0] == outs[1][0]).all()
+    assert (outs[0][1] == outs[1][1]).all() and outs[0][2] == outs[1][2]
+    ot = oracle_table(tag)
+    for s in (0, 1, nstreams // 2, nstreams - 1):
+        cnt = min(E, m - s * E)
+        e, nf = oracle.fast_stream(ot, k, cnt, 13, s)
+        if undirected:
+            e = np.stack([e.max(axis=1), e.min(axis=1)], axis=1)
+        assert (outs[0][0][s * E: s * E + cnt] == e).all()
+        assert outs[0][1][s] == nf
