@@ -353,8 +353,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // bits.  A unit holds one edge boundary unless f + D >= 2k (or D = 32);
   // an iteration where any lane has such a unit runs per sample instead
   // (for the BASELINE tables that never happens: deep fragments are rare).
-  static_assert(!VU || (FB == 16 && RMAT_IDP && !OUT64 && !PREFIX && !REF && !W64 && !SG && GRP == 1),
-                "variable units: the plain uint32 fast path");
+  static_assert(!VU || (FB == 16 && RMAT_IDP && SMEM && !REF && !W64 && !SG && GRP == 1 && !BANK),
+                "variable units: the shared-memory scheme-P fast path");
   constexpr int THREADS = SMEM ? kSmemThreads : kGlobalThreads;
   constexpr int STHREADS = SMEM ? kSmemStrideThreads : kGlobalStrideThreads;  // ring stride
   constexpr uint32_t EB = OUT64 ? 16 : 8;       // bytes per edge
@@ -808,29 +808,60 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 
   // VU: one unit = samples (ta, tb) of a call, fast path only (see above)
   const uint32_t vu_lim = min(k, 31u);
-  // d bits (r, c) appended; at most one edge boundary (d <= min(k, 31))
+  // d bits (r, c) appended; at most one edge boundary (d <= min(k, 31)):
+  // the per-sample path's append / cut / store for one unit (same forms)
   auto append_bits = [&](uint32_t r, uint32_t c, uint32_t d) {
     const uint32_t pw = 1u << d;
     const uint32_t vr = mad_lo(cur_r, pw, r);
-    const uint32_t vrh = __funnelshift_l(cur_r, 0u, d);
+    const uint32_t vrh = (RMAT_HI_SHF && !OUT64) ? __funnelshift_l(cur_r, 0u, d) : mul_hi(cur_r, pw);
     const uint32_t vc = mad_lo(cur_c, pw, c);
-    const uint32_t vch = mul_hi(cur_c, pw);
+    const uint32_t vch = (RMAT_HI_SHF == 1 && !OUT64) ? __funnelshift_l(cur_c, 0u, d) : mul_hi(cur_c, pw);
     const uint32_t tt = f + d;
     const bool emit = tt >= k;
     const uint32_t over = __viaddmin_u32(tt, 0u - k, tt);
     cur_r = vr;
     cur_c = vc;
     f = over;
-    uint32_t eu = __funnelshift_r(vr, vrh, over) & kmask;
-    uint32_t ev = __funnelshift_r(vc, vch, over) & kmask;
-    if constexpr (UND) {
-      const uint32_t hi = max(eu, ev);
-      ev = min(eu, ev);
-      eu = hi;
-    }
-    if (emit) {
-      sts64(rp_addr(roff), eu, ev);
-      roff = rp_next(roff);
+    if constexpr (OUT64) {
+      const uint32_t rlo = PREFIX ? (uint32_t)p.rpre : 0u, rhi = PREFIX ? (uint32_t)(p.rpre >> 32) : 0u;
+      const uint32_t clo = PREFIX ? (uint32_t)p.cpre : 0u, chi = PREFIX ? (uint32_t)(p.cpre >> 32) : 0u;
+      uint64_t u, v;
+      if constexpr (K32) {
+        u = ((uint64_t)and_or(vrh >> over, hmask, rhi) << 32) | __funnelshift_r(vr, vrh, over);
+        v = ((uint64_t)and_or(vch >> over, hmask, chi) << 32) | __funnelshift_r(vc, vch, over);
+      } else {
+        u = ((uint64_t)and_or(vrh >> over, hmask, rhi) << 32) |
+            and_or(__funnelshift_r(vr, vrh, over), kmask, rlo);
+        v = ((uint64_t)and_or(vch >> over, hmask, chi) << 32) |
+            and_or(__funnelshift_r(vc, vch, over), kmask, clo);
+      }
+      if constexpr (UND) {
+        const uint64_t hi = u > v ? u : v;
+        v = u > v ? v : u;
+        u = hi;
+      }
+      if (emit) {
+        sts128(rp_addr(roff), u, v);
+        roff = rp_next(roff);
+      }
+    } else {
+      uint32_t eu, ev;
+      if constexpr (PREFIX) {
+        eu = and_or(__funnelshift_r(vr, vrh, over), kmask, (uint32_t)p.rpre);
+        ev = and_or(__funnelshift_r(vc, vch, over), kmask, (uint32_t)p.cpre);
+      } else {
+        eu = __funnelshift_r(vr, vrh, over) & kmask;
+        ev = __funnelshift_r(vc, vch, over) & kmask;
+      }
+      if constexpr (UND) {
+        const uint32_t hi = max(eu, ev);
+        ev = min(eu, ev);
+        eu = hi;
+      }
+      if (emit) {
+        sts64(rp_addr(roff), eu, ev);
+        roff = rp_next(roff);
+      }
     }
   };
   // one unit = samples (ta, tb) of a call, D = d_ta + d_tb bits at once

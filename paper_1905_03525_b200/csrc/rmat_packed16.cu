@@ -10,46 +10,45 @@
 
 namespace rmat_impl {
 
-template <int FB, bool SMEM, bool UND>
+// VU: variable-depth tables in shared memory append samples in pairs (the
+// kernels' VU note); the per-sample kernels otherwise
+template <int FB, bool SMEM, bool UND, bool VU>
 rmat_status launch_packed_fu(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
                              bool count, cudaStream_t st) {
+  constexpr bool F = false;
   if (out64) {
     // 32 <= k (<= 33 here): whole low words, no low-word mask / prefix (K32)
     if (SMEM && FB == 16 && g.k >= 32 && RMAT_K32) {
       if (prefix)
-        return count ? launch_packed_t<FB, SMEM, true, true, true, UND, false, false, false, true>(t, g, st)
-                     : launch_packed_t<FB, SMEM, true, true, false, UND, false, false, false, true>(t, g, st);
-      return count ? launch_packed_t<FB, SMEM, true, false, true, UND, false, false, false, true>(t, g, st)
-                   : launch_packed_t<FB, SMEM, true, false, false, UND, false, false, false, true>(t, g, st);
+        return count ? launch_packed_t<FB, SMEM, true, true, true, UND, F, F, F, true, F, 1, F, VU>(t, g, st)
+                     : launch_packed_t<FB, SMEM, true, true, false, UND, F, F, F, true, F, 1, F, VU>(t, g, st);
+      return count ? launch_packed_t<FB, SMEM, true, false, true, UND, F, F, F, true, F, 1, F, VU>(t, g, st)
+                   : launch_packed_t<FB, SMEM, true, false, false, UND, F, F, F, true, F, 1, F, VU>(t, g, st);
     }
     if (prefix)
-      return count ? launch_packed_t<FB, SMEM, true, true, true, UND>(t, g, st)
-                   : launch_packed_t<FB, SMEM, true, true, false, UND>(t, g, st);
-    return count ? launch_packed_t<FB, SMEM, true, false, true, UND>(t, g, st)
-                 : launch_packed_t<FB, SMEM, true, false, false, UND>(t, g, st);
+      return count ? launch_packed_t<FB, SMEM, true, true, true, UND, F, F, F, F, F, 1, F, VU>(t, g, st)
+                   : launch_packed_t<FB, SMEM, true, true, false, UND, F, F, F, F, F, 1, F, VU>(t, g, st);
+    return count ? launch_packed_t<FB, SMEM, true, false, true, UND, F, F, F, F, F, 1, F, VU>(t, g, st)
+                 : launch_packed_t<FB, SMEM, true, false, false, UND, F, F, F, F, F, 1, F, VU>(t, g, st);
   }
   if (prefix)
-    return count ? launch_packed_t<FB, SMEM, false, true, true, UND>(t, g, st)
-                 : launch_packed_t<FB, SMEM, false, true, false, UND>(t, g, st);
-  if constexpr (SMEM && FB == 16) {
-    // variable-depth tables: fragments in units of two samples (VU;
-    // RMAT_DISABLE_VU=1 keeps the per-sample kernel)
-    if (t->dmin != t->dmax && std::getenv("RMAT_DISABLE_VU") == nullptr) {
-      constexpr bool F = false;
-      return count ? launch_packed_t<16, true, F, F, true, UND, F, F, F, F, F, 1, F, true>(t, g, st)
-                   : launch_packed_t<16, true, F, F, false, UND, F, F, F, F, F, 1, F, true>(t, g, st);
-    }
-  }
-  return count ? launch_packed_t<FB, SMEM, false, false, true, UND>(t, g, st)
-               : launch_packed_t<FB, SMEM, false, false, false, UND>(t, g, st);
+    return count ? launch_packed_t<FB, SMEM, false, true, true, UND, F, F, F, F, F, 1, F, VU>(t, g, st)
+                 : launch_packed_t<FB, SMEM, false, true, false, UND, F, F, F, F, F, 1, F, VU>(t, g, st);
+  return count ? launch_packed_t<FB, SMEM, false, false, true, UND, F, F, F, F, F, 1, F, VU>(t, g, st)
+               : launch_packed_t<FB, SMEM, false, false, false, UND, F, F, F, F, F, 1, F, VU>(t, g, st);
 }
 
 template <int FB, bool SMEM>
 rmat_status launch_packed_fb(const rmat_table* t, const rmat::GenLaunch& g, bool out64, bool prefix,
                              bool count, cudaStream_t st) {
+  // variable-depth tables in shared memory: units of two samples (RMAT_DISABLE_VU=1: per sample)
+  if (SMEM && t->dmin != t->dmax && std::getenv("RMAT_DISABLE_VU") == nullptr)
+    return (g.post & RMAT_POST_UNDIRECTED)
+               ? launch_packed_fu<FB, SMEM, true, SMEM>(t, g, out64, prefix, count, st)
+               : launch_packed_fu<FB, SMEM, false, SMEM>(t, g, out64, prefix, count, st);
   return (g.post & RMAT_POST_UNDIRECTED)
-             ? launch_packed_fu<FB, SMEM, true>(t, g, out64, prefix, count, st)
-             : launch_packed_fu<FB, SMEM, false>(t, g, out64, prefix, count, st);
+             ? launch_packed_fu<FB, SMEM, true, false>(t, g, out64, prefix, count, st)
+             : launch_packed_fu<FB, SMEM, false, false>(t, g, out64, prefix, count, st);
 }
 
 
