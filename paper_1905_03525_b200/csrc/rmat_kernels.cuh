@@ -353,7 +353,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // bits.  A unit holds one edge boundary unless f + D >= 2k (or D = 32);
   // an iteration where any lane has such a unit runs per sample instead
   // (for the BASELINE tables that never happens: deep fragments are rare).
-  static_assert(!VU || (FB == 16 && RMAT_IDP && SMEM && !REF && !W64 && !SG && GRP == 1 && !BANK),
+  static_assert(!VU || (FB == 16 && RMAT_IDP && SMEM && !W64 && !SG && GRP == 1 && !BANK),
                 "variable units: the shared-memory scheme-P fast path");
   constexpr int THREADS = SMEM ? kSmemThreads : kGlobalThreads;
   constexpr int STHREADS = SMEM ? kSmemStrideThreads : kGlobalStrideThreads;  // ring stride
@@ -463,9 +463,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #define RMAT_WIDE_CPI 1
 #endif
 #ifndef RMAT_VU_CPI
-#define RMAT_VU_CPI 1
+#define RMAT_VU_CPI 1  // fast mode: two calls per iteration spill at 128 registers (measured)
 #endif
-  constexpr int CPI = VU ? RMAT_VU_CPI
+#ifndef RMAT_VU_REF_CPI
+#define RMAT_VU_REF_CPI 2  // reference blocks: +3 % over per sample (one call: -7 %)
+#endif
+  constexpr int CPI = VU ? (REF ? RMAT_VU_REF_CPI : RMAT_VU_CPI)
                       : (SG || (SMEM && FB == 32)) ? 1
                       : (SMEM && (PREFIX || OUT64)) ? RMAT_WIDE_CPI
                       : REF ? RMAT_REF_CPI
@@ -811,11 +814,19 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // d bits (r, c) appended; at most one edge boundary (d <= min(k, 31)):
   // the per-sample path's append / cut / store for one unit (same forms)
   auto append_bits = [&](uint32_t r, uint32_t c, uint32_t d) {
-    const uint32_t pw = 1u << d;
-    const uint32_t vr = mad_lo(cur_r, pw, r);
-    const uint32_t vrh = (RMAT_HI_SHF && !OUT64) ? __funnelshift_l(cur_r, 0u, d) : mul_hi(cur_r, pw);
-    const uint32_t vc = mad_lo(cur_c, pw, c);
-    const uint32_t vch = (RMAT_HI_SHF == 1 && !OUT64) ? __funnelshift_l(cur_c, 0u, d) : mul_hi(cur_c, pw);
+    uint32_t vr, vrh, vc, vch;
+    if constexpr (REF && RMAT_REF_SHIFT_APPEND) {  // (numpy's Philox4x64 keeps the FMA pipe busy)
+      vr = (cur_r << d) | r;
+      vrh = __funnelshift_l(cur_r, 0u, d);
+      vc = (cur_c << d) | c;
+      vch = __funnelshift_l(cur_c, 0u, d);
+    } else {
+      const uint32_t pw = 1u << d;
+      vr = mad_lo(cur_r, pw, r);
+      vrh = (RMAT_HI_SHF && !OUT64) ? __funnelshift_l(cur_r, 0u, d) : mul_hi(cur_r, pw);
+      vc = mad_lo(cur_c, pw, c);
+      vch = (RMAT_HI_SHF == 1 && !OUT64) ? __funnelshift_l(cur_c, 0u, d) : mul_hi(cur_c, pw);
+    }
     const uint32_t tt = f + d;
     const bool emit = tt >= k;
     const uint32_t over = __viaddmin_u32(tt, 0u - k, tt);
@@ -867,9 +878,15 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // one unit = samples (ta, tb) of a call, D = d_ta + d_tb bits at once
   // (the caller has checked D <= min(k, 31) for every unit of the iteration)
   auto step_unit = [&](const Batch& cb, int ta, int tb, uint32_t D) {
-    const uint32_t pwb = 1u << dp4a_u(cb.b[tb], cb.sel[tb]);
-    append_bits(mad_lo(dp2a_lo(cb.a[ta].x, cb.sel[ta]), pwb, dp2a_lo(cb.a[tb].x, cb.sel[tb])),
-                mad_lo(dp2a_lo(cb.a[ta].y, cb.sel[ta]), pwb, dp2a_lo(cb.a[tb].y, cb.sel[tb])), D);
+    const uint32_t db = dp4a_u(cb.b[tb], cb.sel[tb]);
+    const uint32_t ra = dp2a_lo(cb.a[ta].x, cb.sel[ta]), rb = dp2a_lo(cb.a[tb].x, cb.sel[tb]);
+    const uint32_t ca = dp2a_lo(cb.a[ta].y, cb.sel[ta]), cb_ = dp2a_lo(cb.a[tb].y, cb.sel[tb]);
+    if constexpr (REF && RMAT_REF_SHIFT_APPEND) {
+      append_bits((ra << db) | rb, (ca << db) | cb_, D);
+    } else {
+      const uint32_t pwb = 1u << db;
+      append_bits(mad_lo(ra, pwb, rb), mad_lo(ca, pwb, cb_), D);
+    }
   };
   // after a call's two units (at most two edges): the per-sample path's sector check
   auto unit_flush = [&]() {
