@@ -925,7 +925,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       if constexpr (VU) {
         // unit depths; a unit deeper than min(k, 31) bits might hold two edge
         // boundaries (f + D >= 2k needs D > k since f < k) or overflow 2^D:
-        // then the whole iteration runs per sample (below)
+        // then the whole iteration runs per sample (below; with two calls per
+        // iteration this kernel spills at 128 registers, per-call votes too)
         uint32_t DU[CPI][2];
         bool deep = false;
 #pragma unroll
