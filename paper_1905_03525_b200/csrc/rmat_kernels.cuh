@@ -424,9 +424,17 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #ifndef RMAT_RK_REGS
 #define RMAT_RK_REGS 1
 #endif
+#ifndef RMAT_VU_CPI
+// fast mode, uint32 block streams: two calls per iteration with the round
+// keys read from the constant bank (VU_RKC; with the keys in registers this
+// kernel spills 64 B at 128 registers): C3 +1.9 % over one call (measured)
+#define RMAT_VU_CPI 2
+#endif
   uint32_t rk[20];
+  // VU_RKC: the two-call VU fast path reads the round keys from the constant bank
+  constexpr bool VU_RKC = VU && !REF && !PREFIX && !OUT64 && RMAT_VU_CPI == 2;
   if (REF) {
-  } else if (RMAT_RK_REGS == 0) {
+  } else if (RMAT_RK_REGS == 0 || VU_RKC) {
 #pragma unroll
     for (int i = 0; i < 20; ++i) rk[i] = g.rk[i];
   } else {
@@ -462,13 +470,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #ifndef RMAT_WIDE_CPI
 #define RMAT_WIDE_CPI 1
 #endif
-#ifndef RMAT_VU_CPI
-#define RMAT_VU_CPI 1  // fast mode: two calls per iteration spill at 128 registers (measured)
-#endif
 #ifndef RMAT_VU_REF_CPI
 #define RMAT_VU_REF_CPI 2  // reference blocks: +3 % over per sample (one call: -7 %)
 #endif
-  constexpr int CPI = VU ? (REF ? RMAT_VU_REF_CPI : RMAT_VU_CPI)
+  constexpr int CPI = VU ? (REF ? RMAT_VU_REF_CPI : (PREFIX || OUT64) ? RMAT_WIDE_CPI : RMAT_VU_CPI)
                       : (SG || (SMEM && FB == 32)) ? 1
                       : (SMEM && (PREFIX || OUT64)) ? RMAT_WIDE_CPI
                       : REF ? RMAT_REF_CPI
