@@ -353,7 +353,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // bits.  A unit holds one edge boundary unless f + D >= 2k (or D = 32);
   // an iteration where any lane has such a unit runs per sample instead
   // (for the BASELINE tables that never happens: deep fragments are rare).
-  static_assert(!VU || (FB == 16 && RMAT_IDP && SMEM && !W64 && !SG && GRP == 1 && !BANK),
+  static_assert(!VU || (FB == 16 && RMAT_IDP && SMEM && !W64 && !SG && GRP == 1),
                 "variable units: the shared-memory scheme-P fast path");
   constexpr int THREADS = SMEM ? kSmemThreads : kGlobalThreads;
   constexpr int STHREADS = SMEM ? kSmemStrideThreads : kGlobalStrideThreads;  // ring stride

@@ -34,6 +34,12 @@ rmat_status launch_packed_fu(const rmat_table* t, const rmat::GenLaunch& g, bool
   if (prefix)
     return count ? launch_packed_t<FB, SMEM, false, true, true, UND, F, F, F, F, F, 1, F, VU>(t, g, st)
                  : launch_packed_t<FB, SMEM, false, true, false, UND, F, F, F, F, F, 1, F, VU>(t, g, st);
+  // small variable-depth tables on units: bank-spread copies (RMAT_DISABLE_BANK=1: one copy)
+  if constexpr (SMEM && VU) {
+    if (bank_spread_ok(t) && std::getenv("RMAT_DISABLE_BANK") == nullptr)
+      return count ? launch_packed_t<16, true, false, false, true, UND, F, F, F, F, F, 1, true, true>(t, g, st)
+                   : launch_packed_t<16, true, false, false, false, UND, F, F, F, F, F, 1, true, true>(t, g, st);
+  }
   return count ? launch_packed_t<FB, SMEM, false, false, true, UND, F, F, F, F, F, 1, F, VU>(t, g, st)
                : launch_packed_t<FB, SMEM, false, false, false, UND, F, F, F, F, F, 1, F, VU>(t, g, st);
 }
