@@ -382,8 +382,8 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
   const int grp = (RMAT_GRP && t->fb == 16 && !out64 && !prefix &&
                    std::getenv("RMAT_DISABLE_GRP") == nullptr) ? fixed_group(t, a->k) : 1;
   // small fixed-depth tables on units: bank-spread copies (RMAT_DISABLE_BANK=1 keeps one copy)
-  const bool bank = packed_ok && grp > 1 && !sg && !w64 && bank_spread_ok(t) &&
-                    std::getenv("RMAT_DISABLE_BANK") == nullptr;
+  const int bank = (packed_ok && grp > 1 && !sg && !w64 &&
+                    std::getenv("RMAT_DISABLE_BANK") == nullptr) ? bank_spread_level(t) : 0;
   uint64_t stream_begin = 0;
   for (uint32_t s0 = 0; s0 < a->n_segments; s0 += rmat::kMaxSegsPerLaunch) {
     rmat::GenLaunch g;
@@ -422,7 +422,7 @@ rmat_status rmat_generate(const rmat_gen_args* a, void* cuda_stream) {
     rmat_status rs;
     switch (kernel) {
       case RMAT_KERNEL_PACKED_SMEM:
-        rs = bank ? launch_packed_bank(t, g, grp, count, st)
+        rs = bank ? launch_packed_bank(t, g, grp, bank, count, st)
              : (grp > 1 && !sg && !w64) ? launch_packed_grp(t, g, true, grp, count, st)
              : sg            ? launch_sg(t, g, out64, prefix, count, st)
              : w64         ? launch_w64(t, g, prefix, count, st)

@@ -41,6 +41,12 @@ struct rmat_table {
 
 namespace rmat_impl {
 
+// shared-memory bytes per table entry of bank-spread copy level lv:
+// 2^AL copies of A (8 B) + 2^BL copies of B (4 B)
+constexpr uint64_t bank_bytes_per_entry(int lv) {
+  return lv == 1 ? 16 * 8 + 32 * 4 : lv == 2 ? 8 * 8 + 16 * 4 : 4 * 8 + 4 * 4;
+}
+
 int max_smem_optin(int dev);
 int num_sms(int dev);
 rmat::PackedTab packed_view(const rmat_table* t, bool rec = false);
@@ -48,7 +54,7 @@ rmat::GenericTab generic_view(const rmat_table* t);
 
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF = false,
           bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1,
-          bool BANK = false, bool VU = false>
+          int BANK = 0, bool VU = false>
 inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g, cudaStream_t st) {
   // R rounds of streams per thread: with the contiguous mapping the partial
   // last round runs on the first SMs only, wasting (ceil R - R) / ceil R of
@@ -66,7 +72,7 @@ inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g
   size_t smem = 0;
   if (SMEM) {
     threads = rmat::kSmemThreads;
-    smem = (BANK ? (size_t)t->n * 256 : t->packed_bytes) +
+    smem = (BANK ? (size_t)t->n * bank_bytes_per_entry(BANK) : t->packed_bytes) +
            (size_t)rmat::kSmemStrideThreads * rmat::kRingBytes;
     blocks = sms;
   } else {
@@ -107,15 +113,20 @@ inline int fixed_group(const rmat_table* t, uint32_t k) {
 // uint32 edges, no tile prefixes, fixed-depth table (GRP > 1)
 rmat_status launch_packed_grp(const rmat_table* t, const rmat::GenLaunch& g, bool smem, int grp,
                               bool count, cudaStream_t st);
-// small scheme-P fixed-depth tables (n <= 512): bank-spread copies in shared
-// memory (uint32 edges, no tile prefixes), fragments in units of grp (2 or 4)
-inline bool bank_spread_ok(const rmat_table* t) {
-  return t->fb == 16 && t->scheme_p && t->n <= 512 &&
-         t->n * 256 + (uint64_t)rmat::kSmemStrideThreads * rmat::kRingBytes <=
-             (uint64_t)max_smem_optin(t->device);
+// small scheme-P tables on unit kernels: bank-spread copy level (0 = none;
+// k_packed BANK note) -- the most copies that fit shared memory beside the ring
+inline int bank_spread_level(const rmat_table* t) {
+  if (!(t->fb == 16 && t->scheme_p)) return 0;
+  const uint64_t room = (uint64_t)max_smem_optin(t->device) -
+                        (uint64_t)rmat::kSmemStrideThreads * rmat::kRingBytes - 1024;
+  for (int lv = 1; lv <= 3; ++lv) {
+    const uint64_t lim = lv == 1 ? 512 : lv == 2 ? 1024 : 4096;
+    if (t->n <= lim && t->n * bank_bytes_per_entry(lv) <= room) return lv;
+  }
+  return 0;
 }
-rmat_status launch_packed_bank(const rmat_table* t, const rmat::GenLaunch& g, int grp, bool count,
-                               cudaStream_t st);
+rmat_status launch_packed_bank(const rmat_table* t, const rmat::GenLaunch& g, int grp, int level,
+                               bool count, cudaStream_t st);
 // the L1/L2-resident kernel on 16-byte records (t->pR; rmat_packed16.cu)
 rmat_status launch_packed_rec(const rmat_table* t, const rmat::GenLaunch& g, bool out64,
                               bool prefix, bool count, cudaStream_t st);

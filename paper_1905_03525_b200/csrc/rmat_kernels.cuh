@@ -342,12 +342,15 @@ __device__ __forceinline__ void flush_tail(char* gptr, uint32_t ring_sa, uint32_
 // careful path (stream ends, sample counts) stays per sample.
 template <int FB, bool SMEM, bool OUT64, bool PREFIX, bool COUNT, bool UND, bool REF,
           bool W64 = false, bool SG = false, bool K32 = false, bool REC = false, int GRP = 1,
-          bool BANK = false, bool SPR = false, bool VU = false>
+          int BANK = 0, bool SPR = false, bool VU = false>
 __global__ void __launch_bounds__(SMEM ? kSmemThreads : kGlobalThreads, SMEM ? 1 : RMAT_GLOBAL_MINB)
 k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   using AE = typename AEntry<FB>::T;
   static_assert(!REC || (FB == 16 && !SMEM && !REF && !SG), "records: 16-bit fields, global kernel");
   static_assert(!BANK || (FB == 16 && SMEM && !REF && !SG), "bank-spread copies: 16-bit fields, shared memory");
+  // bank-spread copy level -> log2 copies of B / A
+  constexpr uint32_t BANK_BL = BANK == 1 ? 5 : BANK == 2 ? 4 : 2;
+  constexpr uint32_t BANK_AL = BANK == 1 ? 4 : BANK == 2 ? 3 : 2;
   // VU (variable-depth tables, uint32 edges, block streams): the fast path
   // appends the fragments of samples (2u, 2u+1) as one unit of d_2u + d_2u+1
   // bits.  A unit holds one edge boundary unless f + D >= 2k (or D = 32);
@@ -369,20 +372,22 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   const uint8_t* baseB;
   uint8_t* stage;
   if (SMEM && BANK) {
-    // Bank-spread copies of a small table (n <= 512): A entry i of copy c at
-    // (16 i + c) * 8, B entry i of copy c at (32 i + c) * 4, lane l reads copy
-    // l & 15 of A and copy l of B -- random gathers without bank conflicts.
+    // Bank-spread copies of a small table: 2^BL copies of B and 2^AL of A
+    // interleaved entry-major (B entry i of copy c at (2^BL i + c) * 4, A at
+    // (2^AL i + c) * 8); lane l reads copy l mod 2^BL of B and l mod 2^AL of
+    // A.  Level 1 (n <= 512): 32 / 16 copies, no bank conflicts at all;
+    // level 2 (n <= 1024): 16 / 8; level 3 (n <= 4096): 4 / 4.
     const uint32_t n = tab.n;
     uint2* dA = reinterpret_cast<uint2*>(smem);
-    uint32_t* dB = reinterpret_cast<uint32_t*>(smem + (size_t)n * 128);
+    uint32_t* dB = reinterpret_cast<uint32_t*>(smem + ((size_t)n << (BANK_AL + 3)));
     const uint2* sA = reinterpret_cast<const uint2*>(tab.A);
-    for (uint32_t i = threadIdx.x; i < n * 16; i += THREADS) dA[i] = __ldg(sA + (i >> 4));
-    for (uint32_t i = threadIdx.x; i < n * 32; i += THREADS) dB[i] = __ldg(tab.B + (i >> 5));
+    for (uint32_t i = threadIdx.x; i < (n << BANK_AL); i += THREADS) dA[i] = __ldg(sA + (i >> BANK_AL));
+    for (uint32_t i = threadIdx.x; i < (n << BANK_BL); i += THREADS) dB[i] = __ldg(tab.B + (i >> BANK_BL));
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31;
-    baseA = smem + (lane & 15) * 8;
-    baseB = smem + (size_t)n * 128 + lane * 4;
-    stage = smem + (size_t)n * 256;
+    baseA = smem + (lane & ((1u << BANK_AL) - 1)) * 8;
+    baseB = smem + ((size_t)n << (BANK_AL + 3)) + (lane & ((1u << BANK_BL) - 1)) * 4;
+    stage = smem + ((size_t)n << (BANK_AL + 3)) + ((size_t)n << (BANK_BL + 2));
   } else if (SMEM) {
     // Stage the bucket arrays: A first (16B aligned), then B.
     const uint32_t n = tab.n;
@@ -600,9 +605,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         q.b[t] = rr.z;
         continue;
       }
-      if constexpr (BANK) {  // this lane's copy: entry i at base + 128 i = base + 32 a4
-        q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + (a4 << 5));
-        q.a[t] = *reinterpret_cast<const AE*>(baseA + (a4 << 5));
+      if constexpr (BANK) {  // this lane's copy: entry i at base + 2^BL 4 i / 2^AL 8 i (a4 = 4 i)
+        q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + (a4 << BANK_BL));
+        q.a[t] = *reinterpret_cast<const AE*>(baseA + (a4 << (BANK_AL + 1)));
         continue;
       }
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);

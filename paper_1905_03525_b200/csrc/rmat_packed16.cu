@@ -36,9 +36,14 @@ rmat_status launch_packed_fu(const rmat_table* t, const rmat::GenLaunch& g, bool
                  : launch_packed_t<FB, SMEM, false, true, false, UND, F, F, F, F, F, 1, F, VU>(t, g, st);
   // small variable-depth tables on units: bank-spread copies (RMAT_DISABLE_BANK=1: one copy)
   if constexpr (SMEM && VU) {
-    if (bank_spread_ok(t) && std::getenv("RMAT_DISABLE_BANK") == nullptr)
-      return count ? launch_packed_t<16, true, false, false, true, UND, F, F, F, F, F, 1, true, true>(t, g, st)
-                   : launch_packed_t<16, true, false, false, false, UND, F, F, F, F, F, 1, true, true>(t, g, st);
+    const int lv = std::getenv("RMAT_DISABLE_BANK") == nullptr ? bank_spread_level(t) : 0;
+#define RMAT_VU_BANK(L)                                                                              \
+  return count ? launch_packed_t<16, true, false, false, true, UND, F, F, F, F, F, 1, L, true>(t, g, st) \
+               : launch_packed_t<16, true, false, false, false, UND, F, F, F, F, F, 1, L, true>(t, g, st)
+    if (lv == 1) RMAT_VU_BANK(1);
+    if (lv == 2) RMAT_VU_BANK(2);
+    if (lv == 3) RMAT_VU_BANK(3);
+#undef RMAT_VU_BANK
   }
   return count ? launch_packed_t<FB, SMEM, false, false, true, UND, F, F, F, F, F, 1, F, VU>(t, g, st)
                : launch_packed_t<FB, SMEM, false, false, false, UND, F, F, F, F, F, 1, F, VU>(t, g, st);
@@ -87,22 +92,30 @@ rmat_status launch_packed_grp(const rmat_table* t, const rmat::GenLaunch& g, boo
 // Small fixed-depth tables as bank-spread copies, units of GRP fragments
 // (uint32 edges, no prefixes).  Per sample the copies measured +-0 (the
 // integer pipes bind together with L1); with the units, +15 % (l = 4).
-template <int GRP, bool UND>
+template <int GRP, bool UND, int LV>
 rmat_status launch_packed_bank_u(const rmat_table* t, const rmat::GenLaunch& g, bool count,
                                  cudaStream_t st) {
   constexpr bool F = false;
-  return count ? launch_packed_t<16, true, F, F, true, UND, F, F, F, F, F, GRP, true>(t, g, st)
-               : launch_packed_t<16, true, F, F, false, UND, F, F, F, F, F, GRP, true>(t, g, st);
+  return count ? launch_packed_t<16, true, F, F, true, UND, F, F, F, F, F, GRP, LV>(t, g, st)
+               : launch_packed_t<16, true, F, F, false, UND, F, F, F, F, F, GRP, LV>(t, g, st);
 }
 
-rmat_status launch_packed_bank(const rmat_table* t, const rmat::GenLaunch& g, int grp, bool count,
-                               cudaStream_t st) {
+template <int LV>
+rmat_status launch_packed_bank_l(const rmat_table* t, const rmat::GenLaunch& g, int grp, bool count,
+                                 cudaStream_t st) {
   const bool und = g.post & RMAT_POST_UNDIRECTED;
   if (grp == 4)
-    return und ? launch_packed_bank_u<4, true>(t, g, count, st)
-               : launch_packed_bank_u<4, false>(t, g, count, st);
-  return und ? launch_packed_bank_u<2, true>(t, g, count, st)
-             : launch_packed_bank_u<2, false>(t, g, count, st);
+    return und ? launch_packed_bank_u<4, true, LV>(t, g, count, st)
+               : launch_packed_bank_u<4, false, LV>(t, g, count, st);
+  return und ? launch_packed_bank_u<2, true, LV>(t, g, count, st)
+             : launch_packed_bank_u<2, false, LV>(t, g, count, st);
+}
+
+rmat_status launch_packed_bank(const rmat_table* t, const rmat::GenLaunch& g, int grp, int level,
+                               bool count, cudaStream_t st) {
+  return level == 1 ? launch_packed_bank_l<1>(t, g, grp, count, st)
+         : level == 2 ? launch_packed_bank_l<2>(t, g, grp, count, st)
+                      : launch_packed_bank_l<3>(t, g, grp, count, st);
 }
 
 // 16-byte bucket records, L1/L2-resident (tables beyond shared memory)

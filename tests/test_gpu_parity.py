@@ -385,11 +385,13 @@ def test_fixed_depth_units_match_per_sample(cuda, monkeypatch, tag, k):
 
 
 @pytest.mark.parametrize("tag,k,undirected", [("f4", 26, False), ("f4", 16, True), ("f1", 7, False),
-                                              ("f4", 9, False), ("v256", 26, False), ("v256", 12, True)])
+                                              ("f4", 9, False), ("v256", 26, False), ("v256", 12, True),
+                                              ("v1024", 26, False), ("f6", 26, True), ("v4096", 24, False),
+                                              ("v4096", 28, True)])
 def test_bank_spread_copies_match_one_copy(cuda, monkeypatch, tag, k, undirected):
-    """Small tables (n <= 512) on fragment units (fixed depth) or sample pairs
-    (variable depth) read bank-spread copies (lane l: copy l of B, l & 15 of
-    A); RMAT_DISABLE_BANK=1 keeps one copy.  Same edges and sample counts, the
+    """Tables of <= 4096 entries on fragment units (fixed depth) or sample pairs
+    (variable depth) read bank-spread copies (three levels: 32/16, 16/8 or 4/4
+    copies of B/A); RMAT_DISABLE_BANK=1 keeps one copy.  Same edges and sample counts, the
     oracle's."""
     dt = device_table(table_for(tag), cuda)
     m, E = 30_000, 1024
