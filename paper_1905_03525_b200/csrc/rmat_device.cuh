@@ -52,18 +52,21 @@ inline uint32_t bucket_word(uint32_t T, uint32_t fm, uint32_t d_self, uint32_t d
 struct BucketTest {
   uint32_t ge;  // 1: fraction top bits >= threshold top bits (alias unless a tie says otherwise)
   bool tie;     // top bits equal: the low F bits decide
+  uint32_t lo;  // tie <=> lo <= fm (so several samples' ties are one min + one compare)
 };
 // `one` must be a run-time 1 (PackedTab::one) so the IMAD is not folded into adds.
 __device__ __forceinline__ BucketTest bucket_test(uint32_t w, uint32_t b, uint32_t fm, uint32_t one) {
   BucketTest r;
   if (RMAT_B_PLAIN) {
     r.ge = w >= b ? 1u : 0u;
-    r.tie = (w ^ b) <= fm;
+    r.lo = w ^ b;
+    r.tie = r.lo <= fm;
   } else {
     uint64_t sum;
     asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(sum) : "r"(w | fm), "r"(one), "l"((uint64_t)b));
     r.ge = (uint32_t)(sum >> 32);
-    r.tie = (uint32_t)sum <= fm;
+    r.lo = (uint32_t)sum;
+    r.tie = r.lo <= fm;
   }
   return r;
 }

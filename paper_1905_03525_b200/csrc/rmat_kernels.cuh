@@ -126,6 +126,17 @@ __device__ __forceinline__ uint32_t dp2a_lo(uint32_t a, uint32_t b) {
   asm("dp2a.lo.u32.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(a), "r"(b));
   return r;
 }
+__device__ __forceinline__ uint32_t dp2a_hi(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("dp2a.hi.u32.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// split-array stride c (bytes): self words at c, alias words at 256 c, 255 c >= 4 n
+__host__ __device__ inline uint32_t asplit_c(uint32_t n) { return 4u * ((n + 254u) / 255u); }
+// bytes of the split fragment arrays in shared memory (16-byte padded)
+__host__ __device__ inline size_t asplit_bytes(uint32_t n) {
+  return ((size_t)256 * asplit_c(n) + (size_t)4 * n + 15) & ~(size_t)15;
+}
 __device__ __forceinline__ uint32_t dp4a_u(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("dp4a.u32.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(a), "r"(b));
@@ -232,6 +243,30 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 // fast loop changes; it times what the rest of the loop costs without them.
 #ifndef RMAT_PROBE
 #define RMAT_PROBE 0
+#endif
+// RMAT_TIE_MIN: fraction ties of an iteration found by one min tree over the
+// samples' tie words and one compare (instead of a predicate per sample OR-ed
+// per call).
+#ifndef RMAT_TIE_MIN
+#define RMAT_TIE_MIN 1
+#endif
+// RMAT_VU_FLUSH_ITER: the unit kernels check for a completed sector once per
+// iteration when its units cannot emit more than G edges (2 units per call,
+// one edge per unit at most: 2 * CPI <= G), instead of once per call.  With s
+// < G edges staged after a check, s + G <= 2G - 1 slots never wrap onto the
+// open sector and at most one sector completes.
+#ifndef RMAT_VU_FLUSH_ITER
+#define RMAT_VU_FLUSH_ITER 1
+#endif
+// RMAT_ASPLIT (unit kernels on one shared-memory table copy): the fragments
+// live in two word arrays, self and alias (one word = row bits | col bits << 16),
+// and a sample gathers only the chosen fragment's 4 bytes after the compare
+// (address = bucket offset + selector * c, selector 1 / 256, arrays at c and
+// 256 c) instead of the 8-byte {self, alias} pair before it: a random 4-byte
+// gather costs ~3.5 L1 wavefronts per warp, the 8-byte one ~6.2.
+// 1: both halves by IDP (FMA pipe); 2: row by LOP3, col by IDP; 3: LOP3 + SHF.
+#ifndef RMAT_ASPLIT
+#define RMAT_ASPLIT 0
 #endif
 #ifndef RMAT_HEADS_CAREFUL
 #define RMAT_HEADS_CAREFUL 1
@@ -366,6 +401,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   constexpr uint32_t STRIDE = RingGeo<OUT64, STHREADS>::STRIDE;  // slot-major ring
   // fragment / depth selection by dot products on one byte selector (RMAT_IDP)
   constexpr bool IDPSEL = RMAT_IDP && FB == 16;
+  constexpr bool ASPLIT = RMAT_ASPLIT && VU && !REF && !BANK && SMEM;
   extern __shared__ __align__(16) uint8_t smem[];
 
   const uint8_t* baseA;
@@ -388,6 +424,24 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     baseA = smem + (lane & ((1u << BANK_AL) - 1)) * 8;
     baseB = smem + ((size_t)n << (BANK_AL + 3)) + (lane & ((1u << BANK_BL) - 1)) * 4;
     stage = smem + ((size_t)n << (BANK_AL + 3)) + ((size_t)n << (BANK_BL + 2));
+  } else if (SMEM && ASPLIT) {
+    // fragment words: self array at c, alias array at 256 c, then B
+    const uint32_t n = tab.n, c = asplit_c(n);
+    const size_t boff = asplit_bytes(n), soff = (boff + (size_t)n * 4 + 15) & ~(size_t)15;
+    const uint2* sA = reinterpret_cast<const uint2*>(tab.A);
+    uint32_t* dS = reinterpret_cast<uint32_t*>(smem + c);
+    uint32_t* dL = reinterpret_cast<uint32_t*>(smem + 256 * (size_t)c);
+    uint32_t* dB = reinterpret_cast<uint32_t*>(smem + boff);
+    for (uint32_t i = threadIdx.x; i < n; i += THREADS) {
+      const uint2 a = __ldg(sA + i);
+      dS[i] = (a.x & 0xFFFFu) | (a.y << 16);
+      dL[i] = (a.x >> 16) | (a.y & 0xFFFF0000u);
+      dB[i] = __ldg(tab.B + i);
+    }
+    __syncthreads();
+    baseA = smem;
+    baseB = smem + boff;
+    stage = smem + soff;
   } else if (SMEM) {
     // Stage the bucket arrays: A first (16B aligned), then B.
     const uint32_t n = tab.n;
@@ -553,8 +607,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // One call's worth of samples: words, bucket entries, byte selectors.
   struct Batch {
     uint32_t w[4], b[4], sel[4], seld[4], x[4];  // x: REF bucket byte offsets
+    uint32_t fw[4];  // ASPLIT: the chosen fragment's word (load_frags)
     AE a[4];
     bool tie;
+    uint32_t tmin;  // min of the four tie words (bucket_test lo): tie <=> tmin <= fm
   };
   // Draw call jj of the current stream and resolve everything that does not
   // depend on the bit accumulator (software-pipelined one call ahead).
@@ -611,24 +667,26 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         continue;
       }
       q.b[t] = *reinterpret_cast<const uint32_t*>(baseB + a4);
-      q.a[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
+      if constexpr (!ASPLIT) q.a[t] = *reinterpret_cast<const AE*>(baseA + a4 * (sizeof(AE) / 4));
     }
     q.tie = false;
+    q.tmin = 0xFFFFFFFFu;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       // B: threshold top bits above the depth fields (rmat_device.cuh
       // bucket_test); ge = alias unless the top bits tie.
       const BucketTest bt = bucket_test(q.w[t], q.b[t], fm, one);
-      q.tie |= bt.tie;
+      if (RMAT_TIE_MIN) q.tmin = min(q.tmin, bt.lo); else q.tie |= bt.tie;
       q.sel[t] = IDPSEL ? mad_lo(bt.ge, 255u, 1u)      // IDP byte selector: 1 self / 256 alias
                         : mad_lo(bt.ge, 0x22u, 0x4410u);  // PRMT selectors: 0x4410 self / 0x4432 alias
       q.seld[t] = bt.ge + 0x4440u;               // depth byte: 0x4440 self / 0x4441 alias
     }
+    if (RMAT_TIE_MIN) q.tie = q.tmin <= fm;
     return q;
   };
   // Rare (2^-(32-F) per sample): decide fraction ties with the lazy word.
   auto resolve_ties = [&](Batch& cb, uint32_t jj) {
-    if (!cb.tie) return;
+    if (RMAT_TIE_MIN ? cb.tmin > fm : !cb.tie) return;
     if constexpr (REF || SG) {  // the word carries its full 32-bit fraction
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -650,6 +708,23 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         cb.sel[t] = IDPSEL ? (lt ? 1u : 256u) : lt ? 0x4410u : 0x4432u;
         cb.seld[t] = lt ? 0x4440u : 0x4441u;
       }
+  };
+  // ASPLIT: gather the chosen fragments once the selectors are final
+  const uint32_t asc = ASPLIT ? asplit_c(tab.n) : 0u;
+  auto load_frags = [&](Batch& cb) {
+    if constexpr (ASPLIT) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        cb.fw[t] = *reinterpret_cast<const uint32_t*>(baseA + mad_lo(cb.sel[t], asc, cb.w[t] & idxmask4));
+    }
+  };
+  auto frag_r = [&](const Batch& cb, int t) -> uint32_t {
+    if constexpr (ASPLIT) return RMAT_ASPLIT == 1 ? dp2a_lo(cb.fw[t], 0x01000001u) : (cb.fw[t] & 0xFFFFu);
+    else return dp2a_lo(cb.a[t].x, cb.sel[t]);
+  };
+  auto frag_c = [&](const Batch& cb, int t) -> uint32_t {
+    if constexpr (ASPLIT) return RMAT_ASPLIT == 3 ? (cb.fw[t] >> 16) : dp2a_hi(cb.fw[t], 0x01000001u);
+    else return dp2a_lo(cb.a[t].y, cb.sel[t]);
   };
   // Fragments of one call appended to the accumulators; stores into the ring
   // and completed sectors flushed.  CAREFUL caps stores at `left`.
@@ -674,8 +749,13 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           c = s2 ? mad_lo(c, gP, cs) : cs;
         }
       } else if constexpr (FB == 16) {
-        r = IDPSEL ? dp2a_lo(cb.a[t].x, cb.sel[t]) : prmt(cb.a[t].x, cb.sel[t]);
-        c = IDPSEL ? dp2a_lo(cb.a[t].y, cb.sel[t]) : prmt(cb.a[t].y, cb.sel[t]);
+        if constexpr (ASPLIT) {
+          r = frag_r(cb, t);
+          c = frag_c(cb, t);
+        } else {
+          r = IDPSEL ? dp2a_lo(cb.a[t].x, cb.sel[t]) : prmt(cb.a[t].x, cb.sel[t]);
+          c = IDPSEL ? dp2a_lo(cb.a[t].y, cb.sel[t]) : prmt(cb.a[t].y, cb.sel[t]);
+        }
       } else {
         const bool lt = cb.sel[t] == 0x4410u;
         r = lt ? cb.a[t].x : cb.a[t].y;
@@ -889,8 +969,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // (the caller has checked D <= min(k, 31) for every unit of the iteration)
   auto step_unit = [&](const Batch& cb, int ta, int tb, uint32_t D) {
     const uint32_t db = dp4a_u(cb.b[tb], cb.sel[tb]);
-    const uint32_t ra = dp2a_lo(cb.a[ta].x, cb.sel[ta]), rb = dp2a_lo(cb.a[tb].x, cb.sel[tb]);
-    const uint32_t ca = dp2a_lo(cb.a[ta].y, cb.sel[ta]), cb_ = dp2a_lo(cb.a[tb].y, cb.sel[tb]);
+    const uint32_t ra = frag_r(cb, ta), rb = frag_r(cb, tb);
+    const uint32_t ca = frag_c(cb, ta), cb_ = frag_c(cb, tb);
     if constexpr (REF && RMAT_REF_SHIFT_APPEND) {
       append_bits((ra << db) | rb, (ca << db) | cb_, D);
     } else {
@@ -925,12 +1005,21 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #pragma unroll
       for (int c = 0; c < CPI; ++c) cb[c] = fetch(j + c);
       bool anytie = false;
+      if constexpr (RMAT_TIE_MIN) {  // one min tree over the iteration's tie words, one compare
+        uint32_t tm = cb[0].tmin;
 #pragma unroll
-      for (int c = 0; c < CPI; ++c) anytie |= cb[c].tie;
+        for (int c = 1; c < CPI; ++c) tm = min(tm, cb[c].tmin);
+        anytie = tm <= fm;
+      } else {
+#pragma unroll
+        for (int c = 0; c < CPI; ++c) anytie |= cb[c].tie;
+      }
       if (__any_sync(0xFFFFFFFFu, anytie)) {
 #pragma unroll
         for (int c = 0; c < CPI; ++c) resolve_ties(cb[c], j + c);
       }
+#pragma unroll
+      for (int c = 0; c < CPI; ++c) load_frags(cb[c]);
       uint32_t unused = 0;
       if constexpr (VU) {
         // unit depths; a unit deeper than min(k, 31) bits might hold two edge
@@ -952,7 +1041,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           for (int c = 0; c < CPI; ++c) {
             step_unit(cb[c], 0, 1, DU[c][0]);
             step_unit(cb[c], 2, 3, DU[c][1]);
-            unit_flush();  // at most two edges this call
+            // at most two edges per call: one check per iteration if they fit a sector
+            if (!(RMAT_VU_FLUSH_ITER && 2 * CPI <= (int)G) || c == CPI - 1) unit_flush();
           }
           j += CPI;
           continue;
@@ -1005,6 +1095,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     }
     Batch cb = fetch(j);
     if (__any_sync(__activemask(), cb.tie)) resolve_ties(cb, j);
+    load_frags(cb);
     step(cb, std::true_type{}, left);
     ++j;
   }
