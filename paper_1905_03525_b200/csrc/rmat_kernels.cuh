@@ -266,7 +266,7 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 // gather costs ~3.5 L1 wavefronts per warp, the 8-byte one ~6.2.
 // 1: both halves by IDP (FMA pipe); 2: row by LOP3, col by IDP; 3: LOP3 + SHF.
 #ifndef RMAT_ASPLIT
-#define RMAT_ASPLIT 0
+#define RMAT_ASPLIT 2  // measured (C3, on top of the per-iteration flush): 1 +3.9 %, 2 +4.1 %, 3 +3.4 %
 #endif
 #ifndef RMAT_HEADS_CAREFUL
 #define RMAT_HEADS_CAREFUL 1
@@ -730,9 +730,12 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   // and completed sectors flushed.  CAREFUL caps stores at `left`.
   // GRP units: fragment width P = 2^dfix, unit depth and its power of two
   const uint32_t gP = 1u << tab.dfix, gD = GRP * tab.dfix, gPW = 1u << (GRP * tab.dfix);
-  auto step = [&](Batch& cb, auto careful_tag, uint32_t& left) {
+  auto step = [&](Batch& cb, auto careful_tag, uint32_t& left, bool last_call = true) {
     constexpr bool CAREFUL = decltype(careful_tag)::value;
     constexpr int UG = (GRP > 1 && !CAREFUL) ? GRP : 1;  // samples per unit
+    // fixed-depth units: 4 / UG edges per call at most; if an iteration's fit one
+    // sector the check runs once per iteration (RMAT_VU_FLUSH_ITER)
+    constexpr bool ITER_FLUSH = RMAT_VU_FLUSH_ITER && UG > 1 && (4 / UG) * CPI <= (int)G;
     if (COUNT) ebits = 0;
 #pragma unroll
     for (int un = 0; un < 4 / UG; ++un) {
@@ -874,7 +877,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         if (CAREFUL) --left;
       }
       if (COUNT) ebits |= (uint32_t)st << t;
-      if ((uint32_t)t % G == G - 1) {
+      if ((uint32_t)t % G == G - 1 && (!ITER_FLUSH || last_call)) {
         // At most G edges since the last check (at most one per unit): the sector at gptr is
         // complete when the next slot has left its ring half.
         const bool full = rp_half(roff) != half;
@@ -1014,13 +1017,13 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #pragma unroll
         for (int c = 0; c < CPI; ++c) anytie |= cb[c].tie;
       }
+      uint32_t unused = 0;
       if (__any_sync(0xFFFFFFFFu, anytie)) {
 #pragma unroll
         for (int c = 0; c < CPI; ++c) resolve_ties(cb[c], j + c);
       }
 #pragma unroll
       for (int c = 0; c < CPI; ++c) load_frags(cb[c]);
-      uint32_t unused = 0;
       if constexpr (VU) {
         // unit depths; a unit deeper than min(k, 31) bits might hold two edge
         // boundaries (f + D >= 2k needs D > k since f < k) or overflow 2^D:
@@ -1056,7 +1059,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         continue;
       }
 #pragma unroll
-      for (int c = 0; c < CPI; ++c) step(cb[c], std::false_type{}, unused);
+      for (int c = 0; c < CPI; ++c) step(cb[c], std::false_type{}, unused, c == CPI - 1);
       j += CPI;
       continue;
     }
