@@ -43,7 +43,7 @@ struct SegDev {
 // and the carry of (w | fm) + B (one 64-bit IMAD) decides.  Either way a tie
 // is settled from the low F fraction bits against TLO.
 #ifndef RMAT_B_PLAIN
-#define RMAT_B_PLAIN 0  // measured: 3 % slower on C3 despite 7 % fewer instructions
+#define RMAT_B_PLAIN 1  // round 1 (per-sample kernel): -3 %; on the unit kernels with the per-iteration flush: C3 +2.2 %, C4 +3.3 %, reference blocks +1.7 %
 #endif
 inline uint32_t bucket_word(uint32_t T, uint32_t fm, uint32_t d_self, uint32_t d_alias) {
   return ((RMAT_B_PLAIN ? T : ~T) & ~fm) | d_self | (d_alias << 8);

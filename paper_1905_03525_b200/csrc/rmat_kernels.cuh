@@ -143,6 +143,11 @@ __device__ __forceinline__ uint32_t dp4a_u(uint32_t a, uint32_t b) {
   return r;
 }
 
+__device__ __forceinline__ uint32_t dp4a_acc(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
 __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
@@ -274,6 +279,10 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 constexpr bool kHeadsCareful = RMAT_HEADS_CAREFUL != 0;  // PREFIX: unaligned heads off the fast path
 // slot-major ring addressing wants a power-of-two thread stride
 constexpr int kSmemStrideThreads = kSmemThreads <= 256 ? 256 : kSmemThreads <= 512 ? 512 : 1024;
+// ASPLIT shared-memory image: ring | B (up to kAsplitMaxN entries) | fragment words
+constexpr uint32_t kAsplitMaxN = 1u << 14;
+constexpr size_t kAsplitBOff = (size_t)kSmemStrideThreads * kRingBytes;
+constexpr size_t kAsplitAOff = kAsplitBOff + (size_t)kAsplitMaxN * 4;
 #ifndef RMAT_GLOBAL_THREADS
 #define RMAT_GLOBAL_THREADS 256
 #endif
@@ -425,12 +434,14 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     baseB = smem + ((size_t)n << (BANK_AL + 3)) + (lane & ((1u << BANK_BL) - 1)) * 4;
     stage = smem + ((size_t)n << (BANK_AL + 3)) + ((size_t)n << (BANK_BL + 2));
   } else if (SMEM && ASPLIT) {
-    // fragment words: self array at c, alias array at 256 c, then B
+    // compile-time offsets (the gathers' LDS take them as immediates): ring,
+    // B (n <= 2^14 entries, host-checked), then the fragment words -- self
+    // array at c, alias array at 256 c
     const uint32_t n = tab.n, c = asplit_c(n);
-    const size_t boff = asplit_bytes(n), soff = (boff + (size_t)n * 4 + 15) & ~(size_t)15;
+    constexpr size_t boff = kAsplitBOff, aoff = kAsplitAOff;
     const uint2* sA = reinterpret_cast<const uint2*>(tab.A);
-    uint32_t* dS = reinterpret_cast<uint32_t*>(smem + c);
-    uint32_t* dL = reinterpret_cast<uint32_t*>(smem + 256 * (size_t)c);
+    uint32_t* dS = reinterpret_cast<uint32_t*>(smem + aoff + c);
+    uint32_t* dL = reinterpret_cast<uint32_t*>(smem + aoff + 256 * (size_t)c);
     uint32_t* dB = reinterpret_cast<uint32_t*>(smem + boff);
     for (uint32_t i = threadIdx.x; i < n; i += THREADS) {
       const uint2 a = __ldg(sA + i);
@@ -439,9 +450,9 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       dB[i] = __ldg(tab.B + i);
     }
     __syncthreads();
-    baseA = smem;
+    baseA = smem + aoff;
     baseB = smem + boff;
-    stage = smem + soff;
+    stage = smem;
   } else if (SMEM) {
     // Stage the bucket arrays: A first (16B aligned), then B.
     const uint32_t n = tab.n;
@@ -677,7 +688,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
       // bucket_test); ge = alias unless the top bits tie.
       const BucketTest bt = bucket_test(q.w[t], q.b[t], fm, one);
       if (RMAT_TIE_MIN) q.tmin = min(q.tmin, bt.lo); else q.tie |= bt.tie;
-      q.sel[t] = IDPSEL ? mad_lo(bt.ge, 255u, 1u)      // IDP byte selector: 1 self / 256 alias
+      q.sel[t] = IDPSEL ? (RMAT_B_PLAIN ? (bt.ge ? 256u : 1u)  // (plain compare: ISETP + SEL)
+                                        : mad_lo(bt.ge, 255u, 1u))  // IDP byte selector: 1 self / 256 alias
                         : mad_lo(bt.ge, 0x22u, 0x4410u);  // PRMT selectors: 0x4410 self / 0x4432 alias
       q.seld[t] = bt.ge + 0x4440u;               // depth byte: 0x4440 self / 0x4441 alias
     }
@@ -1035,7 +1047,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         for (int c = 0; c < CPI; ++c) {
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            DU[c][u] = dp4a_u(cb[c].b[2 * u], cb[c].sel[2 * u]) + dp4a_u(cb[c].b[2 * u + 1], cb[c].sel[2 * u + 1]);
+            // d_2u + d_2u+1: the second dot product accumulates onto the first
+            DU[c][u] = dp4a_acc(cb[c].b[2 * u], cb[c].sel[2 * u], dp4a_u(cb[c].b[2 * u + 1], cb[c].sel[2 * u + 1]));
             deep |= DU[c][u] > vu_lim;
           }
         }
