@@ -270,6 +270,21 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 // 256 c) instead of the 8-byte {self, alias} pair before it: a random 4-byte
 // gather costs ~3.5 L1 wavefronts per warp, the 8-byte one ~6.2.
 // 1: both halves by IDP (FMA pipe); 2: row by LOP3, col by IDP; 3: LOP3 + SHF.
+// RMAT_FASTEND (unit kernels that do not count samples): the fast path runs
+// while the open sector lies wholly inside the stream (L >= G) instead of
+// while 4 CPI + R - 1 edges remain.  An iteration emits at most G edges, so
+// its one sector flush is a whole sector of the stream; edges staged past the
+// stream's end are never flushed (the tail is capped at L).  A stream whose
+// length is a multiple of G ends on that flush (L = 0) and the lane opens its
+// next stream at the top of the loop, so the other lanes of the warp never
+// leave the fast path for it.  A deep unit sends the iteration to the careful
+// path (capped stores) instead of the uncapped per-sample code.
+#ifndef RMAT_FASTEND
+#define RMAT_FASTEND 1
+#endif
+#ifndef RMAT_FASTEND_QUICK
+#define RMAT_FASTEND_QUICK 1
+#endif
 #ifndef RMAT_ASPLIT
 #define RMAT_ASPLIT 2  // measured (C3, on top of the per-iteration flush): 1 +3.9 %, 2 +4.1 %, 3 +3.4 %
 #endif
@@ -502,7 +517,10 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #endif
   uint32_t rk[20];
   // VU_RKC: the two-call VU fast path reads the round keys from the constant bank
-  constexpr bool VU_RKC = VU && !REF && !PREFIX && !OUT64 && RMAT_VU_CPI == 2;
+#ifndef RMAT_VU_RKC
+#define RMAT_VU_RKC 0  // keys in registers (116 registers after the split arrays, no spill): C3 +1.5 %
+#endif
+  constexpr bool VU_RKC = RMAT_VU_RKC && VU && !REF && !PREFIX && !OUT64 && RMAT_VU_CPI == 2;
   if (REF) {
   } else if (RMAT_RK_REGS == 0 || VU_RKC) {
 #pragma unroll
@@ -1006,14 +1024,73 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     if constexpr (!LGPTR) L -= full ? G : 0;
   };
 
+  constexpr bool FASTEND = RMAT_FASTEND && VU && !REF && !COUNT && !LGPTR && !RMAT_PROBE &&
+                           !PREFIX && !OUT64 &&  // (tile streams, C4: measured -1.2 %)
+                           RMAT_VU_FLUSH_ITER && 2 * CPI <= (int)G;  // (at most G edges per iteration)
+  // Stream done: write its partial last sector (capped at the stream's end:
+  // FASTEND may have staged edges past it), account nf, open the next stream.
+  auto next_stream = [&]() -> bool {
+    const uint32_t hi_slot = min(rp_slot(roff) & (G - 1), FASTEND ? L : G);
+    if (hi_slot > lo) flush_tail<OUT64, STHREADS>(gptr, ring_sa, half, lo, hi_slot);
+    if (COUNT) {
+      // nf (generator.py:255-257): the highest sample of call j-1 that
+      // produced an edge this stream needed.
+      const uint64_t nf = 4ull * (j - 1) + (32 - __clz(ebits)) + (REF ? p.nf_base : 0ull);
+      if (!REF || p.report) {
+        total_nf += nf;
+        if (g.samples_per_stream) g.samples_per_stream[s] = nf;
+      }
+    }
+    s += T;
+    p = open_stream<REF>(g, s);
+    if (!p.valid) return false;
+    stream_keys();
+    if (!REF) pre = make_pre();
+    j = 0; cur_r = cur_c = 0; f = REF ? p.lead : 0u;
+    cur_r64 = cur_c64 = 0;
+    L = (uint32_t)p.left;
+    roff = rp_init(p.row);
+    half = rp_half(roff);
+    lo = rp_slot(roff) & (G - 1);
+    L += lo;
+    if (REF) lo += p.drop;
+    gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+    gLend = gptr + (uint64_t)L * EB;
+    gfastL = gLend - (uint64_t)(4 * CPI + R - 1) * EB;
+    return true;
+  };
   for (;;) {
+    if constexpr (FASTEND) {
+      // a stream that ended on the last sector flush: open the next one here,
+      // the warp stays on the fast path
+      if (L == 0) {
+        if (RMAT_FASTEND_QUICK && g.nseg == 1 && s + T + 1 < g.total_streams) {
+          // the next stream is another whole stream of the launch's only
+          // segment: same key, prefixes and length, T streams further on
+          s += T;
+          p.sid += T;
+          p.row += T * g.E;
+          pre = make_pre();
+          j = 0; cur_r = cur_c = 0; f = 0;
+          L = (uint32_t)g.E;
+          roff = rp_init(p.row);
+          half = rp_half(roff);
+          lo = rp_slot(roff) & (G - 1);
+          L += lo;
+          gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+        } else if (!next_stream()) {
+          break;
+        }
+      }
+    }
     // Warp-uniform fast path: every lane has >= 4 edges still to produce
     // (L - staged >= L - (R - 1)), so no stream ends during this call and
     // stores need no cap.
     // Tile streams may start mid-sector (lo != 0): such a lane keeps the warp
     // on the careful path until its partial head sector has been flushed, so
     // the fast path's flush is one predicated sector store with no call.
-    const bool fast_ok = (LGPTR ? gptr <= gfastL : L >= 4 * CPI + R - 1) &&
+    // (FASTEND: the open sector lies inside the stream, see RMAT_FASTEND)
+    const bool fast_ok = (LGPTR ? gptr <= gfastL : FASTEND ? L >= G : L >= 4 * CPI + R - 1) &&
                          (!(PREFIX && kHeadsCareful) || lo == 0);
     if (__all_sync(0xFFFFFFFFu, fast_ok)) {
       Batch cb[CPI];
@@ -1024,7 +1101,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         uint32_t tm = cb[0].tmin;
 #pragma unroll
         for (int c = 1; c < CPI; ++c) tm = min(tm, cb[c].tmin);
-        anytie = tm <= fm;
+        anytie = tm <= fm;  // (ptxas folds the per-call trees into VIMNMX3s)
       } else {
 #pragma unroll
         for (int c = 0; c < CPI; ++c) anytie |= cb[c].tie;
@@ -1071,42 +1148,18 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         j += CPI;
         continue;
       }
+      if constexpr (!FASTEND) {
 #pragma unroll
-      for (int c = 0; c < CPI; ++c) step(cb[c], std::false_type{}, unused, c == CPI - 1);
-      j += CPI;
-      continue;
+        for (int c = 0; c < CPI; ++c) step(cb[c], std::false_type{}, unused, c == CPI - 1);
+        j += CPI;
+        continue;
+      }
+      // (FASTEND: a deep unit somewhere -- this call runs on the careful path below)
     }
     if constexpr (LGPTR) L = (uint32_t)((uint64_t)(gLend - gptr) / EB);
-    uint32_t left = L - staged();
+    uint32_t left = L - (FASTEND ? min(staged(), L) : staged());
     if (left == 0) {
-      // Stream done: write its partial last sector, account nf, open the next.
-      const uint32_t hi_slot = rp_slot(roff) & (G - 1);
-      if (hi_slot > lo) flush_tail<OUT64, STHREADS>(gptr, ring_sa, half, lo, hi_slot);
-      if (COUNT) {
-        // nf (generator.py:255-257): the highest sample of call j-1 that
-        // produced an edge this stream needed.
-        const uint64_t nf = 4ull * (j - 1) + (32 - __clz(ebits)) + (REF ? p.nf_base : 0ull);
-        if (!REF || p.report) {
-          total_nf += nf;
-          if (g.samples_per_stream) g.samples_per_stream[s] = nf;
-        }
-      }
-      s += T;
-      p = open_stream<REF>(g, s);
-      if (!p.valid) break;
-      stream_keys();
-      if (!REF) pre = make_pre();
-      j = 0; cur_r = cur_c = 0; f = REF ? p.lead : 0u;
-      cur_r64 = cur_c64 = 0;
-      L = (uint32_t)p.left;
-      roff = rp_init(p.row);
-      half = rp_half(roff);
-      lo = rp_slot(roff) & (G - 1);
-      L += lo;
-      if (REF) lo += p.drop;
-      gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
-      gLend = gptr + (uint64_t)L * EB;
-      gfastL = gLend - (uint64_t)(4 * CPI + R - 1) * EB;
+      if (!next_stream()) break;
       continue;
     }
     Batch cb = fetch(j);
