@@ -520,7 +520,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #ifndef RMAT_VU_RKC
 #define RMAT_VU_RKC 0  // keys in registers (116 registers after the split arrays, no spill): C3 +1.5 %
 #endif
-  constexpr bool VU_RKC = RMAT_VU_RKC && VU && !REF && !PREFIX && !OUT64 && RMAT_VU_CPI == 2;
+  // (the bank-spread kernels keep no split arrays and would spill with the keys in registers)
+  constexpr bool VU_RKC = (RMAT_VU_RKC || BANK != 0) && VU && !REF && !PREFIX && !OUT64 && RMAT_VU_CPI == 2;
   if (REF) {
   } else if (RMAT_RK_REGS == 0 || VU_RKC) {
 #pragma unroll
