@@ -323,10 +323,10 @@ def pipe_of(op: str) -> str:
 
 def pipe_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
     """The binding integer pipe: the per-sample SASS account of the committed
-    capture (profiles/r02_c3_pipe_account_vu.json) priced with the measured
+    capture (profiles/r02_c3_pipe_account_split.json) priced with the measured
     B200 pipe costs (profiles/r02_pipe_rate_probe.json: 2 cycles per warp
     instruction per SMSP on ALU and FMA-heavy, 4 for IMAD.WIDE / IMAD.HI)."""
-    acct = os.path.join(ROOT, "profiles", "r02_c3_pipe_account_vu.json")
+    acct = os.path.join(ROOT, "profiles", "r02_c3_pipe_account_split.json")
     summ = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(acct) as f:
@@ -350,7 +350,7 @@ def pipe_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
     return {"bound": "fma_heavy_pipe" if pipe == "fma" else "alu_pipe",
             "cycles_per_warp_sample": cyc, "ceiling_edges_per_s": ceiling,
             "achieved_edges_per_s": achieved, "frac": achieved / ceiling,
-            "source": "profiles/r02_c3_pipe_account_vu.json + r02_pipe_rate_probe.json"}
+            "source": "profiles/r02_c3_pipe_account_split.json + r02_pipe_rate_probe.json"}
 
 
 def lsu_bound_from_profile(kernel_s: float, edges: int) -> dict | None:

@@ -14,8 +14,13 @@ import subprocess
 
 
 def raw(rep: str) -> dict:
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    """`rep`: an .ncu-rep, or the `ncu -i rep --page raw --csv` export of one (the GPU
+    box exports it so that the large report need not travel back)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
