@@ -356,10 +356,10 @@ def pipe_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
 def lsu_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
     """The L1 data pipe beside the issue bound: LSU wavefronts per edge from the
     committed ncu capture (random bucket gathers from shared memory, ring staging,
-    sector stores) against one wavefront per SM per cycle.  At 95 % it binds
-    together with the integer pipes: removing the gathers (L1 -61 %) or 4.6 % of
-    the instructions (FMA-heavy -14 %) each leaves the rate unchanged
-    (profiles/r02_ablation.log, r02_ab_ns.log)."""
+    sector stores) against one wavefront per SM per cycle.  86 % busy on the
+    final kernel (95 % before the split fragment arrays, when it bound together
+    with the integer pipes: DESIGN.md section 5, profiles/r02_ablation.log,
+    r02_ab_ns.log, r02_ab_asplit.log)."""
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as f:
@@ -379,7 +379,7 @@ def lsu_bound_from_profile(kernel_s: float, edges: int) -> dict | None:
             "wavefronts_per_32_edges_by_role": parts,
             "ceiling_edges_per_s": ceiling, "achieved_edges_per_s": achieved,
             "frac": achieved / ceiling, "ncu_pct_of_peak": pct,
-            "binding": "co-binding with the integer pipes (DESIGN.md section 5)",
+            "binding": "86 % busy beside issue 65 % / ALU 66 % / FMA-heavy 64 % (DESIGN.md section 5)",
             "source": "profiles/ncu_full_summary.json"}
 
 
