@@ -282,6 +282,15 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 #ifndef RMAT_FASTEND
 #define RMAT_FASTEND 1
 #endif
+#ifndef RMAT_SPEC_LOAD
+#define RMAT_SPEC_LOAD 1  // C3 +0.6 %, C4 +4.5 %
+#endif
+#ifndef RMAT_VOTE_MERGE
+#define RMAT_VOTE_MERGE 1  // with the speculative gathers: C3 +2.2 % (without them it had measured -2.5 %)
+#endif
+#ifndef RMAT_END_IN_SLOW
+#define RMAT_END_IN_SLOW 1  // C3 +0.75 %
+#endif
 #ifndef RMAT_FASTEND_QUICK
 #define RMAT_FASTEND_QUICK 1
 #endif
@@ -1060,30 +1069,35 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     gfastL = gLend - (uint64_t)(4 * CPI + R - 1) * EB;
     return true;
   };
-  for (;;) {
-    if constexpr (FASTEND) {
-      // a stream that ended on the last sector flush: open the next one here,
-      // the warp stays on the fast path
-      if (L == 0) {
-        if (RMAT_FASTEND_QUICK && g.nseg == 1 && s + T + 1 < g.total_streams) {
-          // the next stream is another whole stream of the launch's only
-          // segment: same key, prefixes and length, T streams further on
-          s += T;
-          p.sid += T;
-          p.row += T * g.E;
-          pre = make_pre();
-          j = 0; cur_r = cur_c = 0; f = 0;
-          L = (uint32_t)g.E;
-          roff = rp_init(p.row);
-          half = rp_half(roff);
-          lo = rp_slot(roff) & (G - 1);
-          L += lo;
-          gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
-        } else if (!next_stream()) {
-          break;
-        }
-      }
+  // a FASTEND stream that ended on its last sector flush (L == 0): open the
+  // next one; false when this thread has no stream left
+  auto fastend_switch = [&]() -> bool {
+    if (RMAT_FASTEND_QUICK && g.nseg == 1 && s + T + 1 < g.total_streams) {
+      // the next stream is another whole stream of the launch's only
+      // segment: same key, prefixes and length, T streams further on
+      s += T;
+      p.sid += T;
+      p.row += T * g.E;
+      pre = make_pre();
+      j = 0; cur_r = cur_c = 0; f = 0;
+      L = (uint32_t)g.E;
+      roff = rp_init(p.row);
+      half = rp_half(roff);
+      lo = rp_slot(roff) & (G - 1);
+      L += lo;
+      gptr = reinterpret_cast<char*>(g.out) + (p.row & ~(uint64_t)(G - 1)) * EB;
+    } else if (!next_stream()) {
+      return false;
     }
+    return true;
+  };
+  for (;;) {
+    // RMAT_END_IN_SLOW: the L == 0 test sits behind the failed fast-path vote
+    // (such a lane fails it) instead of at the top of every iteration
+    if constexpr (FASTEND && !RMAT_END_IN_SLOW) {
+      if (L == 0 && !fastend_switch()) break;
+    }
+    bool deep_iter = false;  // FASTEND: the fast block met a deep unit, run this call carefully
     // Warp-uniform fast path: every lane has >= 4 edges still to produce
     // (L - staged >= L - (R - 1)), so no stream ends during this call and
     // stores need no cap.
@@ -1108,12 +1122,63 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         for (int c = 0; c < CPI; ++c) anytie |= cb[c].tie;
       }
       uint32_t unused = 0;
+      // RMAT_SPEC_LOAD: the fragment gathers are issued on the preliminary
+      // selectors, before the tie vote (a tie repeats them) -- their latency
+      // overlaps the vote and the branch.
+      constexpr bool SPEC = RMAT_SPEC_LOAD && ASPLIT;
+      if constexpr (SPEC) {
+#pragma unroll
+        for (int c = 0; c < CPI; ++c) load_frags(cb[c]);
+      }
+      if constexpr (VU && RMAT_VOTE_MERGE && SPEC) {
+        // one vote for "a tie or a deep unit somewhere" (the depth test runs on
+        // the preliminary selectors; the rare path repeats it after the ties)
+        uint32_t DU[CPI][2];
+        auto unit_depths = [&]() -> bool {
+          bool deep = false;
+#pragma unroll
+          for (int c = 0; c < CPI; ++c) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              DU[c][u] = dp4a_acc(cb[c].b[2 * u], cb[c].sel[2 * u], dp4a_u(cb[c].b[2 * u + 1], cb[c].sel[2 * u + 1]));
+              deep |= DU[c][u] > vu_lim;
+            }
+          }
+          return deep;
+        };
+        bool deep = unit_depths();
+        bool per_sample = false;
+        if (__any_sync(0xFFFFFFFFu, anytie || deep)) {
+#pragma unroll
+          for (int c = 0; c < CPI; ++c) resolve_ties(cb[c], j + c);
+#pragma unroll
+          for (int c = 0; c < CPI; ++c) load_frags(cb[c]);
+          deep = unit_depths();
+          per_sample = __any_sync(0xFFFFFFFFu, deep);
+        }
+        if (!per_sample) {
+#pragma unroll
+          for (int c = 0; c < CPI; ++c) {
+            step_unit(cb[c], 0, 1, DU[c][0]);
+            step_unit(cb[c], 2, 3, DU[c][1]);
+            if (!(RMAT_VU_FLUSH_ITER && 2 * CPI <= (int)G) || c == CPI - 1) unit_flush();
+          }
+          j += CPI;
+          continue;
+        }
+      } else {
       if (__any_sync(0xFFFFFFFFu, anytie)) {
 #pragma unroll
         for (int c = 0; c < CPI; ++c) resolve_ties(cb[c], j + c);
-      }
+        if constexpr (SPEC) {
 #pragma unroll
-      for (int c = 0; c < CPI; ++c) load_frags(cb[c]);
+          for (int c = 0; c < CPI; ++c) load_frags(cb[c]);
+        }
+      }
+      if constexpr (!SPEC) {
+#pragma unroll
+        for (int c = 0; c < CPI; ++c) load_frags(cb[c]);
+      }
       if constexpr (VU) {
         // unit depths; a unit deeper than min(k, 31) bits might hold two edge
         // boundaries (f + D >= 2k needs D > k since f < k) or overflow 2^D:
@@ -1142,6 +1207,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
           continue;
         }
       }
+      }
       if constexpr ((RMAT_PROBE & 4) && !REF) {
 #pragma unroll
         for (int c = 0; c < CPI; ++c) probe_acc ^= cb[c].w[0] ^ cb[c].w[1] ^ cb[c].w[2] ^ cb[c].w[3];
@@ -1156,6 +1222,15 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
         continue;
       }
       // (FASTEND: a deep unit somewhere -- this call runs on the careful path below)
+      deep_iter = true;
+    }
+    if constexpr (FASTEND && RMAT_END_IN_SLOW) {
+      if (L == 0) {
+        if (!fastend_switch()) break;
+        continue;
+      }
+      // a lane that could have run fast waits at the vote for the others
+      if (!deep_iter && L >= G) continue;
     }
     if constexpr (LGPTR) L = (uint32_t)((uint64_t)(gLend - gptr) / EB);
     uint32_t left = L - (FASTEND ? min(staged(), L) : staged());
