@@ -519,13 +519,14 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
 #define RMAT_RK_REGS 1
 #endif
 #ifndef RMAT_VU_CPI
-// fast mode, uint32 block streams: two calls per iteration with the round
-// keys read from the constant bank (VU_RKC; with the keys in registers this
-// kernel spills 64 B at 128 registers): C3 +1.9 % over one call (measured)
+// fast mode, uint32 block streams: two calls per iteration, C3 +1.9 % over
+// one call (measured).  Before the split fragment arrays the kernel spilled
+// 64 B at 128 registers with the keys in registers and read them from the
+// constant bank (VU_RKC); the bank-spread kernels still do.
 #define RMAT_VU_CPI 2
 #endif
   uint32_t rk[20];
-  // VU_RKC: the two-call VU fast path reads the round keys from the constant bank
+  // VU_RKC: this two-call VU kernel reads the round keys from the constant bank
 #ifndef RMAT_VU_RKC
 #define RMAT_VU_RKC 0  // keys in registers (116 registers after the split arrays, no spill): C3 +1.5 %
 #endif
