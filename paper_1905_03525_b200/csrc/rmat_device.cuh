@@ -22,11 +22,13 @@ struct SegDev {
 // ---------------------------------------------------------------------------
 // Packed bucket layout (scheme P tables only).  Bucket i is the alias bucket
 // hit by a sample whose word carries i in bits [2, 2+lg):
-//   B[i] = (~T & ~fm) | d_alias << 8 | d_self
+//   B[i] = (T & ~fm) | d_alias << 8 | d_self      (RMAT_B_PLAIN = 0: ~T & ~fm)
 //          T = thr32 clamped to 32 bits (alias forced to self when thr32 == 2^32),
 //          fm = 2^F - 1, F = max(16, lg + 2) fraction bits below the compare
 //   A[i] = both candidate fragments, so one pair of independent loads resolves
-//          the sample without a dependent second lookup:
+//          the sample without a dependent second lookup (the variable-depth
+//          unit kernels re-stage A as split self / alias word arrays and
+//          gather only the chosen fragment: rmat_kernels.cuh RMAT_ASPLIT):
 //          FB=16: uint2 {row_self | row_alias << 16, col_self | col_alias << 16}
 //          FB=32: uint4 {row_self, row_alias, col_self, col_alias}
 //   TLO[i] = T & (4n-1): only read when the fraction's top bits tie T_hi.
