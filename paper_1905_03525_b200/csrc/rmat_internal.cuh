@@ -74,7 +74,7 @@ inline rmat_status launch_packed_t(const rmat_table* t, const rmat::GenLaunch& g
     threads = rmat::kSmemThreads;
     smem = (BANK ? (size_t)t->n * bank_bytes_per_entry(BANK) : t->packed_bytes) +
            (size_t)rmat::kSmemStrideThreads * rmat::kRingBytes;
-    if (RMAT_ASPLIT && VU && !REF && !BANK) {  // split fragment arrays (k_packed ASPLIT)
+    if (RMAT_ASPLIT && VU && (!REF || RMAT_ASPLIT_REF) && !BANK) {  // split fragment arrays (k_packed ASPLIT)
       if (t->n > rmat::kAsplitMaxN) return RMAT_ERR_INVALID;  // (scheme-P tables in shared memory never are)
       smem = rmat::kAsplitAOff + rmat::asplit_bytes(t->n);
     }

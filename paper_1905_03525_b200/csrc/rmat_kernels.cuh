@@ -291,6 +291,10 @@ constexpr bool kCleanAcc = RMAT_CLEAN_ACC != 0;  // u32 untiled: edges need no k
 #ifndef RMAT_END_IN_SLOW
 #define RMAT_END_IN_SLOW 1  // C3 +0.75 %
 #endif
+// RMAT_ASPLIT_REF: the split arrays also for the reference-block unit kernels
+#ifndef RMAT_ASPLIT_REF
+#define RMAT_ASPLIT_REF 1  // reference blocks (C3, thread per block): 7.49 -> 7.59e10 edges/s (+1.3 %)
+#endif
 #ifndef RMAT_FASTEND_QUICK
 #define RMAT_FASTEND_QUICK 1
 #endif
@@ -434,7 +438,7 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
   constexpr uint32_t STRIDE = RingGeo<OUT64, STHREADS>::STRIDE;  // slot-major ring
   // fragment / depth selection by dot products on one byte selector (RMAT_IDP)
   constexpr bool IDPSEL = RMAT_IDP && FB == 16;
-  constexpr bool ASPLIT = RMAT_ASPLIT && VU && !REF && !BANK && SMEM;
+  constexpr bool ASPLIT = RMAT_ASPLIT && VU && (!REF || RMAT_ASPLIT_REF) && !BANK && SMEM;
   extern __shared__ __align__(16) uint8_t smem[];
 
   const uint8_t* baseA;
@@ -756,7 +760,8 @@ k_packed(const PackedTab tab, const __grid_constant__ GenLaunch g) {
     if constexpr (ASPLIT) {
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        cb.fw[t] = *reinterpret_cast<const uint32_t*>(baseA + mad_lo(cb.sel[t], asc, cb.w[t] & idxmask4));
+        cb.fw[t] = *reinterpret_cast<const uint32_t*>(
+            baseA + mad_lo(cb.sel[t], asc, (REF || SG) ? cb.x[t] : (cb.w[t] & idxmask4)));
     }
   };
   auto frag_r = [&](const Batch& cb, int t) -> uint32_t {
